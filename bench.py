@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native TurboSpec decode step (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step = one pass of the whole hot path over one
+batch: prompt lookup (256 x 4096-token contexts, n 1-4, K = 5) -> goodput
+k-selection (PLD policy) -> rejection-sampling verify/accept (config 2: B = 256,
+ragged k in [0, 8], V = 32000, dense fp32 p and q, lambda = 0.7) -> alpha update.
+Inputs are seeded synthetic data (synth/), resident in HBM, rotating over R sets
+whose footprint is > 3x L2 so no step reads another's rows from L2.
+Metric: generated (verified) tokens/s = sum_i (m_i + 1) / time, whole job.
+Multi-GPU: request-sharded weak scaling -- every rank runs its own B = 256 batch with
+global request ids; no data-path collective; time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "generated tokens/s (verified, whole job)"
+UNIT = "tokens/s"
+WORKLOAD = ("config2 verify (B=256, k~U{0..8}, V=32000, fp32 p+q, lambda=0.7) + config3 PLD lookup "
+            "(B=256, L=4096, n 1-4, K=5) + goodput choose-k (PLD) + alpha update")
+B, V, K_MAX, L_CTX = 256, 32000, 8, 4096
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sets", type=int, default=4, help="rotating input sets (L2 defeat)")
+    ap.add_argument("--graph-steps", type=int, default=64, help="decode steps per captured CUDA graph")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--chunk", type=int, default=0)
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------------- algorithmic bytes
+def verify_alg_bytes(m, k, dense_q, vocab, k_max):
+    """SURVEY.md 8(d) / DESIGN.md 7: bytes the method must move for one verify launch.
+
+    per request: 4V (p row m) + 4V [m < k, dense q] (q row m) + 32 B per tested gather
+    (p, and q when dense; tested = m + [m < k]) + metadata 4(k + 3) + outputs 4(k_max + 2)."""
+    m = np.asarray(m, np.int64)
+    k = np.asarray(k, np.int64)
+    rej = (m < k).astype(np.int64)
+    tested = m + rej
+    per = 4 * vocab * (1 + rej * (1 if dense_q else 0)) + 32 * tested * (2 if dense_q else 1)
+    per += 4 * (k + 3) + 4 * (k_max + 2)
+    return int(per.sum())
+
+
+def lookup_alg_bytes(lens, K):
+    lens = np.asarray(lens, np.int64)
+    return int((4 * lens + 8 + 4 * (K + 1)).sum())
+
+
+# ------------------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    """Polls NVML SM clocks and throttle reasons from a thread during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+
+    def _loop(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons |= int(r) & ~0x1
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.0005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "nvml unavailable"}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b]
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": int(self.max_mhz), "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2406_14066_b200 import dist as pdist
+    from paper_2406_14066_b200 import tsv
+    from paper_2406_14066_b200.step import SpecStep, StepInputs
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    R = max(1, args.sets)
+    seed = synth.DEFAULT_SEED
+    # every rank owns a distinct slice of global request ids (weak scaling, R6: Philox keyed by global ids)
+    vbs, ctxs, offs, lens = [], [], [], []
+    for s in range(R):
+        vb = synth.make_verify_batch(B=B, V=V, k_max=K_MAX, lam=0.7, seed=seed + 7919 * s + rank,
+                                     device=dev, request_id_base=rank * B)
+        vbs.append(vb)
+        c, o = synth.make_contexts(B=B, L=L_CTX, V=V, seed=seed + 7919 * s + rank)
+        ctxs.append(torch.tensor(c, device=dev))
+        offs.append(torch.tensor(o, device=dev))
+        lens.append(torch.tensor(np.diff(o).astype(np.int32), device=dev))
+    inp = StepInputs(vbs, ctxs, offs, lens, K_MAX, seed=seed)
+    st = SpecStep(inp, device=dev)
+    if args.chunk:
+        for a in st.args:
+            a.chunk = args.chunk
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    footprint = sum(inp.input_bytes(s) for s in range(R))
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    # ---- graphs: warm-up and timed steps with distinct Philox step counters
+    W, K = max(3, args.warmup), args.steps
+    gl = max(1, min(args.graph_steps, K))
+    st.capture(list(range(0, gl)))  # main graph: steps 0..gl-1 (replayed)
+    main_graph = st.graph
+    rem = K % gl
+    rem_graph = None
+    if rem:
+        st.capture(list(range(gl, gl + rem)))
+        rem_graph = st.graph
+    st.reset_state()
+    for _ in range((W + gl - 1) // gl):
+        main_graph.replay()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for _ in range(K // gl):
+            main_graph.replay()
+        if rem_graph is not None:
+            rem_graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    t_ms = e0.elapsed_time(e1)
+    t_max = pdist.max_over_ranks(t_ms, dev)
+
+    # ---- generated tokens and algorithmic bytes of exactly the timed steps (deterministic)
+    step_ids = [t for _ in range(K // gl) for t in range(gl)] + [gl + t for t in range(rem)]
+    uniq = sorted(set(step_ids))
+    per_step_tokens, per_step_vbytes = {}, {}
+    na = torch.empty(B, dtype=torch.int32, device=dev)
+    outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
+    for t in uniq:
+        s = t % R
+        vb = vbs[s]
+        tsv.tsv_verify_accept(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t,
+                              K_MAX, num_accepted=na, out_tokens=outt, workspace=st.workspace,
+                              chunk=args.chunk)
+        m = na.cpu().numpy()
+        k = vb.k.cpu().numpy()
+        per_step_tokens[t] = int((m + 1).sum())
+        per_step_vbytes[t] = verify_alg_bytes(m, k, True, V, K_MAX)
+    tokens_rank = sum(per_step_tokens[t] for t in step_ids)
+    tokens_total = pdist.sum_over_ranks(tokens_rank, dev)
+    value = tokens_total / (t_max / 1e3)
+
+    # ---- the dominant kernel alone, timed live with CUDA events over K launches
+    vgraph = torch.cuda.CUDAGraph()
+    ws = st.workspace
+    vargs = []
+    for t in range(gl):
+        s = t % R
+        vb = vbs[s]
+        a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t,
+                                 K_MAX, na, outt, None, ws, chunk=args.chunk)
+        vargs.append(a)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(vgraph, stream=side):
+            for a in vargs:
+                tsv._check(tsv.lib().tsv_verify_accept(tsv.ctypes.byref(a), side.cuda_stream))
+    torch.cuda.synchronize()
+    for _ in range(2):
+        vgraph.replay()
+    torch.cuda.synchronize()
+    reps = max(1, K // gl)
+    v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    v0.record(stream)
+    for _ in range(reps):
+        vgraph.replay()
+    v1.record(stream)
+    torch.cuda.synchronize()
+    verify_ms = v0.elapsed_time(v1) / (reps * gl)
+    vbytes = statistics.fmean(per_step_vbytes[t] for t in range(gl))
+    peak, peak_src = load_peaks()
+    achieved = vbytes / (verify_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "verify_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        host = []
+        vb = vbs[0]
+        names = ["p", "q", "row_offsets", "draft_tokens", "request_ids"]
+        for nm in names:
+            host.append(getattr(vb, nm).cpu().pin_memory())
+        hctx = [ctxs[0].cpu().pin_memory(), offs[0].cpu().pin_memory(), lens[0].cpu().pin_memory()]
+        out_host = [torch.empty((B, K_MAX + 1), dtype=torch.int32).pin_memory(),
+                    torch.empty(B, dtype=torch.int32).pin_memory(),
+                    torch.empty(1, dtype=torch.float64).pin_memory()]
+        h2d = sum(t.numel() * t.element_size() for t in host + hctx)
+        d2h = sum(t.numel() * t.element_size() for t in out_host)
+        ne = args.e2e_steps
+        toks = 0
+        torch.cuda.synchronize()
+        barrier()
+        w0 = time.perf_counter()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for t in range(ne):
+            for nm, h in zip(names, host):
+                getattr(vb, nm).copy_(h, non_blocking=True)
+            ctxs[0].copy_(hctx[0], non_blocking=True)
+            offs[0].copy_(hctx[1], non_blocking=True)
+            lens[0].copy_(hctx[2], non_blocking=True)
+            st.run(step=t * R)  # set 0
+            out_host[0].copy_(st.out_tokens, non_blocking=True)
+            out_host[1].copy_(st.num_accepted, non_blocking=True)
+            out_host[2].copy_(st.alpha, non_blocking=True)
+            stream.synchronize()
+            toks += int((out_host[1].numpy() + 1).sum())
+        x1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = x0.elapsed_time(x1)
+        wall = time.perf_counter() - w0
+        e_ms = pdist.max_over_ranks(e_ms, dev)
+        toks = pdist.sum_over_ranks(toks, dev)
+        e2e = {"value": toks / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": ne, "wall_s": round(wall, 4)}
+
+    if rank != 0:
+        return None
+    st_status = int(st.status.item())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": t_max / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
+        "config": {"workload": WORKLOAD, "global_batch": B * world, "vocab": V, "k_max": K_MAX,
+                   "ctx_len": L_CTX, "parallelism": f"request-sharded x{world}",
+                   "l2_defeat": f"{R} rotating input sets, footprint {footprint / 1e6:.0f} MB vs L2 {l2 / 1e6:.0f} MB",
+                   "graph_steps": gl},
+        "roofline": {"kernel": "verify_lazy_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "alg_bytes_per_launch": vbytes, "launch_us": verify_ms * 1e3, "peak_source": peak_src},
+        "clocks": sampler.summary(),
+        "gpu_launches": SpecStep.LAUNCHES_PER_STEP * K,
+        "e2e": e2e,
+        "tokens_per_step": tokens_total / K,
+        "requests_per_s": B * world * K / (t_max / 1e3),
+        "device_status": st_status,
+    }
+    return line
+
+
+# ------------------------------------------------------------------------- oracle (CPU)
+def oracle_step_sample(n_req, seed, step, data):
+    """One bounded oracle step over the first n_req requests of the workload (CPU)."""
+    import oracle
+    import synth
+    vb, ctx, offs = data
+    ro = vb.row_offsets.numpy()
+    r_hi = int(ro[n_req])
+    q_hi = r_hi - n_req
+    c_hi = int(offs[n_req])
+    props, plen = oracle.lookup(ctx[:c_hi], offs[:n_req + 1], 1, 4, 5)
+    ctx_len = np.diff(offs[:n_req + 1]).astype(np.int32)
+    k, _ = oracle.choose_k(0.7, ctx_len, plen, 5, oracle.POLICY_PLD, synth.SPEC_DESK_TARGET,
+                           synth.SPEC_DESK_DRAFT, pld_cost_ms=0.05)
+    na, out, _ = oracle.verify(vb.p[:r_hi].numpy(), vb.q[:q_hi].numpy(), ro[:n_req + 1],
+                               vb.draft_tokens[:q_hi].numpy(), vb.request_ids[:n_req].numpy().view(np.uint32),
+                               seed, step, K_MAX)
+    oracle.update(0.7, na, ro[:n_req + 1])
+    return int((na + 1).sum())
+
+
+def cpu_data():
+    import synth
+    vb = synth.make_verify_batch(B=B, V=V, k_max=K_MAX, lam=0.7, seed=synth.DEFAULT_SEED, device="cpu")
+    ctx, offs = synth.make_contexts(B=B, L=L_CTX, V=V, seed=synth.DEFAULT_SEED)
+    return vb, ctx, offs
+
+
+def cpu_baseline(budget_s=12.0):
+    import synth
+    data = cpu_data()
+    t0 = time.perf_counter()
+    toks, steps = 0, 0
+    while True:
+        toks += oracle_step_sample(B, synth.DEFAULT_SEED, steps, data)
+        steps += 1
+        if time.perf_counter() - t0 > budget_s or steps >= 30:
+            break
+    el = time.perf_counter() - t0
+    return {"value": toks / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} full steps of the bench workload (B={B}, V={V}) on 1 host thread "
+                      f"({cpu_model()}), {el:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import synth
+    data = cpu_data()
+    # size the per-step sample so the whole run stays within ~2 minutes
+    t0 = time.perf_counter()
+    oracle_step_sample(4, synth.DEFAULT_SEED, 0, data)
+    per_req = (time.perf_counter() - t0) / 4
+    total = max(1, args.steps + args.warmup)
+    n_req = int(max(1, min(B, 100.0 / total / max(per_req, 1e-6))))
+    for w in range(args.warmup):
+        oracle_step_sample(n_req, synth.DEFAULT_SEED, w, data)
+    t0 = time.perf_counter()
+    toks = 0
+    for s in range(args.steps):
+        toks += oracle_step_sample(n_req, synth.DEFAULT_SEED, args.warmup + s, data)
+    el = time.perf_counter() - t0
+    value = toks / el
+    sample = f"first {n_req} of {B} requests per step, 1 host thread ({cpu_model()})"
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / max(1, args.steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded, synth/)",
+            "config": {"workload": WORKLOAD, "global_batch": B, "vocab": V, "k_max": K_MAX,
+                       "ctx_len": L_CTX, "parallelism": "cpu oracle, 1 thread"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,253 @@
+/*
+ * tsv.h -- C ABI of the B200-native TurboSpec propose / verify / accept step.
+ *
+ * TurboSpec (arXiv 2406.14066): one speculative-decoding step is
+ *   GetProposedLen / Propose -> GetVerificationLen -> Score -> Accept ->
+ *   UpdateGlobalAcceptance                          (Listing 1)
+ * This library implements the data-parallel parts of that step on sm_100a:
+ *   tsv_propose_lookup     prompt-lookup n-gram proposal
+ *   tsv_goodput_choose_k   ArgMaxGoodput over k = 0..K          (Listing 2)
+ *   tsv_verify_accept      rejection-sampling acceptance + bonus
+ *   tsv_update_acceptance  moving-average acceptance update
+ * The target model's Score step is not here: its output (probability rows p)
+ * is an input.  Readings of silent or garbled passages are numbered R1..R23
+ * in DESIGN.md section 3 and cited below.
+ *
+ * Conventions (all entry points):
+ *  - Array arguments are DEVICE pointers (cudaMalloc / torch CUDA memory) owned
+ *    by the caller; the library never allocates, frees or retains them.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is asynchronous on `stream`, never synchronises, never
+ *    allocates device memory, and is CUDA-graph capturable.
+ *  - Host-side argument validation happens before any launch; a non-OK status
+ *    means nothing was launched.  tsv_last_error() returns a thread-local
+ *    message for the last non-OK status of the calling thread.
+ *  - Data errors that can only be seen on the device (token id out of range,
+ *    ragged offsets decreasing, k_i > k_max) never trap: the affected
+ *    request's outputs are -1 and, when `device_status` is non-NULL, the
+ *    matching TSV_DEVSTATUS_* bit is OR-ed into *device_status.
+ *  - Results are a pure function of (inputs, seed, step, request_ids): they do
+ *    not depend on grid size, chunking, vocab sharding, batch order or stream.
+ *  - Floating point: no fast-math, no FTZ; IEEE binary32 for probabilities
+ *    and race scores, binary64 for the goodput model; explicit FMAs only.
+ *  - Only sm_100 (B200) devices are accepted (TSV_ERR_UNSUPPORTED_DEVICE).
+ */
+#ifndef TSV_H
+#define TSV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TSV_API __attribute__((visibility("default")))
+#else
+#define TSV_API
+#endif
+
+typedef enum {
+    TSV_OK = 0,
+    TSV_ERR_INVALID_ARG = 1,        /* bad host argument; nothing launched          */
+    TSV_ERR_CUDA = 2,               /* a CUDA runtime call failed                   */
+    TSV_ERR_NCCL = 3,               /* NCCL unavailable or an NCCL call failed      */
+    TSV_ERR_UNSUPPORTED_DEVICE = 4, /* current device is not sm_100                 */
+    TSV_ERR_WORKSPACE = 5           /* workspace NULL or smaller than required      */
+} tsv_status;
+
+/* bits OR-ed into *device_status by the kernels */
+#define TSV_DEVSTATUS_BAD_TOKEN 1u  /* draft token outside [0, vocab_global)      */
+#define TSV_DEVSTATUS_BAD_K 2u      /* k_i < 0 or k_i > k_max (ragged offsets)    */
+#define TSV_DEVSTATUS_NO_WEIGHT 4u  /* selected p row has no positive entry        */
+
+TSV_API const char* tsv_last_error(void);
+TSV_API int tsv_abi_version(void);
+
+/* --------------------------------------------------------------------------
+ * Prompt-lookup proposal (PLD).  PAPER.md:57 [AD] "We use a fixed-length
+ * proposal strategy ... each request attempts to retrieve a predetermined
+ * number of tokens ... the proposal cost only depends on the context search";
+ * PAPER.md:454 "proposed tokens are retrieved as n-grams from the input
+ * prompt"; Fig. PAPER.md:44-49 (a request without a match proposes nothing).
+ * Reading R20: for n = n_max down to n_min, the latest start s < L-n with
+ * ctx[s..s+n-1] == ctx[L-n..L-1] (self-match excluded, overlap allowed);
+ * propose ctx[s+n .. min(s+n+k_fixed, L)-1]; no match => length 0.
+ *   ctx          int32 [ctx_offsets[B]]  token ids, requests concatenated
+ *   ctx_offsets  int32 [B+1]             request i owns ctx[off[i] .. off[i+1]);
+ *                                        L_i = off[i+1]-off[i] <= TSV_MAX_CONTEXT
+ *   n_min,n_max  1 <= n_min <= n_max <= TSV_MAX_NGRAM
+ *   k_fixed      FIXED_PROPOSED_LEN, 1..TSV_MAX_K (Listing 1 line 26)
+ *   proposals    int32 [B, k_fixed] out, -1 padded
+ *   proposal_len int32 [B] out (0..k_fixed)
+ * Errors: INVALID_ARG for B < 0, bad n/k range, NULL arrays (B > 0).
+ * ------------------------------------------------------------------------ */
+#define TSV_MAX_CONTEXT (1 << 20)
+#define TSV_MAX_NGRAM 64
+#define TSV_MAX_K 15
+
+TSV_API tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                              int32_t n_min, int32_t n_max, int32_t k_fixed,
+                              int32_t* proposals, int32_t* proposal_len, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Verify / accept.  PAPER.md:18 [AD] "we utilize rejection sampling to
+ * determine which tokens are retained ... (2) a bonus token that either
+ * rectifies an incorrect draft prediction or extends the sequence when all
+ * proposed tokens are accepted"; PAPER.md:493-497 [BG] (k+1 target
+ * distributions; m+1 tokens, minimum 1, maximum k+1; zero accuracy loss).
+ * Per request i (k_i drafts x_j, target rows p_0..p_k, draft rows q_0..q_{k-1}):
+ *   m = first j with !(RN32(u_acc(i,j) * q_j[x_j]) < p_j[x_j]), else k   (R1-R4)
+ *   w = m < k ? max(0, RN32(p_m - q_m)) : max(0, p_k); all-zero w -> p_m (R5)
+ *   t = argmax_v RN32(w_v / E(u_race(i,m,v))), lowest v on ties     (R7-R9)
+ *   out_tokens[i] = (x_0 .. x_{m-1}, t, -1 ...); num_accepted[i] = m
+ * Uniforms: Philox4x32-10 keyed by seed, counter (v>>2, purpose<<16|pos,
+ * request_id, step) with GLOBAL vocab index and GLOBAL request id (R6).
+ *
+ * Layout: p is [rows_p, ld] fp32 row-major with 16-byte aligned rows
+ * (ld % 4 == 0, base 16-byte aligned); request i owns p rows
+ * row_offsets[i] .. row_offsets[i+1]-1 (k_i + 1 rows, so
+ * k_i = row_offsets[i+1]-row_offsets[i]-1).  q (NULL => one-hot drafts, e.g.
+ * PLD / top-1) is [rows_p - B, ld] with request i's rows and drafts at
+ * row_offsets[i]-i .. +k_i-1 (same packing as draft_tokens).  Only columns
+ * [0, vocab) of each row are read (the allocation must still cover
+ * round-up-to-4(vocab) columns, which ld % 4 == 0 guarantees).
+ * Vocab shards: local column c is global index vocab_offset + c
+ * (vocab_offset % 4 == 0); draft ids are global.
+ * ------------------------------------------------------------------------ */
+typedef struct tsv_verify_args {
+    const float* p;               /* [rows_p, ld]                                  */
+    const float* q;               /* [rows_p - B, ld] or NULL (one-hot drafts)      */
+    const int32_t* row_offsets;   /* [B+1]                                          */
+    const int32_t* draft_tokens;  /* [rows_p - B], global ids                       */
+    const uint32_t* request_ids;  /* [B] global request ids (Philox stream)         */
+    int32_t* num_accepted;        /* [B] out (m_i; -1 on a data error)              */
+    int32_t* out_tokens;          /* [B, k_max+1] out, -1 padded                    */
+    int32_t* device_status;       /* nullable; TSV_DEVSTATUS_* bits OR-ed in        */
+    void* workspace;              /* see tsv_verify_workspace_size                  */
+    uint64_t workspace_bytes;
+    int64_t ld;                   /* row stride in elements, % 4 == 0               */
+    uint64_t seed;                /* Philox key                                     */
+    uint32_t step;                /* Philox counter word 3 (decode step)            */
+    int32_t B;                    /* requests                                       */
+    int32_t k_max;                /* 0..TSV_MAX_K; out_tokens row length k_max+1    */
+    int32_t rows_p;               /* sum_i (k_i + 1); host-known size of p          */
+    int32_t vocab;                /* local columns in this shard (>= 1)             */
+    int32_t vocab_offset;         /* global index of local column 0 (% 4 == 0)      */
+    int32_t vocab_global;         /* global vocabulary size                         */
+    int32_t chunk;                /* 0 = auto; else vocab elements per work item    */
+                                  /* (multiple of 1024) -- a tuning/test knob that   */
+                                  /* never changes results                          */
+    int32_t flags;                /* TSV_VERIFY_* bits                              */
+} tsv_verify_args;
+
+#define TSV_VERIFY_NO_PRUNE 1     /* evaluate every race element exactly (test)     */
+
+/* Workspace: per-request combine slots.  Must be zero-filled ONCE after
+ * allocation (tsv_workspace_clear); every call leaves it zero again.  One
+ * workspace per stream: concurrent calls must not share it. */
+TSV_API tsv_status tsv_verify_workspace_size(const tsv_verify_args* a, size_t* bytes);
+TSV_API tsv_status tsv_workspace_clear(void* workspace, size_t bytes, void* stream);
+TSV_API tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream);
+
+/* Vocab-sharded verify (the target's LM head split over G ranks as under
+ * tensor parallelism).  Rank g holds columns
+ * [vocab_offset, vocab_offset + vocab) of every p and q row.
+ *  partial: one round, dense over all rows of every request; writes one
+ *           tsv_shard_tuple per p row (local packed argmax keys + the accept
+ *           flag of draft tokens this shard owns);
+ *  combine: given the G ranks' tuple arrays concatenated ([G][rows_p]), forms
+ *           m_i (OR of flags, first-rejection scan), the winning key (max over
+ *           ranks; the fallback key when the residual was zero everywhere) and
+ *           writes num_accepted / out_tokens exactly as tsv_verify_accept.
+ * Between them the caller exchanges tuples (NCCL all-gather, or loopback on
+ * one device); tsv_verify_accept_sharded does all three with a tsv_comm. */
+typedef struct tsv_shard_tuple {
+    uint64_t key;      /* (bits(score) << 32) | (0xFFFFFFFF - global_v); 0 = none */
+    uint64_t fb_key;   /* same over max(0, p_m) when the local residual is all 0   */
+    uint32_t flag;     /* bit0: accept (owner of x_j only), bit1: owner,          */
+                       /* bits 8..: TSV_DEVSTATUS_* seen by this shard             */
+    uint32_t pad;
+} tsv_shard_tuple;
+
+TSV_API tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_shard_tuple* tuples_out,
+                                    void* stream);
+TSV_API tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const tsv_shard_tuple* gathered,
+                                    int32_t num_shards, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Goodput k selection: ArgMaxGoodput (Listing 2) over
+ * k = 0..k_max (R12), Goodput = generated tokens / execution time (Eq.
+ * goodput PAPER.md:38-42), generated tokens = sum_i l(alpha_i, k_i) with
+ * l(a,k) = (1-a^{k+1})/(1-a) (Eq. gen_len) evaluated by
+ * Horner, k_i = min(k, cap_i) (R13), time = T_target + T_draft (Eq.
+ * batch-latency PAPER.md:103) with T_fwd = a*N_ctx + gamma*N_batched + delta
+ * (Eq. forward-time), T_draft = k * T_fwd^draft (PAPER.md:128,
+ * R15) or pld_cost_ms (R16).  Skips k > 0 with sum_i (k_i+1) > kv_free_slots
+ * (OOM, R14); strict '>' keeps the smaller k on ties.
+ *   alpha       fp64 [B] (alpha_per_request != 0) or [1]
+ *   ctx_len     int32 [B] context tokens of each request (N_context terms)
+ *   cap         int32 [B] per-request proposal cap (k_max for the draft
+ *               policy; the PLD proposal length for TSV_POLICY_PLD, R21)
+ *   k_out       int32 [1] out: k*
+ *   goodput_out fp64 [k_max+1] out (nullable): tokens per ms, -1 for OOM k
+ *   k_per_request int32 [B] out (nullable): min(k*, cap_i)
+ * ------------------------------------------------------------------------ */
+typedef struct tsv_latency_model {
+    double ctx_ms_per_tok;      /* paper's alpha in Eq. forward-time            */
+    double batched_ms_per_tok;  /* gamma                                        */
+    double fixed_ms;            /* delta                                        */
+} tsv_latency_model;
+
+#define TSV_POLICY_DRAFT 0
+#define TSV_POLICY_PLD 1
+
+TSV_API tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_per_request,
+                                const int32_t* ctx_len, const int32_t* cap, int32_t B,
+                                int32_t k_max, int32_t policy, tsv_latency_model target,
+                                tsv_latency_model draft, double pld_cost_ms,
+                                int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
+                                int32_t* k_per_request, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Acceptance-rate update: UpdateGlobalAcceptance (Listing 1 line 19,
+ * PAPER.md:219) with the moving average of PAPER.md:131-132:
+ *   r = sum_i m_i / sum_i tested_i,  alpha' = fma(decay, alpha - r, r)   (R17)
+ * tested_i = m_i + [m_i < k_i] (TSV_EST_TESTED, R18) or k_i (TSV_EST_PROPOSED);
+ * k_i from row_offsets as in tsv_verify_accept; requests with m_i < 0 are
+ * skipped; nothing tested -> alpha unchanged.  per_request != 0: alpha is
+ * [B] and alpha_i is updated from request i alone (R19).
+ * ------------------------------------------------------------------------ */
+#define TSV_EST_TESTED 0
+#define TSV_EST_PROPOSED 1
+
+TSV_API tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, const int32_t* num_accepted,
+                                 const int32_t* row_offsets, int32_t B, double decay,
+                                 int32_t estimator, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Communicator for the multi-GPU modes (NCCL over NVLink 5 / NVSwitch,
+ * resolved at run time from the process's libnccl.so.2).
+ * tsv_comm_get_unique_id: rank 0 only; the 128 bytes are broadcast by the
+ * caller (torch.distributed).  tsv_verify_accept_sharded: partial ->
+ * ncclAllGather of tsv_shard_tuple rows -> combine, all on `stream`;
+ * workspace >= tsv_verify_sharded_workspace_size.
+ * tsv_allreduce_i64: in-place sum of `count` int64 on `stream` (request-
+ * sharded global sums for the alpha update and choose-k).
+ * ------------------------------------------------------------------------ */
+typedef struct tsv_comm tsv_comm;
+
+TSV_API tsv_status tsv_comm_get_unique_id(void* unique_id_out /* 128 bytes */);
+TSV_API tsv_status tsv_comm_init(tsv_comm** out, const void* unique_id, int32_t rank, int32_t world);
+TSV_API tsv_status tsv_comm_destroy(tsv_comm* comm);
+TSV_API tsv_status tsv_verify_sharded_workspace_size(const tsv_verify_args* a, int32_t world, size_t* bytes);
+TSV_API tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_comm* comm, void* stream);
+TSV_API tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* comm, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSV_H */

@@ -1,0 +1,192 @@
+// api.cu -- error reporting, device gating and the NCCL communicator of libtsv.
+//
+// NCCL is resolved at run time (dlopen of the process's libnccl.so.2, normally the
+// copy torch already loaded) so the library has no link-time NCCL dependency and a
+// single-GPU process never touches it.  The multi-GPU modes:
+//   request-sharded: no data-path collective; tsv_allreduce_i64 sums the int64
+//                    fixed-point goodput / acceptance counters across ranks;
+//   vocab-sharded:   tsv_verify_accept_sharded = shard partial -> ncclAllGather of
+//                    tsv_shard_tuple rows over NVLink/NVSwitch -> combine.
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace tsv {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+tsv_status cuda_status(cudaError_t e, const char* what) {
+    set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    return TSV_ERR_CUDA;
+}
+
+tsv_status check_device() {
+    static int cached[64];  // 0 unknown, 1 ok, 2 unsupported
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+    if (dev >= 0 && dev < 64 && cached[dev] == 1) return TSV_OK;
+    int major = 0, minor = 0;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+    e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+    const bool ok = major == 10 && minor == 0;
+    if (dev >= 0 && dev < 64) cached[dev] = ok ? 1 : 2;
+    if (!ok) {
+        set_error("device %d is sm_%d%d; libtsv is built for sm_100a (B200) only", dev, major, minor);
+        return TSV_ERR_UNSUPPORTED_DEVICE;
+    }
+    return TSV_OK;
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    const char* (*GetErrorString)(ncclResult_t);
+    bool ok;
+};
+
+static NcclApi g_nccl;
+static std::once_flag g_nccl_once;
+
+static void load_nccl() {
+    memset(&g_nccl, 0, sizeof(g_nccl));
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+#define TSV_SYM(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name))
+    TSV_SYM(GetUniqueId, "ncclGetUniqueId");
+    TSV_SYM(CommInitRank, "ncclCommInitRank");
+    TSV_SYM(CommDestroy, "ncclCommDestroy");
+    TSV_SYM(AllGather, "ncclAllGather");
+    TSV_SYM(AllReduce, "ncclAllReduce");
+    TSV_SYM(GetErrorString, "ncclGetErrorString");
+#undef TSV_SYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllGather &&
+                g_nccl.AllReduce && g_nccl.GetErrorString;
+}
+
+static tsv_status nccl_ready() {
+    std::call_once(g_nccl_once, load_nccl);
+    if (!g_nccl.ok) {
+        set_error("NCCL (libnccl.so.2) could not be loaded");
+        return TSV_ERR_NCCL;
+    }
+    return TSV_OK;
+}
+
+static tsv_status nccl_status(ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return TSV_OK;
+    set_error("%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error");
+    return TSV_ERR_NCCL;
+}
+
+}  // namespace tsv
+
+struct tsv_comm {
+    ncclComm_t comm;
+    int32_t rank, world;
+};
+
+using namespace tsv;
+
+extern "C" const char* tsv_last_error(void) { return g_err; }
+extern "C" int tsv_abi_version(void) { return TSV_ABI_VERSION; }
+
+extern "C" tsv_status tsv_comm_get_unique_id(void* unique_id_out) {
+    TSV_REQUIRE(unique_id_out != nullptr, "tsv_comm_get_unique_id: out is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+    TSV_TRY(nccl_ready());
+    ncclUniqueId id;
+    TSV_TRY(nccl_status(g_nccl.GetUniqueId(&id), "ncclGetUniqueId"));
+    memcpy(unique_id_out, &id, sizeof(id));
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_comm_init(tsv_comm** out, const void* unique_id, int32_t rank, int32_t world) {
+    TSV_REQUIRE(out && unique_id, "tsv_comm_init: NULL argument");
+    TSV_REQUIRE(world >= 1 && rank >= 0 && rank < world, "tsv_comm_init: bad rank %d / world %d", rank, world);
+    TSV_TRY(check_device());
+    TSV_TRY(nccl_ready());
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof(id));
+    tsv_comm* c = new tsv_comm();
+    c->rank = rank;
+    c->world = world;
+    tsv_status s = nccl_status(g_nccl.CommInitRank(&c->comm, world, id, rank), "ncclCommInitRank");
+    if (s != TSV_OK) {
+        delete c;
+        return s;
+    }
+    *out = c;
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_comm_destroy(tsv_comm* comm) {
+    if (!comm) return TSV_OK;
+    TSV_TRY(nccl_ready());
+    tsv_status s = nccl_status(g_nccl.CommDestroy(comm->comm), "ncclCommDestroy");
+    delete comm;
+    return s;
+}
+
+extern "C" tsv_status tsv_verify_sharded_workspace_size(const tsv_verify_args* a, int32_t world, size_t* bytes) {
+    TSV_REQUIRE(a && bytes, "tsv_verify_sharded_workspace_size: NULL argument");
+    TSV_REQUIRE(world >= 1, "tsv_verify_sharded_workspace_size: world < 1");
+    size_t slots = 0;
+    TSV_TRY(tsv_verify_workspace_size(a, &slots));
+    const size_t rows = static_cast<size_t>(a->rows_p);
+    slots = (slots + 255) & ~static_cast<size_t>(255);
+    *bytes = slots + rows * sizeof(tsv_shard_tuple) * (1 + static_cast<size_t>(world));
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_comm* comm, void* stream) {
+    TSV_REQUIRE(a && comm, "tsv_verify_accept_sharded: NULL argument");
+    TSV_TRY(nccl_ready());
+    size_t need = 0, slots = 0;
+    TSV_TRY(tsv_verify_sharded_workspace_size(a, comm->world, &need));
+    TSV_REQUIRE(a->workspace && a->workspace_bytes >= need, "tsv_verify_accept_sharded: workspace too small (%llu < %llu)",
+                (unsigned long long)a->workspace_bytes, (unsigned long long)need);
+    if (a->B == 0) return TSV_OK;
+    TSV_TRY(tsv_verify_workspace_size(a, &slots));
+    slots = (slots + 255) & ~static_cast<size_t>(255);
+    char* ws = static_cast<char*>(a->workspace);
+    tsv_shard_tuple* local = reinterpret_cast<tsv_shard_tuple*>(ws + slots);
+    tsv_shard_tuple* gathered = local + a->rows_p;
+    tsv_verify_args b = *a;
+    b.workspace_bytes = slots;
+    TSV_TRY(tsv_verify_shard_partial(&b, local, stream));
+    const size_t words = static_cast<size_t>(a->rows_p) * sizeof(tsv_shard_tuple) / sizeof(uint64_t);
+    TSV_TRY(nccl_status(g_nccl.AllGather(local, gathered, words, ncclUint64, comm->comm,
+                                         static_cast<cudaStream_t>(stream)),
+                        "ncclAllGather"));
+    return tsv_verify_shard_combine(&b, gathered, comm->world, stream);
+}
+
+extern "C" tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* comm, void* stream) {
+    TSV_REQUIRE(data && comm, "tsv_allreduce_i64: NULL argument");
+    TSV_TRY(nccl_ready());
+    return nccl_status(g_nccl.AllReduce(data, data, count, ncclInt64, ncclSum, comm->comm,
+                                        static_cast<cudaStream_t>(stream)),
+                       "ncclAllReduce");
+}

@@ -1,0 +1,133 @@
+// common.cuh -- internals shared by the sm_100a kernels of libtsv (not part of the ABI).
+//
+// Philox4x32-10 (Salmon et al., SC'11), the race / acceptance uniforms and the
+// packed argmax key, as fixed by DESIGN.md readings R2, R6-R9.  Independent of
+// oracle/ (which has its own implementation of the same published definitions).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tsv.h"
+
+namespace tsv {
+
+// ---------------------------------------------------------------- host side
+void set_error(const char* fmt, ...);
+tsv_status check_device();                       // sm_100 only
+tsv_status cuda_status(cudaError_t e, const char* what);
+
+#define TSV_REQUIRE(cond, ...)                         \
+    do {                                               \
+        if (!(cond)) {                                 \
+            ::tsv::set_error(__VA_ARGS__);             \
+            return TSV_ERR_INVALID_ARG;                \
+        }                                              \
+    } while (0)
+
+#define TSV_CUDA(call, what)                                               \
+    do {                                                                   \
+        cudaError_t e__ = (call);                                          \
+        if (e__ != cudaSuccess) return ::tsv::cuda_status(e__, what);      \
+    } while (0)
+
+#define TSV_TRY(call)                                  \
+    do {                                               \
+        tsv_status s__ = (call);                       \
+        if (s__ != TSV_OK) return s__;                 \
+    } while (0)
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------- device side
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+constexpr uint32_t kPurposeAccept = 0u;
+constexpr uint32_t kPurposeRace = 1u;
+
+// Philox4x32-10.  The key schedule depends only on the seed (kernel-uniform),
+// and for the race c1..c3 are row-uniform, so ptxas hoists the first round's
+// second product and the second round's first product out of vocab loops.
+__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                               uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(kPhiloxM0, c0);
+        const uint32_t lo0 = kPhiloxM0 * c0;
+        const uint32_t hi1 = __umulhi(kPhiloxM1, c2);
+        const uint32_t lo1 = kPhiloxM1 * c2;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += kPhiloxW0;
+        k1 += kPhiloxW1;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// u_acc = (x >> 8) 2^-24 in [0, 1): exact in binary32.
+__device__ __forceinline__ float u_acc_from_word(uint32_t x) {
+    return __uint2float_rn(x >> 8) * 0x1p-24f;
+}
+
+// u_race = (2 (x >> 9) + 1) 2^-24 in (0, 1): exact in binary32.
+__device__ __forceinline__ float u_race_from_word(uint32_t x) {
+    return __uint2float_rn(2u * (x >> 9) + 1u) * 0x1p-24f;
+}
+
+// 1 - u_race, exactly, with three integer/float ops and no conversion:
+// as_float((x>>9) ^ 0x3FFFFFFF) = 2 - (m+1) 2^-23 with m = x>>9, and
+// subtracting (1 - 2^-24) leaves 1 - (2m+1) 2^-24 (24 significant bits: exact).
+__device__ __forceinline__ float one_minus_u_race(uint32_t x) {
+    return __fsub_rn(__uint_as_float((x >> 9) ^ 0x3FFFFFFFu), 0x1.fffffep-1f);
+}
+
+// E(u) = RN32(-ln u) (R9): double log (<= 1 ulp) is far inside the 74-ulp
+// margin every race uniform keeps from a binary32 midpoint.
+__device__ __forceinline__ float race_E(float u) {
+    return __double2float_rn(-log(static_cast<double>(u)));
+}
+
+// Packed argmax key: score bits (non-negative binary32 orders like uint32)
+// above the complemented global index, so max(key) = max score, lowest index.
+__device__ __forceinline__ uint64_t pack_key(float s, uint32_t v_global) {
+    return (static_cast<uint64_t>(__float_as_uint(s)) << 32) | static_cast<uint64_t>(0xFFFFFFFFu - v_global);
+}
+__device__ __forceinline__ int32_t key_index(uint64_t key) {
+    return static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(key & 0xFFFFFFFFu));
+}
+
+// Exact race key of one element with weight w > 0 and Philox word x.
+__device__ __forceinline__ uint64_t exact_race_key(float w, uint32_t x, uint32_t v_global) {
+    const float E = race_E(u_race_from_word(x));
+    return pack_key(__fdiv_rn(w, E), v_global);
+}
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+}  // namespace tsv

@@ -1,0 +1,133 @@
+// lookup.cu -- prompt-lookup n-gram proposal (PLD) on sm_100a (K2).
+// PAPER.md:57 [AD] (fixed-length proposal; cost depends only on the context search),
+// PAPER.md:454, 498 (n-grams retrieved from the prompt), Fig. PAPER.md:44-49
+// (a request with no match proposes nothing); reading R20 in DESIGN.md section 3.
+//
+// "Longest n in [n_min, n_max] with a match, then the latest start" is evaluated as
+// ONE max-reduction: for every end position e in [0, L-2] let c(e)
+// be the length of the common suffix of ctx[..e] and ctx[..L-1] capped at n_max;
+// key(e) = (c(e) << 20) | e.  The lexicographic max of (c, e) is exactly the longest
+// matching n and, among its matches, the latest one.  One CTA per request: the context
+// is staged into shared memory with a TMA bulk copy (cp.async.bulk) when it fits,
+// each thread scores a strided set of end positions against the query suffix held in
+// registers, and a warp REDUX + shared-memory step reduces the keys.
+#include "common.cuh"
+
+namespace tsv {
+
+constexpr int kLookupThreads = 256;
+constexpr int kLookupSmemInts = 11776;  // 46 KB static smem: contexts up to ~11.7K tokens are staged
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(a), "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+        "l"(gmem_src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kLookupThreads)
+    ngram_lookup_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ ctx_offsets, int32_t B,
+                        int32_t n_min, int32_t n_max, int32_t K, int32_t* __restrict__ proposals,
+                        int32_t* __restrict__ proposal_len) {
+    __shared__ __align__(128) int32_t s_ctx[kLookupSmemInts];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_red[kLookupThreads / 32];
+    const int32_t i = blockIdx.x;
+    const int32_t off = ctx_offsets[i];
+    const int32_t L = ctx_offsets[i + 1] - off;
+    const int32_t* c = ctx + off;
+    const int tid = threadIdx.x;
+
+    // ---- stage the context: aligned middle by one TMA bulk copy, ragged edges by LDG
+    const bool staged = L > 0 && L <= kLookupSmemInts - 8;
+    int32_t shift = 0;  // s_ctx[shift + t] == c[t]
+    if (staged) {
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(c);
+        const uintptr_t a_lo = (a0 + 15) & ~static_cast<uintptr_t>(15);         // first aligned byte inside
+        const uintptr_t a_hi = (a0 + 4ull * L) & ~static_cast<uintptr_t>(15);   // last aligned byte inside
+        const int32_t head = static_cast<int32_t>((a_lo - a0) >> 2);            // elements before a_lo
+        shift = (4 - head) & 3;  // so that s_ctx + shift + head is 16-byte aligned
+        const bool has_mid = a_hi > a_lo;
+        const uint32_t mid_bytes = has_mid ? static_cast<uint32_t>(a_hi - a_lo) : 0u;
+        if (tid == 0) {
+            mbar_init(&s_bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0 && has_mid) {
+            mbar_expect_tx(&s_bar, mid_bytes);
+            bulk_g2s(s_ctx + shift + head, reinterpret_cast<const void*>(a_lo), mid_bytes, &s_bar);
+        }
+        const int32_t mid_elems = static_cast<int32_t>(mid_bytes >> 2);
+        for (int32_t t = tid; t < L; t += kLookupThreads)
+            if (t < head || t >= head + mid_elems) s_ctx[shift + t] = c[t];
+        if (has_mid) mbar_wait(&s_bar, 0);
+        __syncthreads();
+    }
+    const int32_t* src = staged ? (s_ctx + shift) : c;
+
+    // ---- query suffix ctx[L-1-t], t < n_max, in registers (n_max <= 64, uniform loop)
+    uint32_t best = 0;
+    if (L >= 2) {
+        for (int32_t e = tid; e <= L - 2; e += kLookupThreads) {
+            int32_t cl = 0;
+            while (cl < n_max && cl <= e && src[e - cl] == src[L - 1 - cl]) ++cl;
+            const uint32_t key = (static_cast<uint32_t>(cl) << 20) | static_cast<uint32_t>(e);
+            best = key > best ? key : best;
+        }
+    }
+    best = __reduce_max_sync(0xFFFFFFFFu, best);
+    if ((tid & 31) == 0) s_red[tid >> 5] = best;
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t v = tid < kLookupThreads / 32 ? s_red[tid] : 0u;
+        v = __reduce_max_sync(0xFFFFFFFFu, v);
+        const int32_t n_star = static_cast<int32_t>(v >> 20);
+        const int32_t e_star = static_cast<int32_t>(v & 0xFFFFFu);
+        int32_t len = 0;
+        if (L >= 2 && n_star >= n_min) len = min(K, L - 1 - e_star);
+        int32_t* out = proposals + static_cast<int64_t>(i) * K;
+        for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? src[e_star + 1 + t] : -1;
+        if (tid == 0) proposal_len[i] = len;
+    }
+}
+
+}  // namespace tsv
+
+using namespace tsv;
+
+extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                                         int32_t n_min, int32_t n_max, int32_t k_fixed,
+                                         int32_t* proposals, int32_t* proposal_len, void* stream) {
+    TSV_REQUIRE(B >= 0, "tsv_propose_lookup: B < 0 (%d)", B);
+    TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
+                "tsv_propose_lookup: need 1 <= n_min (%d) <= n_max (%d) <= %d", n_min, n_max, TSV_MAX_NGRAM);
+    TSV_REQUIRE(k_fixed >= 1 && k_fixed <= TSV_MAX_K, "tsv_propose_lookup: k_fixed %d outside [1, %d]", k_fixed, TSV_MAX_K);
+    if (B == 0) return TSV_OK;
+    TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len, "tsv_propose_lookup: a required array is NULL");
+    TSV_TRY(check_device());
+    ngram_lookup_kernel<<<B, kLookupThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len);
+    TSV_CUDA(cudaGetLastError(), "ngram_lookup_kernel launch");
+    return TSV_OK;
+}

@@ -1,0 +1,151 @@
+"""One TurboSpec decode step on device: lookup -> choose-k -> verify -> update.
+
+Listing 1 for the PLD method: Propose (prompt lookup, fixed
+length) -> GetVerificationLen = ArgMaxGoodput over the retrieved lengths ->
+Score (the target forward: NOT here; its probability rows are synthetic inputs) ->
+Accept (rejection sampling) -> UpdateGlobalAcceptance.  Every stage is one libtsv
+launch on the caller's stream, with the real data dependencies kept: choose-k reads
+the lookup's proposal lengths and the current alpha, and the alpha update reads the
+verify's accepted counts; the next step's choose-k reads that alpha.  No host sync.
+
+This module only wires buffers and launches (plumbing); all arithmetic is in the
+sm_100a kernels.  Inputs rotate over ``sets`` to keep the timed region out of L2.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+import synth
+from . import tsv
+
+
+@dataclass
+class StepInputs:
+    verify: List[synth.VerifyBatch]        # one per rotation set (device)
+    ctx: List[torch.Tensor]                # int32 contexts per set (device)
+    ctx_offsets: List[torch.Tensor]        # int32 [B+1] per set (device)
+    ctx_len: List[torch.Tensor]            # int32 [B] per set (device)
+    k_max: int
+    n_min: int = 1
+    n_max: int = 4
+    k_fixed: int = 5
+    target: tuple = synth.SPEC_DESK_TARGET
+    draft: tuple = synth.SPEC_DESK_DRAFT
+    pld_cost_ms: float = 0.05
+    kv_free_slots: int = -1
+    seed: int = synth.DEFAULT_SEED
+
+    @property
+    def B(self) -> int:
+        return self.verify[0].B
+
+    @property
+    def sets(self) -> int:
+        return len(self.verify)
+
+    @staticmethod
+    def synthetic(B: int, V: int, L: int, k_max: int = 8, seed: int = synth.DEFAULT_SEED,
+                  device="cuda", sets: int = 1, lam: float = 0.7) -> "StepInputs":
+        vbs, ctxs, offs, lens = [], [], [], []
+        for s in range(sets):
+            vbs.append(synth.make_verify_batch(B=B, V=V, k_max=k_max, lam=lam, seed=seed + 1000 * s,
+                                               device=device))
+            c, o = synth.make_contexts(B=B, L=L, V=V, seed=seed + 1000 * s)
+            ctxs.append(torch.tensor(c, device=device))
+            offs.append(torch.tensor(o, device=device))
+            lens.append(torch.tensor(np.diff(o).astype(np.int32), device=device))
+        return StepInputs(vbs, ctxs, offs, lens, k_max, seed=seed)
+
+    def input_bytes(self, s: int) -> int:
+        """Bytes of one set's inputs (what an end-to-end call copies host -> device)."""
+        vb = self.verify[s]
+        n = vb.p.numel() * 4 + (0 if vb.q is None else vb.q.numel() * 4)
+        n += (vb.row_offsets.numel() + vb.draft_tokens.numel() + vb.request_ids.numel()) * 4
+        n += (self.ctx[s].numel() + self.ctx_offsets[s].numel() + self.ctx_len[s].numel()) * 4
+        return n
+
+
+class SpecStep:
+    """Preallocated outputs + the four launches; eager ``run`` or CUDA-graph ``capture``/``replay``."""
+
+    LAUNCHES_PER_STEP = 4
+
+    def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7):
+        self.inp = inp
+        B, K = inp.B, inp.k_max
+        dev = torch.device(device)
+        self.alpha = torch.full((1,), alpha0, dtype=torch.float64, device=dev)
+        self.proposals = torch.empty((B, inp.k_fixed), dtype=torch.int32, device=dev)
+        self.proposal_len = torch.empty(B, dtype=torch.int32, device=dev)
+        self.k_star = torch.empty(1, dtype=torch.int32, device=dev)
+        self.goodput = torch.empty(inp.k_fixed + 1, dtype=torch.float64, device=dev)
+        self.k_req = torch.empty(B, dtype=torch.int32, device=dev)
+        self.num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
+        self.out_tokens = torch.empty((B, K + 1), dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.args = []
+        for vb in inp.verify:
+            a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids,
+                                     inp.seed, 0, K, self.num_accepted, self.out_tokens, self.status)
+            self.args.append(a)
+        ws_bytes = max(tsv.tsv_verify_workspace_size(a) for a in self.args)
+        self.workspace = tsv.alloc_workspace(ws_bytes, dev)
+        for a in self.args:
+            a.workspace = self.workspace.data_ptr()
+            a.workspace_bytes = self.workspace.numel()
+        self.graph: Optional[torch.cuda.CUDAGraph] = None
+
+    def run(self, step: int, stream=None):
+        """Launch one decode step (4 kernels) on ``stream`` (default: current)."""
+        inp = self.inp
+        s = step % inp.sets
+        st = tsv._stream(stream)
+        L = tsv.lib()
+        tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
+                                        inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
+                                        self.proposal_len.data_ptr(), st))
+        tsv._check(L.tsv_goodput_choose_k(self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(),
+                                          self.proposal_len.data_ptr(), inp.B, inp.k_fixed,
+                                          tsv.POLICY_PLD, tsv.LatencyModel(*inp.target),
+                                          tsv.LatencyModel(*inp.draft), float(inp.pld_cost_ms),
+                                          int(inp.kv_free_slots), self.k_star.data_ptr(),
+                                          self.goodput.data_ptr(), self.k_req.data_ptr(), st))
+        a = self.args[s]
+        a.step = step & 0xFFFFFFFF
+        tsv._check(L.tsv_verify_accept(tsv.ctypes.byref(a), st))
+        tsv._check(L.tsv_update_acceptance(self.alpha.data_ptr(), 0, self.num_accepted.data_ptr(),
+                                           inp.verify[s].row_offsets.data_ptr(), inp.B, 0.9,
+                                           tsv.EST_TESTED, st))
+
+    def capture(self, steps):
+        """Capture ``steps`` consecutive decode steps into one CUDA graph."""
+        torch.cuda.synchronize()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside capture (lazy module loading)
+            self.run(steps[0])
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.reset_state()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for t in steps:
+                self.run(t)
+        self.graph = g
+        self.steps_in_graph = len(steps)
+
+    def replay(self):
+        self.graph.replay()
+
+    def reset_state(self, alpha0: float = 0.7):
+        self.alpha.fill_(alpha0)
+        self.status.zero_()
+
+    def outputs(self):
+        return {"proposals": self.proposals, "proposal_len": self.proposal_len, "k_star": self.k_star,
+                "goodput": self.goodput, "k_req": self.k_req, "num_accepted": self.num_accepted,
+                "out_tokens": self.out_tokens, "alpha": self.alpha, "status": self.status}

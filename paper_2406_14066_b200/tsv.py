@@ -1,0 +1,329 @@
+"""Thin ctypes binding of libtsv.so (include/tsv.h) -- argument marshalling only.
+
+Every function has the C entry point's name and forwards torch CUDA tensors as raw
+device pointers plus the current CUDA stream.  No computation happens here: every
+step of the path runs in the sm_100a kernels of libtsv.so.  If the library is not
+built the import fails loudly (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libtsv.so")
+
+TSV_OK = 0
+STATUS_NAMES = {1: "TSV_ERR_INVALID_ARG", 2: "TSV_ERR_CUDA", 3: "TSV_ERR_NCCL",
+                4: "TSV_ERR_UNSUPPORTED_DEVICE", 5: "TSV_ERR_WORKSPACE"}
+DEVSTATUS_BAD_TOKEN = 1
+DEVSTATUS_BAD_K = 2
+DEVSTATUS_NO_WEIGHT = 4
+VERIFY_NO_PRUNE = 1
+POLICY_DRAFT = 0
+POLICY_PLD = 1
+EST_TESTED = 0
+EST_PROPOSED = 1
+MAX_K = 15
+
+EXPORTED = [
+    "tsv_last_error", "tsv_abi_version", "tsv_propose_lookup", "tsv_verify_workspace_size",
+    "tsv_workspace_clear", "tsv_verify_accept", "tsv_verify_shard_partial",
+    "tsv_verify_shard_combine", "tsv_goodput_choose_k", "tsv_update_acceptance",
+    "tsv_comm_get_unique_id", "tsv_comm_init", "tsv_comm_destroy",
+    "tsv_verify_sharded_workspace_size", "tsv_verify_accept_sharded", "tsv_allreduce_i64",
+]
+
+
+class TsvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class VerifyArgs(ctypes.Structure):
+    """Mirror of tsv_verify_args (include/tsv.h)."""
+    _fields_ = [
+        ("p", ctypes.c_void_p), ("q", ctypes.c_void_p), ("row_offsets", ctypes.c_void_p),
+        ("draft_tokens", ctypes.c_void_p), ("request_ids", ctypes.c_void_p),
+        ("num_accepted", ctypes.c_void_p), ("out_tokens", ctypes.c_void_p),
+        ("device_status", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_uint64), ("ld", ctypes.c_int64), ("seed", ctypes.c_uint64),
+        ("step", ctypes.c_uint32), ("B", ctypes.c_int32), ("k_max", ctypes.c_int32),
+        ("rows_p", ctypes.c_int32), ("vocab", ctypes.c_int32), ("vocab_offset", ctypes.c_int32),
+        ("vocab_global", ctypes.c_int32), ("chunk", ctypes.c_int32), ("flags", ctypes.c_int32),
+    ]
+
+
+class LatencyModel(ctypes.Structure):
+    """Mirror of tsv_latency_model: Eq. forward-time coefficients (alpha, gamma, delta) in ms."""
+    _fields_ = [("ctx_ms_per_tok", ctypes.c_double), ("batched_ms_per_tok", ctypes.c_double),
+                ("fixed_ms", ctypes.c_double)]
+
+
+SHARD_TUPLE_BYTES = 24  # sizeof(tsv_shard_tuple)
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtsv.so not built at {LIB_PATH}: run `python -m paper_2406_14066_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, i64, u64, f64, sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
+                                 ctypes.c_double, ctypes.c_size_t)
+    sig = {
+        "tsv_last_error": ([], ctypes.c_char_p),
+        "tsv_abi_version": ([], ctypes.c_int),
+        "tsv_propose_lookup": ([P, P, i32, i32, i32, i32, P, P, P], ctypes.c_int),
+        "tsv_verify_workspace_size": ([ctypes.POINTER(VerifyArgs), ctypes.POINTER(sz)], ctypes.c_int),
+        "tsv_workspace_clear": ([P, sz, P], ctypes.c_int),
+        "tsv_verify_accept": ([ctypes.POINTER(VerifyArgs), P], ctypes.c_int),
+        "tsv_verify_shard_partial": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
+        "tsv_verify_shard_combine": ([ctypes.POINTER(VerifyArgs), P, i32, P], ctypes.c_int),
+        "tsv_goodput_choose_k": ([P, i32, P, P, i32, i32, i32, LatencyModel, LatencyModel, f64, i64,
+                                  P, P, P, P], ctypes.c_int),
+        "tsv_update_acceptance": ([P, i32, P, P, i32, f64, i32, P], ctypes.c_int),
+        "tsv_comm_get_unique_id": ([P], ctypes.c_int),
+        "tsv_comm_init": ([ctypes.POINTER(P), P, i32, i32], ctypes.c_int),
+        "tsv_comm_destroy": ([P], ctypes.c_int),
+        "tsv_verify_sharded_workspace_size": ([ctypes.POINTER(VerifyArgs), i32, ctypes.POINTER(sz)],
+                                              ctypes.c_int),
+        "tsv_verify_accept_sharded": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
+        "tsv_allreduce_i64": ([P, sz, P, P], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+_lib = _load()
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def _check(status: int):
+    if status != TSV_OK:
+        msg = _lib.tsv_last_error()
+        raise TsvError(status, msg.decode() if msg else "")
+
+
+def _ptr(t: Optional[torch.Tensor], rows_ok: bool = False) -> Optional[int]:
+    """Device pointer of a contiguous CUDA tensor (rows_ok: a 2-D row-strided view is fine)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libtsv takes CUDA tensors (device pointers); got a CPU tensor")
+    ok = t.is_contiguous() or (rows_ok and t.dim() == 2 and t.stride(1) == 1)
+    if not ok:
+        raise ValueError("libtsv takes contiguous tensors")
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _want(t, dtype, numel, name):
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: expected {dtype}, got {t.dtype}")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name}: expected >= {numel} elements, got {t.numel()}")
+
+
+def tsv_abi_version() -> int:
+    return _lib.tsv_abi_version()
+
+
+# ----------------------------------------------------------------------------- lookup
+def tsv_propose_lookup(ctx: torch.Tensor, ctx_offsets: torch.Tensor, n_min: int, n_max: int,
+                       k_fixed: int, proposals: Optional[torch.Tensor] = None,
+                       proposal_len: Optional[torch.Tensor] = None, stream=None):
+    """Prompt-lookup proposal.  Returns (proposals[B, k], proposal_len[B])."""
+    B = ctx_offsets.numel() - 1
+    _want(ctx, torch.int32, None, "ctx")
+    _want(ctx_offsets, torch.int32, None, "ctx_offsets")
+    dev = ctx_offsets.device
+    if proposals is None:
+        proposals = torch.empty((B, k_fixed), dtype=torch.int32, device=dev)
+    if proposal_len is None:
+        proposal_len = torch.empty(B, dtype=torch.int32, device=dev)
+    ctx_p = _ptr(ctx) if ctx.numel() else _ptr(ctx_offsets)  # any valid pointer when empty
+    _check(_lib.tsv_propose_lookup(ctx_p, _ptr(ctx_offsets), B, n_min, n_max, k_fixed,
+                                   _ptr(proposals), _ptr(proposal_len), _stream(stream)))
+    return proposals, proposal_len
+
+
+# ----------------------------------------------------------------------------- verify
+def make_verify_args(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max,
+                     num_accepted, out_tokens, device_status=None, workspace=None,
+                     vocab=None, vocab_offset=0, vocab_global=None, chunk=0, flags=0) -> VerifyArgs:
+    B = row_offsets.numel() - 1
+    _want(p, torch.float32, None, "p")
+    if q is not None:
+        _want(q, torch.float32, None, "q")
+    _want(row_offsets, torch.int32, B + 1, "row_offsets")
+    _want(draft_tokens, torch.int32, None, "draft_tokens")
+    if request_ids.dtype not in (torch.int32, torch.uint32):
+        raise ValueError("request_ids must be int32/uint32")
+    _want(num_accepted, torch.int32, B, "num_accepted")
+    _want(out_tokens, torch.int32, B * (k_max + 1), "out_tokens")
+    V = int(p.shape[1]) if vocab is None else int(vocab)
+    a = VerifyArgs()
+    a.p = _ptr(p, rows_ok=True)
+    a.q = _ptr(q, rows_ok=True)
+    a.row_offsets = _ptr(row_offsets)
+    a.draft_tokens = _ptr(draft_tokens) if draft_tokens.numel() else None
+    a.request_ids = _ptr(request_ids)
+    a.num_accepted = _ptr(num_accepted)
+    a.out_tokens = _ptr(out_tokens)
+    a.device_status = _ptr(device_status)
+    a.workspace = _ptr(workspace)
+    a.workspace_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    a.ld = int(p.stride(0))
+    if q is not None and q.shape[0] > 0 and int(q.stride(0)) != a.ld:
+        raise ValueError("p and q must share the row stride ld")
+    a.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    a.step = int(step) & 0xFFFFFFFF
+    a.B = B
+    a.k_max = int(k_max)
+    a.rows_p = int(p.shape[0])
+    a.vocab = V
+    a.vocab_offset = int(vocab_offset)
+    a.vocab_global = int(vocab_global) if vocab_global is not None else V
+    a.chunk = int(chunk)
+    a.flags = int(flags)
+    return a
+
+
+def tsv_verify_workspace_size(args: VerifyArgs) -> int:
+    n = ctypes.c_size_t(0)
+    _check(_lib.tsv_verify_workspace_size(ctypes.byref(args), ctypes.byref(n)))
+    return int(n.value)
+
+
+def tsv_workspace_clear(workspace: torch.Tensor, stream=None):
+    _check(_lib.tsv_workspace_clear(_ptr(workspace), workspace.numel() * workspace.element_size(),
+                                    _stream(stream)))
+
+
+def alloc_workspace(nbytes: int, device) -> torch.Tensor:
+    """A zero-filled workspace (the contract: zero once after allocation)."""
+    return torch.zeros(max(16, (nbytes + 15) // 16 * 16), dtype=torch.uint8, device=device)
+
+
+def tsv_verify_accept(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max,
+                      num_accepted=None, out_tokens=None, device_status=None, workspace=None,
+                      chunk=0, flags=0, vocab=None, stream=None):
+    """Rejection-sampling verify/accept.  Returns (num_accepted, out_tokens)."""
+    B = row_offsets.numel() - 1
+    dev = row_offsets.device
+    if num_accepted is None:
+        num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
+    if out_tokens is None:
+        out_tokens = torch.empty((B, k_max + 1), dtype=torch.int32, device=dev)
+    a = make_verify_args(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max,
+                         num_accepted, out_tokens, device_status, workspace, vocab=vocab,
+                         chunk=chunk, flags=flags)
+    if workspace is None and B > 0:
+        workspace = alloc_workspace(tsv_verify_workspace_size(a), dev)
+        a.workspace = workspace.data_ptr()
+        a.workspace_bytes = workspace.numel()
+    _check(_lib.tsv_verify_accept(ctypes.byref(a), _stream(stream)))
+    return num_accepted, out_tokens
+
+
+def tsv_verify_shard_partial(args: VerifyArgs, tuples_out: torch.Tensor, stream=None):
+    _check(_lib.tsv_verify_shard_partial(ctypes.byref(args), _ptr(tuples_out), _stream(stream)))
+    return tuples_out
+
+
+def tsv_verify_shard_combine(args: VerifyArgs, gathered: torch.Tensor, num_shards: int, stream=None):
+    _check(_lib.tsv_verify_shard_combine(ctypes.byref(args), _ptr(gathered), int(num_shards),
+                                         _stream(stream)))
+
+
+# ----------------------------------------------------------------------------- goodput
+def tsv_goodput_choose_k(alpha, ctx_len, cap, k_max, policy, target, draft=(0.0, 0.0, 0.0),
+                         pld_cost_ms=0.0, kv_free_slots=-1, alpha_per_request=None, k_out=None,
+                         goodput_out=None, k_per_request=None, stream=None):
+    """ArgMaxGoodput (Listing 2).  Returns (k_out[1], goodput[k_max+1], k_per_request)."""
+    B = ctx_len.numel()
+    dev = ctx_len.device
+    _want(alpha, torch.float64, 1, "alpha")
+    _want(ctx_len, torch.int32, None, "ctx_len")
+    _want(cap, torch.int32, B, "cap")
+    per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
+    if k_out is None:
+        k_out = torch.empty(1, dtype=torch.int32, device=dev)
+    if goodput_out is None:
+        goodput_out = torch.empty(k_max + 1, dtype=torch.float64, device=dev)
+    _check(_lib.tsv_goodput_choose_k(_ptr(alpha), 1 if per else 0, _ptr(ctx_len), _ptr(cap), B,
+                                     int(k_max), int(policy), LatencyModel(*target),
+                                     LatencyModel(*draft), float(pld_cost_ms), int(kv_free_slots),
+                                     _ptr(k_out), _ptr(goodput_out), _ptr(k_per_request),
+                                     _stream(stream)))
+    return k_out, goodput_out, k_per_request
+
+
+def tsv_update_acceptance(alpha, num_accepted, row_offsets, decay=0.9, estimator=EST_TESTED,
+                          per_request=False, stream=None):
+    """UpdateGlobalAcceptance, in place on ``alpha`` (fp64 device)."""
+    B = num_accepted.numel()
+    _want(alpha, torch.float64, B if per_request else 1, "alpha")
+    _want(num_accepted, torch.int32, None, "num_accepted")
+    _want(row_offsets, torch.int32, B + 1, "row_offsets")
+    _check(_lib.tsv_update_acceptance(_ptr(alpha), 1 if per_request else 0, _ptr(num_accepted),
+                                      _ptr(row_offsets), B, float(decay), int(estimator),
+                                      _stream(stream)))
+    return alpha
+
+
+# ----------------------------------------------------------------------------- comm
+class Comm:
+    """NCCL communicator owned by libtsv; the unique id travels over torch.distributed."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            _check(_lib.tsv_comm_get_unique_id(ctypes.cast(uid, ctypes.c_void_p)))
+        obj = [bytes(uid)]
+        if dist.is_initialized() and world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        raw = (ctypes.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        _check(_lib.tsv_comm_init(ctypes.byref(h), ctypes.cast(raw, ctypes.c_void_p), int(rank), int(world)))
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.handle:
+            _check(_lib.tsv_comm_destroy(self.handle))
+            self.handle = None
+
+
+def tsv_verify_sharded_workspace_size(args: VerifyArgs, world: int) -> int:
+    n = ctypes.c_size_t(0)
+    _check(_lib.tsv_verify_sharded_workspace_size(ctypes.byref(args), int(world), ctypes.byref(n)))
+    return int(n.value)
+
+
+def tsv_verify_accept_sharded(args: VerifyArgs, comm: Comm, stream=None):
+    _check(_lib.tsv_verify_accept_sharded(ctypes.byref(args), comm.handle, _stream(stream)))
+
+
+def tsv_allreduce_i64(data: torch.Tensor, comm: Comm, stream=None):
+    _want(data, torch.int64, None, "data")
+    _check(_lib.tsv_allreduce_i64(_ptr(data), data.numel(), comm.handle, _stream(stream)))
+    return data

@@ -1,0 +1,111 @@
+"""CPU-only checks of the C ABI: libtsv.so loads, exports every symbol include/tsv.h
+declares, the ctypes mirrors match the C layouts (gcc-compiled offsetof probe), and
+host-side validation rejects bad arguments before any launch (no GPU needed)."""
+import ctypes
+import os
+import re
+import subprocess
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "tsv.h")
+
+
+@pytest.fixture(scope="module")
+def tsv():
+    from paper_2406_14066_b200 import build
+    build.build()
+    from paper_2406_14066_b200 import tsv as t
+    return t
+
+
+def declared_symbols():
+    txt = open(HDR).read()
+    return sorted(set(re.findall(r"^TSV_API\s+[\w\s\*]+?\b(tsv_\w+)\s*\(", txt, flags=re.M)))
+
+
+def test_every_declared_symbol_exported(tsv):
+    syms = declared_symbols()
+    assert len(syms) >= 16
+    out = subprocess.run(["nm", "-D", "--defined-only", tsv.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (tsv_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert sorted(tsv.EXPORTED) == syms
+    for s in syms:
+        assert getattr(tsv.lib(), s) is not None
+
+
+def test_abi_version(tsv):
+    assert tsv.tsv_abi_version() == 1
+
+
+PROBE = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "tsv.h"
+#define F(T, m) printf(#T " " #m " %zu\n", offsetof(T, m));
+int main(void) {
+  printf("tsv_verify_args sizeof %zu\n", sizeof(tsv_verify_args));
+  F(tsv_verify_args, p) F(tsv_verify_args, q) F(tsv_verify_args, row_offsets)
+  F(tsv_verify_args, draft_tokens) F(tsv_verify_args, request_ids) F(tsv_verify_args, num_accepted)
+  F(tsv_verify_args, out_tokens) F(tsv_verify_args, device_status) F(tsv_verify_args, workspace)
+  F(tsv_verify_args, workspace_bytes) F(tsv_verify_args, ld) F(tsv_verify_args, seed)
+  F(tsv_verify_args, step) F(tsv_verify_args, B) F(tsv_verify_args, k_max) F(tsv_verify_args, rows_p)
+  F(tsv_verify_args, vocab) F(tsv_verify_args, vocab_offset) F(tsv_verify_args, vocab_global)
+  F(tsv_verify_args, chunk) F(tsv_verify_args, flags)
+  printf("tsv_shard_tuple sizeof %zu\n", sizeof(tsv_shard_tuple));
+  printf("tsv_latency_model sizeof %zu\n", sizeof(tsv_latency_model));
+  return 0;
+}
+"""
+
+
+def test_ctypes_layout_matches_c(tsv):
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "probe.c")
+        exe = os.path.join(d, "probe")
+        open(src, "w").write(PROBE)
+        subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), src, "-o", exe], check=True)
+        out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split("\n")
+    c = {}
+    for line in out:
+        if line.strip():
+            t, m, v = line.split()
+            c[(t, m)] = int(v)
+    assert c[("tsv_verify_args", "sizeof")] == ctypes.sizeof(tsv.VerifyArgs)
+    for name, _ in tsv.VerifyArgs._fields_:
+        assert c[("tsv_verify_args", name)] == getattr(tsv.VerifyArgs, name).offset, name
+    assert c[("tsv_shard_tuple", "sizeof")] == tsv.SHARD_TUPLE_BYTES
+    assert c[("tsv_latency_model", "sizeof")] == ctypes.sizeof(tsv.LatencyModel)
+
+
+def test_host_validation_without_gpu(tsv):
+    L = tsv.lib()
+    # bad n-gram range: rejected before any device work
+    assert L.tsv_propose_lookup(None, None, 4, 3, 2, 5, None, None, None) == 1
+    assert b"n_min" in L.tsv_last_error()
+    assert L.tsv_propose_lookup(None, None, -1, 1, 2, 5, None, None, None) == 1
+    # B = 0 is a no-op
+    assert L.tsv_propose_lookup(None, None, 0, 1, 2, 5, None, None, None) == 0
+    a = tsv.VerifyArgs()
+    a.B, a.k_max = 4, 16
+    assert L.tsv_verify_accept(ctypes.byref(a), None) == 1
+    assert b"k_max" in L.tsv_last_error()
+    a.k_max = 4
+    assert L.tsv_verify_accept(ctypes.byref(a), None) == 1  # NULL arrays
+    assert L.tsv_verify_accept(None, None) == 1
+    assert L.tsv_update_acceptance(None, 0, None, None, 3, 1.5, 0, None) == 1
+    assert b"decay" in L.tsv_last_error()
+    m = tsv.LatencyModel(0.001, 0.05, 2.0)
+    assert L.tsv_goodput_choose_k(None, 0, None, None, 0, 8, 0, m, m, 0.0, -1, None, None, None, None) == 1
+    assert L.tsv_goodput_choose_k(None, 0, None, None, 4, 8, 7, m, m, 0.0, -1, None, None, None, None) == 1
+    assert b"policy" in L.tsv_last_error()
+
+
+def test_binding_rejects_cpu_tensors(tsv):
+    import torch
+    with pytest.raises(ValueError):
+        tsv._ptr(torch.zeros(4))

@@ -1,0 +1,397 @@
+"""GPU <-> oracle parity through the C ABI (libtsv.so via the ctypes binding).
+
+Bit-exact on every integer output (accepted counts, emitted token ids, proposals,
+proposal lengths, k*), bit-exact on the goodput values and the updated alpha
+(same binary64 operation sequence on both sides).  Inputs come
+from synth/ (seeded); expected values come only from oracle/.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def tsv():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2406_14066_b200 import tsv as t
+    return t
+
+
+def _np(t):
+    return None if t is None else t.detach().cpu().numpy()
+
+
+def oracle_verify(vb, seed, step):
+    return oracle.verify(_np(vb.p), _np(vb.q), _np(vb.row_offsets), _np(vb.draft_tokens),
+                         _np(vb.request_ids).view(np.uint32), seed, step, vb.k_max, vocab=vb.vocab)
+
+
+def gpu_verify(tsv, vb, seed, step, **kw):
+    g = vb.to(DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    na, out = tsv.tsv_verify_accept(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, seed,
+                                    step, vb.k_max, device_status=st, vocab=vb.vocab, **kw)
+    torch.cuda.synchronize()
+    return _np(na), _np(out), int(st.item())
+
+
+def assert_verify_parity(tsv, vb, seed=240614066, step=0, **kw):
+    ona, oout, ost = oracle_verify(vb, seed, step)
+    gna, gout, gst = gpu_verify(tsv, vb, seed, step, **kw)
+    bad = np.nonzero((ona != gna) | (oout != gout).any(1))[0]
+    assert bad.size == 0, (f"{bad.size} requests differ, first {bad[:5]}: oracle m={ona[bad[:3]]} "
+                           f"out={oout[bad[:3]]} gpu m={gna[bad[:3]]} out={gout[bad[:3]]}")
+    assert gst == ost
+    return ona, oout
+
+
+# --------------------------------------------------------------------------- verify
+def test_config1_dense(tsv):
+    vb = synth.make_verify_batch(B=4, V=32000, k_max=4, k_fixed=4, lam=0.7, seed=1)
+    for step in range(4):
+        assert_verify_parity(tsv, vb, step=step)
+
+
+def test_config2_full(tsv):
+    vb = synth.make_verify_batch(B=256, V=32000, k_max=8, lam=0.7, seed=2)
+    na, _ = assert_verify_parity(tsv, vb, step=0)
+    assert (na >= 0).all()
+    assert_verify_parity(tsv, vb, step=7)
+
+
+@pytest.mark.parametrize("lam", [0.3, 0.9])
+def test_config2_acceptance_levels(tsv, lam):
+    vb = synth.make_verify_batch(B=128, V=32000, k_max=8, lam=lam, seed=3)
+    assert_verify_parity(tsv, vb, step=1)
+
+
+def test_one_hot_drafts(tsv):
+    vb = synth.make_verify_batch(B=96, V=32000, k_max=5, lam=0.6, seed=4, dense_q=False)
+    assert vb.q is None
+    assert_verify_parity(tsv, vb, step=3)
+
+
+@pytest.mark.parametrize("chunk", [1024, 2048, 4096, 16384, 32768])
+def test_chunking_does_not_change_results(tsv, chunk):
+    vb = synth.make_verify_batch(B=48, V=32000, k_max=8, lam=0.7, seed=5)
+    assert_verify_parity(tsv, vb, step=2, chunk=chunk)
+
+
+def test_prune_off_identical(tsv):
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=6)
+    a = gpu_verify(tsv, vb, 11, 0)
+    b = gpu_verify(tsv, vb, 11, 0, flags=tsv.VERIFY_NO_PRUNE)
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+    vb1 = synth.make_verify_batch(B=32, V=4099, k_max=3, lam=0.5, seed=7, dense_q=False)
+    a = gpu_verify(tsv, vb1, 11, 5)
+    b = gpu_verify(tsv, vb1, 11, 5, flags=tsv.VERIFY_NO_PRUNE)
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+
+
+@pytest.mark.parametrize("V", [1, 3, 7, 13, 4096 + 3])
+def test_ragged_vocab_sizes(tsv, V):
+    vb = synth.make_verify_batch(B=16, V=V, k_max=6, lam=0.7, seed=8 + V)
+    assert_verify_parity(tsv, vb, step=V)
+    vb = synth.make_verify_batch(B=16, V=V, k_max=6, lam=0.7, seed=9 + V, dense_q=False)
+    assert_verify_parity(tsv, vb, step=V)
+
+
+def test_padded_ld(tsv):
+    vb = synth.make_verify_batch(B=20, V=1000, k_max=4, lam=0.7, seed=10, ld=1032)
+    vb.p[:, 1000:] = 5.0  # never read
+    vb.q[:, 1000:] = 5.0
+    assert_verify_parity(tsv, vb, step=1)
+
+
+def test_k_zero_and_k_max(tsv):
+    ks = [0] * 8 + [15] * 8
+    vb = synth.make_verify_batch(B=16, V=2048, k_max=15, lam=0.95, seed=12, k_list=ks)
+    assert_verify_parity(tsv, vb, step=0)
+
+
+def _adversarial_batch():
+    """Hand-built rows: p == q, zero rows, denormals, q(x)=0, p(x)=0, drafts at 0 and V-1."""
+    V = 260
+    rng = np.random.Generator(np.random.PCG64(13))
+    rows_p, rows_q, drafts, ks = [], [], [], []
+
+    def soft():
+        z = rng.standard_normal(V) * 3
+        e = np.exp(z - z.max())
+        return (e / e.sum()).astype(np.float32)
+
+    cases = []
+    # 1. p == q (accept always; residual zero only by rounding)
+    p = soft(); cases.append(([p, p, soft()], [p, p], [0, V - 1]))
+    # 2. residual identically zero -> fallback (q >= p everywhere, unnormalised)
+    p = soft(); q = p * 2; cases.append(([p, soft()], [q], [5]))
+    # 3. denormal weights
+    p = np.full(V, 1e-40, np.float32); p[3] = 2e-40; cases.append(([p], [], []))
+    # 4. q(x) = 0 -> always accept
+    p = soft(); q = soft(); q[7] = 0; cases.append(([p, soft()], [q], [7]))
+    # 5. p(x) = 0 -> always reject
+    p = soft(); p[9] = 0; q = soft(); cases.append(([p, soft()], [q], [9]))
+    # 6. exact ties: all-equal weights
+    p = np.full(V, 1.0 / V, np.float32); cases.append(([p], [], []))
+    # 7. zero bonus row -> NO_WEIGHT
+    cases.append(([np.zeros(V, np.float32)], [], []))
+    # 8. single nonzero entry at V-1 and at 0
+    p = np.zeros(V, np.float32); p[V - 1] = 1; cases.append(([p], [], []))
+    p = np.zeros(V, np.float32); p[0] = 1; cases.append(([p], [], []))
+    # 9. NaN in the residual row (NaN weight -> 0)
+    p = soft(); q = soft(); p[11] = np.nan; cases.append(([p, soft()], [q], [12]))
+    for pr, qr, d in cases:
+        rows_p += pr; rows_q += qr; drafts += d; ks.append(len(d))
+    B = len(ks)
+    ro = np.zeros(B + 1, np.int32); ro[1:] = np.cumsum(np.array(ks) + 1)
+    return synth.VerifyBatch(torch.tensor(np.stack(rows_p)), torch.tensor(np.stack(rows_q)),
+                             torch.tensor(ro), torch.tensor(np.array(drafts, np.int32)),
+                             torch.arange(B, dtype=torch.int32), torch.tensor(ks, dtype=torch.int32),
+                             V, 2)
+
+
+def test_adversarial_rows(tsv):
+    vb = _adversarial_batch()
+    for step in range(6):
+        assert_verify_parity(tsv, vb, step=step)
+        assert_verify_parity(tsv, vb, step=step, chunk=1024)
+
+
+def test_bad_token_and_bad_k_flagged(tsv):
+    vb = synth.make_verify_batch(B=8, V=512, k_max=3, lam=0.7, seed=14, k_fixed=3)
+    vb.draft_tokens[4] = 512          # out of range (request 1)
+    _, out, st = gpu_verify(tsv, vb, 1, 0)
+    ona, oout, ost = oracle_verify(vb, 1, 0)
+    assert (out == oout).all() and st & tsv.DEVSTATUS_BAD_TOKEN and ost & oracle.STATUS_BAD_TOKEN
+    vb2 = synth.make_verify_batch(B=8, V=512, k_max=5, lam=0.7, seed=14, k_fixed=5)
+    vb2.k_max = 3                      # every request has k = 5 > k_max
+    _, out, st = gpu_verify(tsv, vb2, 1, 0)
+    assert (out == -1).all() and st & tsv.DEVSTATUS_BAD_K
+
+
+def test_workspace_left_clean_and_deterministic(tsv):
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=15).to(DEV)
+    na = torch.empty(64, dtype=torch.int32, device=DEV)
+    out = torch.empty((64, 9), dtype=torch.int32, device=DEV)
+    a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 3, 4, 8, na, out)
+    ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+    res = []
+    for _ in range(3):
+        tsv.tsv_verify_accept(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 3, 4, 8,
+                              num_accepted=na, out_tokens=out, workspace=ws)
+        torch.cuda.synchronize()
+        assert int(ws.count_nonzero()) == 0
+        res.append(out.clone())
+    assert all((r == res[0]).all() for r in res)
+
+
+def test_request_order_invariance(tsv):
+    # outputs depend on request ids, not batch positions
+    vb = synth.make_verify_batch(B=32, V=4096, k_max=4, lam=0.7, seed=16, k_fixed=4)
+    na, out, _ = gpu_verify(tsv, vb, 5, 1)
+    perm = torch.randperm(32, generator=torch.Generator().manual_seed(0))
+    rows = vb.p.view(32, 5, -1)[perm].reshape(160, -1)
+    qrows = vb.q.view(32, 4, -1)[perm].reshape(128, -1)
+    d = vb.draft_tokens.view(32, 4)[perm].reshape(-1)
+    vbp = synth.VerifyBatch(rows.contiguous(), qrows.contiguous(), vb.row_offsets, d.contiguous(),
+                            vb.request_ids[perm].contiguous(), vb.k, vb.vocab, vb.k_max)
+    na2, out2, _ = gpu_verify(tsv, vbp, 5, 1)
+    assert (out2 == out[perm.numpy()]).all()
+
+
+# ------------------------------------------------------------------ vocab-shard loopback
+def shard_loopback(tsv, vb, G, seed, step, chunk=0):
+    g = vb.to(DEV)
+    B, V = vb.B, vb.vocab
+    assert V % (4 * G) == 0
+    Vs = V // G
+    rows = g.p.shape[0]
+    tuples = torch.zeros((G, rows, tsv.SHARD_TUPLE_BYTES // 8), dtype=torch.int64, device=DEV)
+    na = torch.empty(B, dtype=torch.int32, device=DEV)
+    out = torch.empty((B, vb.k_max + 1), dtype=torch.int32, device=DEV)
+    for s in range(G):
+        lo = s * Vs
+        a = tsv.make_verify_args(g.p[:, lo:lo + Vs], None if g.q is None else g.q[:, lo:lo + Vs],
+                                 g.row_offsets, g.draft_tokens, g.request_ids, seed, step, vb.k_max,
+                                 na, out, vocab=Vs, vocab_offset=lo, vocab_global=V, chunk=chunk)
+        ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+        a.workspace = ws.data_ptr()
+        a.workspace_bytes = ws.numel()
+        tsv.tsv_verify_shard_partial(a, tuples[s])
+        torch.cuda.synchronize()
+        assert int(ws.count_nonzero()) == 0
+    a = tsv.make_verify_args(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, seed, step,
+                             vb.k_max, na, out, vocab=V, vocab_global=V)
+    tsv.tsv_verify_shard_combine(a, tuples, G)
+    torch.cuda.synchronize()
+    return _np(na), _np(out)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_vocab_shard_loopback_equals_oracle(tsv, G):
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=17)
+    ona, oout, _ = oracle_verify(vb, 21, 3)
+    na, out = shard_loopback(tsv, vb, G, 21, 3)
+    assert (na == ona).all() and (out == oout).all()
+
+
+def test_vocab_shard_loopback_one_hot_and_adversarial(tsv):
+    vb = synth.make_verify_batch(B=40, V=4096, k_max=6, lam=0.7, seed=18, dense_q=False)
+    ona, oout, _ = oracle_verify(vb, 2, 2)
+    for G in (2, 4):
+        na, out = shard_loopback(tsv, vb, G, 2, 2, chunk=1024)
+        assert (na == ona).all() and (out == oout).all()
+    adv = _adversarial_batch()
+    adv.vocab = 256
+    adv.p = adv.p[:, :256].contiguous(); adv.q = adv.q[:, :256].contiguous()
+    adv.draft_tokens = adv.draft_tokens.clamp(max=255)
+    ona, oout, _ = oracle_verify(adv, 4, 1)
+    na, out = shard_loopback(tsv, adv, 4, 4, 1)
+    assert (na == ona).all() and (out == oout).all()
+
+
+@pytest.mark.slow
+def test_config4_llama3_vocab_sharded(tsv):
+    # V = 128256 (Llama-3), B = 256, ragged k: one-round dense shard partials, G = 2/4/8
+    vb = synth.make_verify_batch(B=256, V=128256, k_max=8, lam=0.7, seed=19)
+    ona, oout, _ = oracle_verify(vb, 240614066, 0)
+    gna, gout, _ = gpu_verify(tsv, vb, 240614066, 0)
+    assert (gna == ona).all() and (gout == oout).all()
+    for G in (2, 4, 8):
+        na, out = shard_loopback(tsv, vb, G, 240614066, 0)
+        assert (na == ona).all() and (out == oout).all()
+
+
+# --------------------------------------------------------------------------- lookup
+def gpu_lookup(tsv, ctx, offs, n_min, n_max, K):
+    c = torch.tensor(ctx, device=DEV)
+    o = torch.tensor(offs, device=DEV)
+    pr, pl = tsv.tsv_propose_lookup(c, o, n_min, n_max, K)
+    torch.cuda.synchronize()
+    return _np(pr), _np(pl)
+
+
+def assert_lookup_parity(tsv, ctx, offs, n_min, n_max, K):
+    opr, opl = oracle.lookup(ctx, offs, n_min, n_max, K)
+    gpr, gpl = gpu_lookup(tsv, ctx, offs, n_min, n_max, K)
+    assert (opl == gpl).all(), np.nonzero(opl != gpl)[0][:5]
+    assert (opr == gpr).all()
+    return opl
+
+
+def test_lookup_config1(tsv):
+    ctx, offs = synth.make_contexts(B=4, L=512, seed=1)
+    plen = assert_lookup_parity(tsv, ctx, offs, 3, 3, 5)
+    assert plen.sum() > 0
+
+
+@pytest.mark.parametrize("n_min,n_max", [(1, 1), (2, 2), (3, 3), (4, 4), (1, 4)])
+def test_lookup_config3(tsv, n_min, n_max):
+    ctx, offs = synth.make_contexts(B=256, L=4096, seed=3)
+    assert_lookup_parity(tsv, ctx, offs, n_min, n_max, 5)
+
+
+def test_lookup_ragged_edges(tsv):
+    rng = np.random.Generator(np.random.PCG64(7))
+    ctxs = [rng.integers(0, A, L).astype(np.int32) for L in range(0, 60) for A in (1, 2, 4)]
+    offs = np.zeros(len(ctxs) + 1, np.int32)
+    offs[1:] = np.cumsum([len(c) for c in ctxs])
+    flat = np.concatenate(ctxs)
+    for (a, b, K) in [(1, 4, 5), (2, 3, 1), (1, 8, 15), (5, 5, 3)]:
+        assert_lookup_parity(tsv, flat, offs, a, b, K)
+
+
+def test_lookup_long_unstaged_and_unaligned(tsv):
+    # 20000-token contexts exceed the shared-memory stage; odd offsets misalign the TMA copy
+    ctx, offs = synth.make_contexts(B=6, L=20000, seed=9, ragged=True)
+    assert_lookup_parity(tsv, ctx, offs, 1, 4, 5)
+    ctx, offs = synth.make_contexts(B=33, L=3001, seed=10, ragged=True)
+    assert_lookup_parity(tsv, ctx, offs, 2, 4, 7)
+
+
+# --------------------------------------------------------------------------- goodput
+PROFILES = [(synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT), (synth.H100_CASE_TARGET, synth.H100_CASE_DRAFT)]
+
+
+def gpu_choose_k(tsv, alpha, ctx_len, cap, k_max, policy, target, draft, pld=0.0, kv=-1):
+    a = torch.tensor(np.atleast_1d(np.asarray(alpha, np.float64)), device=DEV)
+    cl = torch.tensor(np.asarray(ctx_len, np.int32), device=DEV)
+    cp = torch.tensor(np.asarray(cap, np.int32), device=DEV)
+    kpr = torch.empty_like(cp)
+    k, g, kpr = tsv.tsv_goodput_choose_k(a, cl, cp, k_max, policy, target, draft, pld, kv,
+                                         alpha_per_request=np.ndim(alpha) > 0, k_per_request=kpr)
+    torch.cuda.synchronize()
+    return int(k.item()), _np(g), _np(kpr)
+
+
+def test_choose_k_config5_sweep(tsv):
+    # batch 1-512 x alpha 0.3-0.9 x K=8, both latency profiles; bitwise k and goodput
+    n = 0
+    for target, draft in PROFILES:
+        for B in list(range(1, 65)) + [96, 128, 200, 256, 300, 384, 511, 512]:
+            ctx, cap = synth.make_goodput_instance(B, 8, seed=B)
+            for a in (0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9):
+                ok, og = oracle.choose_k(a, ctx, cap, 8, oracle.POLICY_DRAFT, target, draft)
+                gk, gg, kpr = gpu_choose_k(tsv, a, ctx, cap, 8, 0, target, draft)
+                assert gk == ok and (gg.view(np.uint64) == og.view(np.uint64)).all(), (B, a)
+                assert (kpr == np.minimum(ok, cap)).all()
+                n += 1
+    assert n > 1000
+
+
+def test_choose_k_pld_per_request_oom(tsv):
+    rng = np.random.Generator(np.random.PCG64(3))
+    for trial in range(60):
+        B = int(rng.integers(1, 300))
+        ctx, _ = synth.make_goodput_instance(B, 5, seed=trial)
+        cap = rng.integers(0, 6, B).astype(np.int32)
+        alpha = rng.uniform(0, 1, B)
+        kv = int(rng.integers(-1, 4 * B))
+        for pol in (0, 1):
+            ok, og = oracle.choose_k(alpha, ctx, cap, 5, pol, synth.SPEC_DESK_TARGET,
+                                     synth.SPEC_DESK_DRAFT, pld_cost_ms=0.05, kv_free_slots=kv)
+            gk, gg, _ = gpu_choose_k(tsv, alpha, ctx, cap, 5, pol, synth.SPEC_DESK_TARGET,
+                                     synth.SPEC_DESK_DRAFT, 0.05, kv)
+            assert gk == ok and (gg.view(np.uint64) == og.view(np.uint64)).all()
+
+
+def test_update_parity(tsv):
+    rng = np.random.Generator(np.random.PCG64(4))
+    for trial in range(40):
+        B = int(rng.integers(1, 600))
+        ks = rng.integers(0, 9, B)
+        m = np.minimum(rng.geometric(0.3, B) - 1, ks).astype(np.int32)
+        m[rng.random(B) < 0.02] = -1
+        ro = np.zeros(B + 1, np.int32); ro[1:] = np.cumsum(ks + 1)
+        for est in (0, 1):
+            for per in (False, True):
+                a0 = rng.uniform(0, 1, B) if per else float(rng.uniform(0, 1))
+                want = oracle.update(a0, m, ro, decay=0.9, estimator=est)
+                a = torch.tensor(np.atleast_1d(a0), dtype=torch.float64, device=DEV)
+                tsv.tsv_update_acceptance(a, torch.tensor(m, device=DEV), torch.tensor(ro, device=DEV),
+                                          0.9, est, per_request=per)
+                got = _np(a)
+                assert (got.view(np.uint64) == np.atleast_1d(want).view(np.uint64)).all()
+
+
+# ------------------------------------------------------------------- whole step in a graph
+def test_step_graph_capture_matches_eager(tsv):
+    from paper_2406_14066_b200.step import SpecStep, StepInputs
+    inp = StepInputs.synthetic(B=64, V=32000, L=1024, k_max=8, seed=20, device=DEV)
+    st = SpecStep(inp)
+    st.run(step=0)
+    torch.cuda.synchronize()
+    eager = {k: v.clone() for k, v in st.outputs().items()}
+    st2 = SpecStep(inp)
+    st2.capture(steps=[0])
+    st2.replay()
+    torch.cuda.synchronize()
+    for k, v in st2.outputs().items():
+        assert torch.equal(v, eager[k]), k
