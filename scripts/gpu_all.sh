@@ -17,7 +17,7 @@ if [[ "$what" == bench || "$what" == all ]]; then
   tail -c 3000 gpurun_out/bench.json; tail -5 gpurun_out/bench.err
 fi
 if [[ "$what" == ncu || "$what" == all ]]; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"verify|lookup|goodput|update" -c 400 --csv \
       --log-file gpurun_out/launches.csv python bench.py --steps 64 --warmup 3 --graph-steps 8 --sets 4 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_bench.log 2>&1; echo "ncu-launches rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:verify_lazy -s 8 -c 2 \
       -o gpurun_out/verify_full -f python bench.py --steps 16 --warmup 3 --graph-steps 4 --sets 4 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_full.log 2>&1; echo "ncu-full rc=$?"
