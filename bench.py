@@ -167,10 +167,7 @@ def run_ours(args, rank, world, local_rank):
         offs.append(torch.tensor(o, device=dev))
         lens.append(torch.tensor(np.diff(o).astype(np.int32), device=dev))
     inp = StepInputs(vbs, ctxs, offs, lens, K_MAX, seed=seed)
-    st = SpecStep(inp, device=dev)
-    if args.chunk:
-        for a in st.args:
-            a.chunk = args.chunk
+    st = SpecStep(inp, device=dev, chunk=args.chunk)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     footprint = sum(inp.input_bytes(s) for s in range(R))
 
@@ -320,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
                    "ctx_len": L_CTX, "parallelism": f"request-sharded x{world}",
                    "l2_defeat": f"{R} rotating input sets, footprint {footprint / 1e6:.0f} MB vs L2 {l2 / 1e6:.0f} MB",
                    "graph_steps": gl},
-        "roofline": {"kernel": "verify_lazy_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+        "roofline": {"kernel": "tsv_verify_accept (verify_scan + verify_race + verify_emit)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": vbytes, "launch_us": verify_ms * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),

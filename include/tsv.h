@@ -138,16 +138,16 @@ typedef struct tsv_verify_args {
     int32_t vocab;                /* local columns in this shard (>= 1)             */
     int32_t vocab_offset;         /* global index of local column 0 (% 4 == 0)      */
     int32_t vocab_global;         /* global vocabulary size                         */
-    int32_t chunk;                /* 0 = auto; else vocab elements per work item    */
-                                  /* (multiple of 1024) -- a tuning/test knob that   */
-                                  /* never changes results                          */
+    int32_t chunk;                /* 0 = auto (2048); else vocab columns per work    */
+                                  /* item, a multiple of 1024 up to 16384: a tuning */
+                                  /* / test knob that never changes results          */
     int32_t flags;                /* TSV_VERIFY_* bits                              */
 } tsv_verify_args;
 
 #define TSV_VERIFY_NO_PRUNE 1     /* evaluate every race element exactly (test)     */
 
-/* Workspace: per-request combine slots.  Must be zero-filled ONCE after
- * allocation (tsv_workspace_clear); every call leaves it zero again.  One
+/* Workspace: device scratch for per-request scan results and per-chunk race
+ * keys (size from tsv_verify_workspace_size; no initialisation needed).  One
  * workspace per stream: concurrent calls must not share it. */
 TSV_API tsv_status tsv_verify_workspace_size(const tsv_verify_args* a, size_t* bytes);
 TSV_API tsv_status tsv_workspace_clear(void* workspace, size_t bytes, void* stream);

@@ -87,10 +87,11 @@ float oracle_u_acc(uint32_t x)
     return (float)(x >> 8) * 0x1p-24f;
 }
 
-/* Race uniform: odd multiples of 2^-24 in (0, 1), never 0 or 1 (R6). */
+/* Race uniform: odd multiples of 2^-24 in (0, 1), never 0 or 1, from the
+ * low 23 bits of the Philox word (R6/R7). */
 float oracle_u_race(uint32_t x)
 {
-    return (float)(2u * (x >> 9) + 1u) * 0x1p-24f;
+    return (float)(2u * (x & 0x7FFFFFu) + 1u) * 0x1p-24f;
 }
 
 /* E(u) = -ln(u) rounded once to binary32 (R9).  The double log

@@ -74,16 +74,87 @@ __device__ __forceinline__ float u_acc_from_word(uint32_t x) {
     return __uint2float_rn(x >> 8) * 0x1p-24f;
 }
 
-// u_race = (2 (x >> 9) + 1) 2^-24 in (0, 1): exact in binary32.
+// u_race = (2 (x & 0x7FFFFF) + 1) 2^-24 in (0, 1): exact in binary32 (R7).
 __device__ __forceinline__ float u_race_from_word(uint32_t x) {
-    return __uint2float_rn(2u * (x >> 9) + 1u) * 0x1p-24f;
+    return __uint2float_rn(2u * (x & 0x7FFFFFu) + 1u) * 0x1p-24f;
 }
 
-// 1 - u_race, exactly, with three integer/float ops and no conversion:
-// as_float((x>>9) ^ 0x3FFFFFFF) = 2 - (m+1) 2^-23 with m = x>>9, and
+// 1 - u_race, exactly, with one LOP3 and one FADD:
+// as_float((x & 0x7FFFFF) ^ 0x3FFFFFFF) = 2 - (m+1) 2^-23 with m = x & 0x7FFFFF, and
 // subtracting (1 - 2^-24) leaves 1 - (2m+1) 2^-24 (24 significant bits: exact).
 __device__ __forceinline__ float one_minus_u_race(uint32_t x) {
-    return __fsub_rn(__uint_as_float((x >> 9) ^ 0x3FFFFFFFu), 0x1.fffffep-1f);
+    uint32_t b;  // (x & 0x7FFFFF) ^ 0x3FFFFFFF as ONE lop3 (ptxas otherwise emits two)
+    asm("lop3.b32 %0, %1, 0x7FFFFF, %2, 0x6A;" : "=r"(b) : "r"(x), "r"(0x3FFFFFFFu));
+    return __fsub_rn(__uint_as_float(b), 0x1.fffffep-1f);
+}
+
+// 32x32 -> 64-bit product as one IMAD.WIDE.U32: returns lo, writes hi.
+__device__ __forceinline__ uint32_t mulhilo(uint32_t a, uint32_t m, uint32_t& hi) {
+    const unsigned long long p = static_cast<unsigned long long>(a) * m;
+    hi = static_cast<uint32_t>(p >> 32);
+    return static_cast<uint32_t>(p);
+}
+
+// Philox4x32-10 for the race of one row: counter (quad, c1, c2, c3) with c1..c3 fixed
+// for the row.  Rounds 1-3 fold the row-uniform products and xors into constants
+// computed once per row (RaceCtr), leaving 2 + 3 + 4 + 7*4 = 37 ops per quad.
+struct RaceCtr {
+    uint32_t u0, u1;   // round-1 outputs c0', c1' (depend only on c1, c2, k0)
+    uint32_t k1a;      // c3 ^ k1
+    uint32_t k0b;      // u1 ^ (k0 + W0)
+    uint32_t k1b;      // hi(M0 u0) ^ (k1 + W1)
+    uint32_t l0;       // lo(M0 u0)
+    uint32_t k1c;      // l0 ^ (k1 + 2 W1)
+};
+
+__device__ __forceinline__ RaceCtr race_ctr(uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+    RaceCtr r;
+    const uint32_t hi1 = __umulhi(kPhiloxM1, c2), lo1 = kPhiloxM1 * c2;
+    r.u0 = hi1 ^ c1 ^ k0;
+    r.u1 = lo1;
+    r.k1a = c3 ^ k1;
+    const uint32_t H0 = __umulhi(kPhiloxM0, r.u0), L0 = kPhiloxM0 * r.u0;
+    r.k0b = r.u1 ^ (k0 + kPhiloxW0);
+    r.k1b = H0 ^ (k1 + kPhiloxW1);
+    r.l0 = L0;
+    r.k1c = L0 ^ (k1 + 2u * kPhiloxW1);
+    return r;
+}
+
+// ks0[r] = k0 + r W0, ks1[r] = k1 + r W1: the key schedule, precomputed on the host and
+// passed in the kernel parameter block so every xor reads it from the constant bank.
+template <typename KS>
+__device__ __forceinline__ uint4 philox_race(const RaceCtr& r, uint32_t quad, const KS& ks) {
+    uint32_t hi0, hi1;
+    // round 1
+    uint32_t c3 = mulhilo(quad, kPhiloxM0, hi0);
+    uint32_t c2 = hi0 ^ r.k1a;
+    // round 2 (c0 = u0 is row-uniform: its product is r.k1b / r.l0)
+    uint32_t lo1 = mulhilo(c2, kPhiloxM1, hi1);
+    uint32_t c0 = hi1 ^ r.k0b;
+    uint32_t c1 = lo1;
+    c2 = r.k1b ^ c3;
+    // round 3 (its c3 input is r.l0)
+    {
+        const uint32_t lo0 = mulhilo(c0, kPhiloxM0, hi0);
+        lo1 = mulhilo(c2, kPhiloxM1, hi1);
+        c0 = hi1 ^ c1 ^ ks.ks0[2];
+        c1 = lo1;
+        c2 = hi0 ^ r.k1c;
+        c3 = lo0;
+    }
+#pragma unroll
+    for (int rr = 3; rr < 10; ++rr) {
+        const uint32_t lo0 = mulhilo(c0, kPhiloxM0, hi0);
+        lo1 = mulhilo(c2, kPhiloxM1, hi1);
+        const uint32_t n0 = hi1 ^ c1 ^ ks.ks0[rr];
+        const uint32_t n2 = hi0 ^ c3 ^ ks.ks1[rr];
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
 }
 
 // E(u) = RN32(-ln u) (R9): double log (<= 1 ulp) is far inside the 74-ulp
@@ -128,6 +199,38 @@ __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
+}
+
+// ---------------------------------------------------------------- TMA bulk copy + mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {  // spin on try_wait.parity
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(a), "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+        "l"(gmem_src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
 }  // namespace tsv

@@ -15,31 +15,24 @@
 
 namespace tsv {
 
-constexpr int kGpThreads = 512;
+constexpr int kGpThreads = 256;
+constexpr int kGpWarps = kGpThreads / 32;
 constexpr int kGpMaxK = TSV_MAX_K + 1;
 
-__device__ __forceinline__ long long block_sum_i64(long long v, long long* red) {
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    long long t = 0;
-    if (warp == 0) {
-        t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
-        if (lane == 0) red[0] = t;
-    }
-    __syncthreads();
-    return red[0];
+    return v;
 }
 
 __device__ __forceinline__ double fwd_time(const tsv_latency_model& m, double n_ctx, double n_batched) {
     return __fma_rn(m.batched_ms_per_tok, n_batched, __fma_rn(m.ctx_ms_per_tok, n_ctx, m.fixed_ms));
 }
 
+// One CTA.  Each thread accumulates, for every candidate k, the fixed-point token sum
+// L(k) = sum_i rint(2^32 l(alpha_i, min(k, cap_i))) and sum_i min(k, cap_i); one warp
+// reduction + one shared-memory step give the totals; lane k of warp 0 then evaluates
+// T(k) and G(k) in parallel and lane 0 runs Listing 2's strict-'>' scan over k.
 __global__ void __launch_bounds__(kGpThreads)
     goodput_choose_k_kernel(const double* __restrict__ alpha, int32_t alpha_per_request,
                             const int32_t* __restrict__ ctx_len, const int32_t* __restrict__ cap,
@@ -47,17 +40,17 @@ __global__ void __launch_bounds__(kGpThreads)
                             tsv_latency_model draft, double pld_cost_ms, long long kv_free,
                             int32_t* __restrict__ k_out, double* __restrict__ goodput_out,
                             int32_t* __restrict__ k_per_request) {
-    __shared__ long long red[kGpThreads / 32];
-    __shared__ long long s_L[kGpMaxK];
+    __shared__ long long sL[kGpWarps][kGpMaxK];
+    __shared__ long long sN[kGpWarps][kGpMaxK];
+    __shared__ long long sC[kGpWarps][3];
     __shared__ int s_best;
-    long long Lk[kGpMaxK];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long Lk[kGpMaxK], Nk[kGpMaxK];
 #pragma unroll
-    for (int k = 0; k < kGpMaxK; ++k) Lk[k] = 0;
-    long long n_ctx = 0, n_ctx_spec = 0, b_spec = 0, cap_sum[kGpMaxK];
-#pragma unroll
-    for (int k = 0; k < kGpMaxK; ++k) cap_sum[k] = 0;
+    for (int k = 0; k < kGpMaxK; ++k) Lk[k] = Nk[k] = 0;
+    long long n_ctx = 0, n_ctx_spec = 0, b_spec = 0;
     const double a_glob = alpha_per_request ? 0.0 : alpha[0];
-    for (int32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
         const double a = alpha_per_request ? alpha[i] : a_glob;
         const int32_t ci = cap[i];
         const int32_t cl = ctx_len[i];
@@ -66,66 +59,94 @@ __global__ void __launch_bounds__(kGpThreads)
             n_ctx_spec += cl;
             b_spec += 1;
         }
-        double l = 1.0;  // l(a, 0)
-        long long fix_prev = __double2ll_rn(l * 0x1p32);
+        double l = 1.0;  // l(a, 0); Horner step l(a, j+1) = fma(a, l(a, j), 1)
+        long long fix = __double2ll_rn(l * 0x1p32);
         int32_t jcur = 0;
 #pragma unroll
         for (int k = 0; k < kGpMaxK; ++k) {
-            if (k <= k_max) {
-                int32_t ki = k < ci ? k : ci;
-                if (ki < 0) ki = 0;
-                while (jcur < ki) {  // Horner step: l(a, j+1) = fma(a, l(a, j), 1)
-                    l = __fma_rn(a, l, 1.0);
-                    ++jcur;
-                    fix_prev = __double2ll_rn(l * 0x1p32);
-                }
-                Lk[k] += fix_prev;
-                cap_sum[k] += ki;
+            int32_t ki = k < ci ? k : ci;
+            if (ki < 0) ki = 0;
+            while (jcur < ki) {
+                l = __fma_rn(a, l, 1.0);
+                ++jcur;
+                fix = __double2ll_rn(l * 0x1p32);
+            }
+            Lk[k] += fix;
+            Nk[k] += ki;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kGpMaxK; ++k) {
+        if (k <= k_max) {
+            const long long l = warp_sum_i64(Lk[k]);
+            const long long n = warp_sum_i64(Nk[k]);
+            if (lane == 0) {
+                sL[warp][k] = l;
+                sN[warp][k] = n;
             }
         }
     }
-    for (int k = 0; k <= k_max; ++k) {
-        const long long s = block_sum_i64(Lk[k], red);
-        const long long n = block_sum_i64(cap_sum[k], red);
-        if (threadIdx.x == 0) {
-            s_L[k] = s;
-            cap_sum[k] = n;  // thread 0 keeps the totals
-        }
+    n_ctx = warp_sum_i64(n_ctx);
+    n_ctx_spec = warp_sum_i64(n_ctx_spec);
+    b_spec = warp_sum_i64(b_spec);
+    if (lane == 0) {
+        sC[warp][0] = n_ctx;
+        sC[warp][1] = n_ctx_spec;
+        sC[warp][2] = b_spec;
     }
-    n_ctx = block_sum_i64(n_ctx, red);
-    n_ctx_spec = block_sum_i64(n_ctx_spec, red);
-    b_spec = block_sum_i64(b_spec, red);
-    if (threadIdx.x == 0) {
+    __syncthreads();
+    if (warp == 0) {
+        long long c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+        for (int w = 0; w < kGpWarps; ++w) {
+            c0 += sC[w][0];
+            c1 += sC[w][1];
+            c2 += sC[w][2];
+        }
+        double g = -1.0;
+        bool valid = false;
+        if (lane <= k_max) {
+            long long L = 0, N = 0;
+#pragma unroll
+            for (int w = 0; w < kGpWarps; ++w) {
+                L += sL[w][lane];
+                N += sN[w][lane];
+            }
+            const long long n_batched = N + static_cast<long long>(B);
+            if (!(lane > 0 && kv_free >= 0 && n_batched > kv_free)) {  // Listing 2 line 5: OOM -> skip
+                const double t_target = fwd_time(target, static_cast<double>(c0), static_cast<double>(n_batched));
+                double t_draft;
+                if (policy == TSV_POLICY_PLD)
+                    t_draft = pld_cost_ms;
+                else
+                    t_draft = lane > 0 ? __dmul_rn(static_cast<double>(lane),
+                                                   fwd_time(draft, static_cast<double>(c1), static_cast<double>(c2)))
+                                       : 0.0;
+                g = __ddiv_rn(__dmul_rn(static_cast<double>(L), 0x1p-32), __dadd_rn(t_target, t_draft));
+                valid = true;
+            }
+            if (goodput_out) goodput_out[lane] = g;
+        }
+        // Listing 2: max_goodput = -1; for k: if goodput > max_goodput: take k (strict >)
         double max_goodput = -1.0;
         int best_k = 0;
         for (int k = 0; k <= k_max; ++k) {
-            const long long n_batched = cap_sum[k] + static_cast<long long>(B);
-            if (k > 0 && kv_free >= 0 && n_batched > kv_free) {  // Listing 2 line 5: OOM -> continue
-                if (goodput_out) goodput_out[k] = -1.0;
-                continue;
-            }
-            const double t_target = fwd_time(target, static_cast<double>(n_ctx), static_cast<double>(n_batched));
-            double t_draft;
-            if (policy == TSV_POLICY_PLD)
-                t_draft = pld_cost_ms;
-            else
-                t_draft = k > 0 ? __dmul_rn(static_cast<double>(k),
-                                            fwd_time(draft, static_cast<double>(n_ctx_spec), static_cast<double>(b_spec)))
-                                : 0.0;
-            const double g = __ddiv_rn(__dmul_rn(static_cast<double>(s_L[k]), 0x1p-32), __dadd_rn(t_target, t_draft));
-            if (goodput_out) goodput_out[k] = g;
-            if (g > max_goodput) {
-                max_goodput = g;
+            const double gk = __shfl_sync(0xFFFFFFFFu, g, k);
+            const bool vk = __shfl_sync(0xFFFFFFFFu, valid, k);
+            if (vk && gk > max_goodput) {
+                max_goodput = gk;
                 best_k = k;
             }
         }
-        *k_out = best_k;
-        s_best = best_k;
+        if (lane == 0) {
+            *k_out = best_k;
+            s_best = best_k;
+        }
     }
     if (k_per_request) {
         __syncthreads();
         const int32_t kb = s_best;
-        for (int32_t i = threadIdx.x; i < B; i += blockDim.x) {
+        for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
             int32_t ki = kb < cap[i] ? kb : cap[i];
             k_per_request[i] = ki < 0 ? 0 : ki;
         }
@@ -136,9 +157,9 @@ __global__ void __launch_bounds__(kGpThreads)
     update_acceptance_kernel(double* __restrict__ alpha, int32_t per_request,
                              const int32_t* __restrict__ num_accepted, const int32_t* __restrict__ row_offsets,
                              int32_t B, double decay, int32_t estimator) {
-    __shared__ long long red[kGpThreads / 32];
+    __shared__ long long red[kGpWarps][2];
     long long sm = 0, stt = 0;
-    for (int32_t i = threadIdx.x; i < B; i += blockDim.x) {
+    for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
         const int32_t k = row_offsets[i + 1] - row_offsets[i] - 1;
         const int32_t m = num_accepted[i];
         if (m < 0) continue;
@@ -154,11 +175,25 @@ __global__ void __launch_bounds__(kGpThreads)
         }
     }
     if (per_request) return;
-    sm = block_sum_i64(sm, red);
-    stt = block_sum_i64(stt, red);
-    if (threadIdx.x == 0 && stt > 0) {
-        const double r = __ddiv_rn(static_cast<double>(sm), static_cast<double>(stt));
-        alpha[0] = __fma_rn(decay, __dsub_rn(alpha[0], r), r);
+    sm = warp_sum_i64(sm);
+    stt = warp_sum_i64(stt);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red[warp][0] = sm;
+        red[warp][1] = stt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long a = 0, b = 0;
+#pragma unroll
+        for (int w = 0; w < kGpWarps; ++w) {
+            a += red[w][0];
+            b += red[w][1];
+        }
+        if (b > 0) {
+            const double r = __ddiv_rn(static_cast<double>(a), static_cast<double>(b));
+            alpha[0] = __fma_rn(decay, __dsub_rn(alpha[0], r), r);
+        }
     }
 }
 

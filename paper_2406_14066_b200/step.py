@@ -72,9 +72,9 @@ class StepInputs:
 class SpecStep:
     """Preallocated outputs + the four launches; eager ``run`` or CUDA-graph ``capture``/``replay``."""
 
-    LAUNCHES_PER_STEP = 4
+    LAUNCHES_PER_STEP = 6  # lookup, choose-k, verify (scan + race + emit), update
 
-    def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7):
+    def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0):
         self.inp = inp
         B, K = inp.B, inp.k_max
         dev = torch.device(device)
@@ -90,7 +90,8 @@ class SpecStep:
         self.args = []
         for vb in inp.verify:
             a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids,
-                                     inp.seed, 0, K, self.num_accepted, self.out_tokens, self.status)
+                                     inp.seed, 0, K, self.num_accepted, self.out_tokens, self.status,
+                                     chunk=chunk)
             self.args.append(a)
         ws_bytes = max(tsv.tsv_verify_workspace_size(a) for a in self.args)
         self.workspace = tsv.alloc_workspace(ws_bytes, dev)

@@ -37,12 +37,13 @@ def test_u_acc_boundaries():
 
 
 def test_u_race_boundaries():
-    # u_race = (2 (x >> 9) + 1) 2^-24 in (0, 1): never 0 or 1
+    # u_race = (2 (x & 0x7FFFFF) + 1) 2^-24 in (0, 1): never 0 or 1; high 9 bits ignored
     assert oracle.u_race(0) == 2.0 ** -24
-    assert oracle.u_race(511) == 2.0 ** -24
-    assert oracle.u_race(512) == 3 * 2.0 ** -24
+    assert oracle.u_race(0xFF800000) == 2.0 ** -24
+    assert oracle.u_race(1) == 3 * 2.0 ** -24
+    assert oracle.u_race(0x7FFFFF) == 1.0 - 2.0 ** -24
     assert oracle.u_race(0xFFFFFFFF) == 1.0 - 2.0 ** -24
-    assert oracle.u_race(0x80000000) == 0.5 + 2.0 ** -24
+    assert oracle.u_race(0x400000) == 0.5 + 2.0 ** -24
 
 
 def _correctly_rounded_neg_log():
