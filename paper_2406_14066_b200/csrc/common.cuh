@@ -157,8 +157,26 @@ __device__ __forceinline__ uint4 philox_race(const RaceCtr& r, uint32_t quad, co
     return make_uint4(c0, c1, c2, c3);
 }
 
-// E(u) = RN32(-ln u) (R9): double log (<= 1 ulp) is far inside the 74-ulp
-// margin every race uniform keeps from a binary32 midpoint.
+// E(u) = RN32(-ln u) (R9).  Any double evaluation within a few ulp of -ln u rounds to the
+// same binary32 value: every race uniform keeps >= 74 double-ulp from a binary32 midpoint
+// (oracle pin; GPU-checked exhaustively).  Near u = 1 -- where the race's survivors live --
+// -ln u = -log1p(-x), x = 1 - u exact, is summed as x + x^2/2 + ... + x^8/8 by Horner
+// (truncation < x^8/9 relative <= 2^-51 for x < 2^-6); elsewhere the CUDA double log.
+__device__ __forceinline__ float race_E_omu(float omu) {
+    const double x = static_cast<double>(omu);
+    if (omu < 0x1p-6f) {
+        double s = 1.0 / 8.0;
+        s = __fma_rn(s, x, 1.0 / 7.0);
+        s = __fma_rn(s, x, 1.0 / 6.0);
+        s = __fma_rn(s, x, 1.0 / 5.0);
+        s = __fma_rn(s, x, 1.0 / 4.0);
+        s = __fma_rn(s, x, 1.0 / 3.0);
+        s = __fma_rn(s, x, 0.5);
+        s = __fma_rn(s, x, 1.0);
+        return __double2float_rn(__dmul_rn(s, x));
+    }
+    return __double2float_rn(-log(1.0 - x));
+}
 __device__ __forceinline__ float race_E(float u) {
     return __double2float_rn(-log(static_cast<double>(u)));
 }
@@ -174,8 +192,15 @@ __device__ __forceinline__ int32_t key_index(uint64_t key) {
 
 // Exact race key of one element with weight w > 0 and Philox word x.
 __device__ __forceinline__ uint64_t exact_race_key(float w, uint32_t x, uint32_t v_global) {
-    const float E = race_E(u_race_from_word(x));
+    const float E = race_E_omu(one_minus_u_race(x));
     return pack_key(__fdiv_rn(w, E), v_global);
+}
+
+// F = 1 - u + (1 - 2^-24) in [1, 2): the float bits (x & 0x7FFFFF) ^ 0x3FFFFFFF, one LOP3.
+__device__ __forceinline__ float race_F(uint32_t x) {
+    uint32_t b;
+    asm("lop3.b32 %0, %1, 0x7FFFFF, %2, 0x6A;" : "=r"(b) : "r"(x), "r"(0x3FFFFFFFu));
+    return __uint_as_float(b);
 }
 
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
@@ -231,6 +256,29 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
 
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of a step is launched with programmaticStreamSerialization: it may start
+// while its predecessor drains, runs its prologue, and blocks in griddepcontrol.wait
+// before touching data the predecessor produced (full completion + visibility).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 }  // namespace tsv

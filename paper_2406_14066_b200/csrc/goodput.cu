@@ -40,6 +40,8 @@ __global__ void __launch_bounds__(kGpThreads)
                             tsv_latency_model draft, double pld_cost_ms, long long kv_free,
                             int32_t* __restrict__ k_out, double* __restrict__ goodput_out,
                             int32_t* __restrict__ k_per_request) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ long long sL[kGpWarps][kGpMaxK];
     __shared__ long long sN[kGpWarps][kGpMaxK];
     __shared__ long long sC[kGpWarps][3];
@@ -157,6 +159,8 @@ __global__ void __launch_bounds__(kGpThreads)
     update_acceptance_kernel(double* __restrict__ alpha, int32_t per_request,
                              const int32_t* __restrict__ num_accepted, const int32_t* __restrict__ row_offsets,
                              int32_t B, double decay, int32_t estimator) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ long long red[kGpWarps][2];
     long long sm = 0, stt = 0;
     for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
@@ -212,10 +216,10 @@ extern "C" tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_pe
     TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_choose_k: unknown policy %d", policy);
     TSV_REQUIRE(alpha && ctx_len && cap && k_out, "tsv_goodput_choose_k: a required array is NULL");
     TSV_TRY(check_device());
-    goodput_choose_k_kernel<<<1, kGpThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        alpha, alpha_per_request, ctx_len, cap, B, k_max, policy, target, draft, pld_cost_ms,
-        static_cast<long long>(kv_free_slots), k_out, goodput_out, k_per_request);
-    TSV_CUDA(cudaGetLastError(), "goodput_choose_k_kernel launch");
+    TSV_CUDA(launch_pdl(goodput_choose_k_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream),
+                        alpha, alpha_per_request, ctx_len, cap, B, k_max, policy, target, draft, pld_cost_ms,
+                        static_cast<long long>(kv_free_slots), k_out, goodput_out, k_per_request),
+             "goodput_choose_k_kernel launch");
     return TSV_OK;
 }
 
@@ -228,8 +232,8 @@ extern "C" tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, 
     if (B == 0) return TSV_OK;
     TSV_REQUIRE(alpha && num_accepted && row_offsets, "tsv_update_acceptance: a required array is NULL");
     TSV_TRY(check_device());
-    update_acceptance_kernel<<<1, kGpThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        alpha, per_request, num_accepted, row_offsets, B, decay, estimator);
-    TSV_CUDA(cudaGetLastError(), "update_acceptance_kernel launch");
+    TSV_CUDA(launch_pdl(update_acceptance_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream),
+                        alpha, per_request, num_accepted, row_offsets, B, decay, estimator),
+             "update_acceptance_kernel launch");
     return TSV_OK;
 }

@@ -25,6 +25,8 @@ __global__ void __launch_bounds__(kLookupThreads)
     __shared__ __align__(128) int32_t s_ctx[kLookupSmemInts];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_red[kLookupThreads / 32];
+    pdl_wait();
+    pdl_launch_dependents();
     const int32_t i = blockIdx.x;
     const int32_t off = ctx_offsets[i];
     const int32_t L = ctx_offsets[i + 1] - off;
@@ -32,8 +34,8 @@ __global__ void __launch_bounds__(kLookupThreads)
     const int tid = threadIdx.x;
 
     // ---- stage the context: aligned middle by one TMA bulk copy, ragged edges by LDG
-    const bool staged = L > 0 && L <= kLookupSmemInts - 8;
-    int32_t shift = 0;  // s_ctx[shift + t] == c[t]
+    const bool staged = L > 0 && L <= kLookupSmemInts - 8 && (reinterpret_cast<uintptr_t>(ctx) & 15u) == 0;
+    int32_t shift = 0;  // s_ctx[shift + t] == c[t]; shift = off & 3 keeps int4 groups aligned
     if (staged) {
         const uintptr_t a0 = reinterpret_cast<uintptr_t>(c);
         const uintptr_t a_lo = (a0 + 15) & ~static_cast<uintptr_t>(15);         // first aligned byte inside
@@ -52,21 +54,51 @@ __global__ void __launch_bounds__(kLookupThreads)
             bulk_g2s(s_ctx + shift + head, reinterpret_cast<const void*>(a_lo), mid_bytes, &s_bar);
         }
         const int32_t mid_elems = static_cast<int32_t>(mid_bytes >> 2);
-        for (int32_t t = tid; t < L; t += kLookupThreads)
-            if (t < head || t >= head + mid_elems) s_ctx[shift + t] = c[t];
+        const int32_t n_head = min(head, L);              // ragged edges by plain loads
+        const int32_t tail0 = head + mid_elems;
+        if (tid < n_head) s_ctx[shift + tid] = c[tid];
+        if (has_mid && tail0 + tid < L) s_ctx[shift + tail0 + tid] = c[tail0 + tid];
+        if (!has_mid)
+            for (int32_t t = n_head + tid; t < L; t += kLookupThreads) s_ctx[shift + t] = c[t];
         if (has_mid) mbar_wait(&s_bar, 0);
         __syncthreads();
     }
     const int32_t* src = staged ? (s_ctx + shift) : c;
 
-    // ---- query suffix ctx[L-1-t], t < n_max, in registers (n_max <= 64, uniform loop)
+    // ---- key(e) = (min(c(e), n_max) << 20) | e over e in [0, L-2]; c(e) = common suffix
+    // length of ctx[..e] and ctx[..L-1].  Fast path: compare ctx[e] with the last token q0
+    // four positions at a time; only on a hit is the rest of the suffix compared.
     uint32_t best = 0;
     if (L >= 2) {
-        for (int32_t e = tid; e <= L - 2; e += kLookupThreads) {
-            int32_t cl = 0;
+        const int32_t q0 = src[L - 1];
+        auto suffix_key = [&](int32_t e) -> uint32_t {  // ctx[e] == q0 already
+            int32_t cl = 1;
             while (cl < n_max && cl <= e && src[e - cl] == src[L - 1 - cl]) ++cl;
-            const uint32_t key = (static_cast<uint32_t>(cl) << 20) | static_cast<uint32_t>(e);
-            best = key > best ? key : best;
+            return (static_cast<uint32_t>(cl) << 20) | static_cast<uint32_t>(e);
+        };
+        if (staged) {
+            const int4* s4 = reinterpret_cast<const int4*>(s_ctx);
+            const int32_t n_groups = (shift + L - 1 + 3) >> 2;  // smem ints [0, shift + L - 1) hold e <= L-2
+            for (int32_t g = tid; g < n_groups; g += kLookupThreads) {
+                const int4 v = s4[g];
+                const int32_t e0 = 4 * g - shift;
+                const int32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    const int32_t e = e0 + s;
+                    if (vv[s] == q0 && e >= 0 && e <= L - 2) {
+                        const uint32_t key = suffix_key(e);
+                        best = key > best ? key : best;
+                    }
+                }
+            }
+        } else {
+            for (int32_t e = tid; e <= L - 2; e += kLookupThreads) {
+                if (src[e] == q0) {
+                    const uint32_t key = suffix_key(e);
+                    best = key > best ? key : best;
+                }
+            }
         }
     }
     best = __reduce_max_sync(0xFFFFFFFFu, best);
@@ -99,8 +131,8 @@ extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_
     if (B == 0) return TSV_OK;
     TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len, "tsv_propose_lookup: a required array is NULL");
     TSV_TRY(check_device());
-    ngram_lookup_kernel<<<B, kLookupThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len);
-    TSV_CUDA(cudaGetLastError(), "ngram_lookup_kernel launch");
+    TSV_CUDA(launch_pdl(ngram_lookup_kernel, dim3(B), dim3(kLookupThreads), 0, static_cast<cudaStream_t>(stream),
+                        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len),
+             "ngram_lookup_kernel launch");
     return TSV_OK;
 }

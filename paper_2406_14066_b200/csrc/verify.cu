@@ -43,8 +43,8 @@ struct RaceParams {
     int32_t* out_tokens;
     int32_t* devstatus;
     ReqMeta* meta;             // [B]
-    uint64_t* keys;            // [n_key_rows * n_chunks] race keys
-    uint64_t* fbkeys;          // [n_key_rows * n_chunks] fallback keys (valid where key == 0)
+    uint32_t* rowT;            // [n_key_rows] shared race threshold per raced row (float bits)
+    unsigned long long* rowkey;  // [n_key_rows] max race key per raced row (0: nothing evaluated)
     tsv_shard_tuple* tuples;   // shard mode
     int64_t ld;
     uint32_t k0, k1, step;
@@ -60,8 +60,6 @@ constexpr float kPruneC = 0x1.fffffap-1f;        // 1 - 3*2^-24 <= (1-2^-23)(1-2
 constexpr float kLbC = 0x1.ffffe0p-1f;           // 1 - 2^-20
 constexpr float kMinNormal = 0x1p-126f;
 
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Lower bound on the exact score RN32(w / E(u)) of an element:
 // E <= (-ln u)(1+2^-24) <= ((1-u)/u)(1+2^-24), and rcp.approx is within 2^-22.
@@ -74,22 +72,35 @@ __device__ __forceinline__ float prune_scale(float T) {
     return T >= kMinNormal ? __fmul_rd(T, kPruneC) : 0.0f;
 }
 
+struct Race;
+
 // Per-thread race state.  T is warp-uniform: a lower bound on (or an exact value of) a
-// score achieved by an element of this row; Tc = RD(T (1 - 3 2^-24)).
+// score achieved by an element of this row.  Prune test: skipping element
+// (w, u) is safe iff w <= Tc (1 - u) with Tc = RD(T (1 - 3 2^-24)).  With F = 1 - u + K,
+// K = 1 - 2^-24 (race_F, exact), t = RN(Tc F - w) (one FFMA) and Th = RU(Tc (1 + 2^-23)),
+// t >= Th implies Tc F - w >= Th - |t| 2^-24 >= Tc K, i.e. w <= Tc (1 - u): skip.  So an
+// element is a candidate iff t < Th (3 instructions: LOP3, FFMA, FSETP); w <= 0 and NaN
+// never pass the exact step (checked on the rare candidate path).
 struct Race {
-    float T, Tc, Tloc;
+    float T, Tc, Th, Tloc;
     uint64_t best;
     bool has_pend;
     float pend_w, pend_omu;
     uint32_t pend_x, pend_v;
 
     __device__ __forceinline__ void init() {
-        T = Tc = Tloc = 0.0f;
+        T = Tc = Th = Tloc = 0.0f;
         best = 0;
         has_pend = false;
         pend_w = 0.0f;
         pend_omu = 1.0f;
         pend_x = pend_v = 0;
+    }
+
+    __device__ __forceinline__ void set_T(float t) {
+        T = t;
+        Tc = prune_scale(T);
+        Th = __fmul_ru(Tc, 0x1.000002p+0f);
     }
 
     __device__ __forceinline__ void eval_exact(float w, uint32_t x, uint32_t vg) {
@@ -98,7 +109,18 @@ struct Race {
         Tloc = fmaxf(Tloc, __uint_as_float(static_cast<uint32_t>(best >> 32)));
     }
 
-    // One float4 of weights w (0 = not a candidate) with Philox words r, global index v0.
+    // Seed T from lower bounds of one float4 (first step of an item; warp-uniform call).
+    __device__ __forceinline__ void warm(const float (&w)[4], const uint4& r) {
+        const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+        float lb = 0.0f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (w[e] > 0.0f) lb = fmaxf(lb, race_lower_bound(w[e], one_minus_u_race(rw[e])));
+        Tloc = fmaxf(Tloc, lb);
+        sync_T();
+    }
+
+    // One float4 of weights w with Philox words r, global index v0.
     template <bool PRUNE>
     __device__ __forceinline__ void quad(const float (&w)[4], const uint4& r, uint32_t v0) {
         const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
@@ -107,51 +129,32 @@ struct Race {
             for (int e = 0; e < 4; ++e)
                 if (w[e] > 0.0f) eval_exact(w[e], rw[e], v0 + e);
         } else {
-            quad_pruned(w, rw, v0);
-        }
-    }
-
-    __device__ __forceinline__ void quad_pruned(const float (&w)[4], const uint32_t (&rw)[4], uint32_t v0) {
-        float omu[4];
+            bool cand[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) omu[e] = one_minus_u_race(rw[e]);
-        if (T == 0.0f) {  // warp-uniform warm-up: seed T from lower bounds
-            float lb = 0.0f;
+            for (int e = 0; e < 4; ++e) cand[e] = __fmaf_rn(Tc, race_F(rw[e]), -w[e]) < Th;
+            if (cand[0] | cand[1] | cand[2] | cand[3]) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (w[e] > 0.0f) lb = fmaxf(lb, race_lower_bound(w[e], omu[e]));
-            Tloc = fmaxf(Tloc, lb);
-            sync_T();
-        }
-        bool cand[4];
-        bool any = false;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            cand[e] = w[e] > __fmul_rd(Tc, omu[e]);
-            any |= cand[e];
-        }
-        if (any) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                if (cand[e]) {
-                    Tloc = fmaxf(Tloc, race_lower_bound(w[e], omu[e]));
-                    if (has_pend && pend_w > __fmul_rd(Tc, pend_omu)) eval_exact(pend_w, pend_x, pend_v);
-                    has_pend = true;
-                    pend_w = w[e];
-                    pend_omu = omu[e];
-                    pend_x = rw[e];
-                    pend_v = v0 + e;
+                for (int e = 0; e < 4; ++e) {
+                    if (cand[e] && w[e] > 0.0f) {
+                        const float omu = one_minus_u_race(rw[e]);
+                        Tloc = fmaxf(Tloc, race_lower_bound(w[e], omu));
+                        if (has_pend && pend_w > __fmul_rd(Tc, pend_omu)) eval_exact(pend_w, pend_x, pend_v);
+                        has_pend = true;
+                        pend_w = w[e];
+                        pend_omu = omu;
+                        pend_x = rw[e];
+                        pend_v = v0 + e;
+                    }
                 }
             }
         }
     }
 
     __device__ __forceinline__ void sync_T() {  // warp-wide max (REDUX on the float bits)
-        T = __uint_as_float(__reduce_max_sync(0xFFFFFFFFu, __float_as_uint(Tloc)));
-        Tc = prune_scale(T);
+        set_T(__uint_as_float(__reduce_max_sync(0xFFFFFFFFu, __float_as_uint(Tloc))));
     }
 
-    // Flush the parked candidate against a (possibly CTA-wide) final threshold.
+    // Flush the parked candidate against a (possibly shared) final threshold.
     template <bool PRUNE>
     __device__ __forceinline__ void finish(float T_final) {
         if constexpr (PRUNE) {
@@ -162,29 +165,26 @@ struct Race {
     }
 };
 
-// Weights of one float4: residual max(0, p - q) (dense q, or one-hot at local column xm)
-// or bonus max(0, p); columns >= col_end are 0.  NaN -> 0 (fmaxf).
+// Weights of one float4: residual p - q (dense q, or one-hot at local column xm) or bonus
+// p; columns >= col_end are 0.  No max(0, .) clamp: the prune comparison rejects w <= 0
+// and NaN (t < Th fails) and the candidate path re-checks w > 0, so max(0, p - q) of R1 is
+// realised exactly.
 template <bool DENSE_Q>
 __device__ __forceinline__ void quad_weights(float (&w)[4], const float4& a, const float4& b, bool residual,
                                              int32_t col, int32_t col_end, int32_t xm) {
     const float pv[4] = {a.x, a.y, a.z, a.w};
     const float qv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w[e] = pv[e];
     if (residual) {
         if (DENSE_Q) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) w[e] = fmaxf(__fsub_rn(pv[e], qv[e]), 0.0f);
-        } else {
+            for (int e = 0; e < 4; ++e) w[e] = __fsub_rn(pv[e], qv[e]);
+        } else if ((col >> 2) == (xm >> 2)) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) w[e] = fmaxf(pv[e], 0.0f);
-            if ((col >> 2) == (xm >> 2)) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (col + e == xm) w[e] = fmaxf(__fsub_rn(pv[e], 1.0f), 0.0f);
-            }
+            for (int e = 0; e < 4; ++e)
+                if (col + e == xm) w[e] = __fsub_rn(pv[e], 1.0f);
         }
-    } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) w[e] = fmaxf(pv[e], 0.0f);
     }
     if (col + 4 > col_end) {
 #pragma unroll
@@ -218,6 +218,7 @@ __device__ __forceinline__ void emit(const RaceParams& P, int32_t i, int32_t qba
 // Shard: writes the accept / owner flags of every p row of the request into its tuple.
 template <int MODE>
 __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
+    pdl_wait();               // inputs of this step are complete
     pdl_launch_dependents();  // let the race kernel launch and set up while we scan
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= P.B) return;
@@ -252,6 +253,15 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     const uint32_t rej = ~accm & kmask;
     const int32_t m = rej ? (__ffs(rej) - 1) : (ok == 1 ? k : -1);
     const int32_t xm = __shfl_sync(0xFFFFFFFFu, x, (m >= 0 ? m : 0) & 31);
+    if (MODE == kLazy) {
+        if (lane == 0) {
+            P.rowT[i] = 0u;
+            P.rowkey[i] = 0ull;
+        }
+    } else if (ok == 1 && lane <= k) {
+        P.rowT[r0 + lane] = 0u;
+        P.rowkey[r0 + lane] = 0ull;
+    }
     if (lane == 0) {
         ReqMeta rm;
         rm.r0 = r0;
@@ -277,28 +287,31 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
 }
 
 // ------------------------------------------------------------------ 2. the race
-// Warp-independent: every warp races its own work items (request [, position], chunk of
-// P.chunk columns), statically interleaved over all warps of the grid so residual and
-// bonus rows mix on every SM.  Each lane streams float4s of the row chunk straight into
-// registers (LDG.128, L1 no-allocate, 256-byte L2 prefetch) with a 2-deep software
-// prefetch; no shared memory, no barriers, no atomics.  The item's key is a plain store.
+// Warp-independent: every warp races work items -- (request [, position], chunk of P.chunk
+// columns) -- interleaved over all warps of the grid so residual (p and q) and bonus (p
+// only) rows mix on every SM.  Each step issues the loads of kUnroll float4 per lane (p,
+// and q on a rejection) before racing them: one specialised Philox4x32-10 call per
+// float4, the 3-instruction prune test, deferred exact evaluation of survivors.  Warps
+// racing chunks of the same row share their threshold (red.max on rowT, read back before
+// the final flush) and their best key (red.max on rowkey).  No barriers, no shared memory.
 constexpr int kRaceThreads = 256;
 constexpr int kRaceWarps = kRaceThreads / 32;
+constexpr int kUnroll = 2;
 
 template <int MODE, bool DENSE_Q, bool PRUNE>
 __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const RaceParams P) {
-    pdl_wait();  // the scan kernel's ReqMeta is complete and visible from here on
+    pdl_wait();  // the scan kernel's ReqMeta / rowT / rowkey are complete and visible
     pdl_launch_dependents();
     const int lane = threadIdx.x & 31;
-    const int64_t warp_id = static_cast<int64_t>(blockIdx.x) * kRaceWarps + (threadIdx.x >> 5);
-    const int64_t n_warps = static_cast<int64_t>(gridDim.x) * kRaceWarps;
+    const int32_t warp_id = blockIdx.x * kRaceWarps + (threadIdx.x >> 5);
+    const int32_t n_warps = gridDim.x * kRaceWarps;
     const int32_t per_req = (MODE == kLazy) ? P.n_chunks : (P.k_max + 1) * P.n_chunks;
-    const int64_t n_items = static_cast<int64_t>(P.B) * per_req;
+    const int32_t n_items = P.B * per_req;
     const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
 
-    for (int64_t item = warp_id; item < n_items; item += n_warps) {
-        const int32_t i = static_cast<int32_t>(item / per_req);
-        const int32_t rem = static_cast<int32_t>(item - static_cast<int64_t>(i) * per_req);
+    for (int32_t item = warp_id; item < n_items; item += n_warps) {
+        const int32_t i = item / per_req;
+        const int32_t rem = item - i * per_req;
         const int32_t j = rem / P.n_chunks;
         const int32_t c = rem - j * P.n_chunks;
         const ReqMeta rm = P.meta[i];
@@ -309,6 +322,7 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
         const bool use_q = DENSE_Q && residual;
         int32_t xm_local = -1;
         if (residual && !DENSE_Q) xm_local = ((MODE == kLazy) ? rm.xm : P.drafts[rm.qbase + sel]) - P.vocab_offset;
+        const int32_t key_row = (MODE == kLazy) ? i : rm.r0 + sel;
         const int32_t col_begin = c * P.chunk;
         const int32_t col_end = min(P.vocab, col_begin + P.chunk);
         const float4* prow = reinterpret_cast<const float4*>(P.p + static_cast<int64_t>(rm.r0 + sel) * P.ld + col_begin);
@@ -317,33 +331,28 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
         const int32_t nq = (col_end - col_begin + 3) >> 2;
         const int32_t iters = (nq + 31) >> 5;
         const RaceCtr rc = race_ctr((kPurposeRace << 16) | static_cast<uint32_t>(sel), rm.rid, P.step, P.k0, P.k1);
-
         Race R;
         R.init();
-        // full iterations: all 32 lanes in range, two float4 per lane per step, no masking
-        const int32_t nfull = (col_end - col_begin) >> 7;  // 32 lanes x 4 columns
+        const int32_t nfull = (col_end - col_begin) >> 7;  // iterations with all 128 columns in range
         int32_t it = 0;
-        for (; it + 1 < nfull; it += 2) {
-            const int32_t f0 = it * 32 + lane, f1 = f0 + 32;
-            const float4 a0 = ldg_stream(prow + f0);
-            const float4 a1 = ldg_stream(prow + f1);
-            float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;  // read only when use_q
-            if (use_q) {
-                b0 = ldg_stream(qrow + f0);
-                b1 = ldg_stream(qrow + f1);
+        for (; it + kUnroll <= nfull; it += kUnroll) {
+            float4 a[kUnroll], b[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) a[u] = ldg_stream(prow + (it + u) * 32 + lane);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) b[u] = use_q ? ldg_stream(qrow + (it + u) * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int32_t col = col_begin + 4 * ((it + u) * 32 + lane);
+                const uint4 r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col >> 2), P);
+                float w[4];
+                quad_weights<DENSE_Q>(w, a[u], b[u], residual, col, 0x7FFFFFFF, xm_local);
+                if (PRUNE && u == 0 && R.T == 0.0f) R.warm(w, r);
+                R.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
             }
-            const int32_t col0 = col_begin + 4 * f0, col1 = col0 + 128;
-            const uint4 r0 = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col0 >> 2), P);
-            const uint4 r1 = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col1 >> 2), P);
-            float w0[4], w1[4];
-            quad_weights<DENSE_Q>(w0, a0, b0, residual, col0, 0x7FFFFFFF, xm_local);
-            quad_weights<DENSE_Q>(w1, a1, b1, residual, col1, 0x7FFFFFFF, xm_local);
-            R.quad<PRUNE>(w0, r0, vbase + static_cast<uint32_t>(col0));
-            R.quad<PRUNE>(w1, r1, vbase + static_cast<uint32_t>(col1));
             if (PRUNE) R.sync_T();
         }
-        // remaining iterations (odd count / ragged tail): bounds checks and column masking
-        for (; it < iters; ++it) {
+        for (; it < iters; ++it) {  // remaining iterations: bounds checks and column masking
             const int32_t f = it * 32 + lane;
             const int32_t col = col_begin + 4 * f;
             float w[4] = {0.f, 0.f, 0.f, 0.f};
@@ -354,73 +363,81 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
                 quad_weights<DENSE_Q>(w, a, b, residual, col, col_end, xm_local);
                 r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col >> 2), P);
             }
+            if (PRUNE && R.T == 0.0f) R.warm(w, r);
             R.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
             if (PRUNE) R.sync_T();
         }
-        R.finish<PRUNE>(R.T);
+        if (PRUNE) {  // share this chunk's bound, then flush against the row's best bound
+            if (lane == 0) atomicMax(P.rowT + key_row, __float_as_uint(R.T));
+            const float t = __uint_as_float(*reinterpret_cast<volatile uint32_t*>(P.rowT + key_row));
+            R.finish<PRUNE>(fmaxf(R.T, t));
+        }
         const uint64_t best = warp_max_u64(R.best);
-        uint64_t fb = 0;
-        if (best == 0 && residual) {  // residual identically zero on this chunk: race over p (R5)
-            Race F;
-            F.init();
-            for (int32_t it = 0; it < iters; ++it) {
-                const int32_t f = it * 32 + lane;
-                const int32_t col = col_begin + 4 * f;
-                const float4 a = f < nq ? ldg_stream(prow + f) : make_float4(0.f, 0.f, 0.f, 0.f);
-                float w[4];
-                quad_weights<true>(w, a, a, false, col, col_end, -1);
-                const uint4 r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col >> 2), P);
-                F.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
-                if (PRUNE) F.sync_T();
-            }
-            F.finish<PRUNE>(F.T);
-            fb = warp_max_u64(F.best);
-        }
-        if (lane == 0) {
-            const int64_t key_index = static_cast<int64_t>(MODE == kLazy ? i : rm.r0 + sel) * P.n_chunks + c;
-            P.keys[key_index] = best;
-            P.fbkeys[key_index] = fb;
-        }
+        if (lane == 0 && best) atomicMax(P.rowkey + key_row, static_cast<unsigned long long>(best));
     }
 }
 
 // ------------------------------------------------------------------ 3. emit
-// Lazy: one warp per request.  Shard: one warp per p row (writes the tuple keys).
-template <int MODE>
+// One warp per request: the row key is the red.max of every warp that raced a slice of
+// the row.  A key of 0 means no element of the row had positive weight (the maximal
+// element of a row is always evaluated), i.e. the residual is identically zero: the
+// warp then races max(0, p_m) over the row itself (R5; measure-zero, not performance
+// relevant).
+template <bool PRUNE>
+__device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_t sel, uint32_t rid) {
+    const RaceCtr rc = race_ctr((kPurposeRace << 16) | static_cast<uint32_t>(sel), rid, P.step, P.k0, P.k1);
+    const int lane = threadIdx.x & 31;
+    const float4* p4 = reinterpret_cast<const float4*>(prow);
+    const int32_t nq = (P.vocab + 3) >> 2;
+    const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
+    Race F;
+    F.init();
+    for (int32_t f0 = 0; f0 < nq; f0 += 32) {
+        const int32_t f = f0 + lane;
+        const int32_t col = 4 * f;
+        float w[4] = {0.f, 0.f, 0.f, 0.f};
+        uint4 r = make_uint4(0, 0, 0, 0);
+        if (f < nq) {
+            const float4 a = p4[f];
+            quad_weights<true>(w, a, a, false, col, P.vocab, -1);
+            r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(f), P);
+        }
+        F.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
+        if (PRUNE) F.sync_T();
+    }
+    F.finish<PRUNE>(F.T);
+    return warp_max_u64(F.best);
+}
+
+template <int MODE, bool PRUNE>
 __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P) {
     pdl_wait();
+    pdl_launch_dependents();
     const int32_t unit = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (MODE == kLazy) {
         if (unit >= P.B) return;
         const ReqMeta rm = P.meta[unit];
         if (rm.ok != 1) return;  // emitted by the scan kernel
-        uint64_t key = 0, fb = 0;
-        for (int32_t c = lane; c < P.n_chunks; c += 32) {
-            const uint64_t a = P.keys[static_cast<int64_t>(unit) * P.n_chunks + c];
-            const uint64_t b = P.fbkeys[static_cast<int64_t>(unit) * P.n_chunks + c];
-            key = a > key ? a : key;
-            fb = b > fb ? b : fb;
-        }
-        key = warp_max_u64(key);
-        fb = warp_max_u64(fb);
-        if (key == 0 && rm.m < rm.k) key = fb;  // R5 (valid: every chunk raced p_m)
+        uint64_t key = P.rowkey[unit];
+        if (key == 0 && rm.m < rm.k)  // R5: residual identically zero -> race over p_m
+            key = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
         emit(P, unit, rm.qbase, rm.m, key ? key_index(key) : -1);
         if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
     } else {
-        if (unit >= P.rows_p) return;
-        uint64_t key = 0, fb = 0;
-        for (int32_t c = lane; c < P.n_chunks; c += 32) {
-            const uint64_t a = P.keys[static_cast<int64_t>(unit) * P.n_chunks + c];
-            const uint64_t b = P.fbkeys[static_cast<int64_t>(unit) * P.n_chunks + c];
-            key = a > key ? a : key;
-            fb = b > fb ? b : fb;
-        }
-        key = warp_max_u64(key);
-        fb = warp_max_u64(fb);
-        if (lane == 0) {
-            P.tuples[unit].key = key;
-            P.tuples[unit].fb_key = key ? 0ull : fb;
+        if (unit >= P.B) return;
+        const ReqMeta rm = P.meta[unit];
+        if (rm.ok != 1) return;  // the combine flags invalid requests
+        for (int32_t j = 0; j <= rm.k; ++j) {
+            const int32_t row = rm.r0 + j;
+            const uint64_t key = P.rowkey[row];
+            uint64_t fb = 0;
+            if (key == 0 && j < rm.k)  // this shard's residual is zero: its share of the R5 fallback
+                fb = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(row) * P.ld, j, rm.rid);
+            if (lane == 0) {
+                P.tuples[row].key = key;
+                P.tuples[row].fb_key = fb;
+            }
         }
     }
 }
@@ -430,6 +447,8 @@ __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P) {
 // row m over shards (fallback keys if every shard's residual was zero), emit.
 __global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_tuple* __restrict__ g,
                                             int32_t G, int32_t rows_p) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int32_t warps_per_block = blockDim.x >> 5;
     const int32_t i = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
     if (i >= P.B) return;
@@ -494,12 +513,11 @@ static tsv_status validate(const tsv_verify_args* a) {
 
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
-// workspace: [ReqMeta B][keys n][fbkeys n], n = key rows * n_chunks (key rows: B lazy, rows_p shard)
+// workspace: [ReqMeta B][rowT rows][rowkey rows] (rows: max(B, rows_p))
 static size_t workspace_bytes(const tsv_verify_args* a) {
-    const int32_t chunk = auto_chunk(a);
-    const size_t n_chunks = static_cast<size_t>((a->vocab + chunk - 1) / chunk);
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);
-    return align256(sizeof(ReqMeta) * static_cast<size_t>(a->B)) + 2 * align256(sizeof(uint64_t) * rows * n_chunks);
+    return align256(sizeof(ReqMeta) * static_cast<size_t>(a->B)) + align256(sizeof(uint32_t) * rows) +
+           align256(sizeof(uint64_t) * rows);
 }
 
 static RaceParams make_params(const tsv_verify_args* a) {
@@ -532,10 +550,13 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.rows_p = a->rows_p;
     const size_t n_chunks = static_cast<size_t>(P.n_chunks);
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);
+    (void)n_chunks;
     char* ws = static_cast<char*>(a->workspace);
     P.meta = reinterpret_cast<ReqMeta*>(ws);
-    P.keys = reinterpret_cast<uint64_t*>(ws + align256(sizeof(ReqMeta) * static_cast<size_t>(a->B)));
-    P.fbkeys = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(P.keys) + align256(sizeof(uint64_t) * rows * n_chunks));
+    ws += align256(sizeof(ReqMeta) * static_cast<size_t>(a->B));
+    P.rowT = reinterpret_cast<uint32_t*>(ws);
+    ws += align256(sizeof(uint32_t) * rows);
+    P.rowkey = reinterpret_cast<unsigned long long*>(ws);
     return P;
 }
 
@@ -546,22 +567,6 @@ static int sm_count() {
     if (dev < 0 || dev >= 64) return 148;
     if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
     return n[dev] > 0 ? n[dev] : 148;
-}
-
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                              Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 template <int MODE, bool DENSE_Q, bool PRUNE>
@@ -575,26 +580,25 @@ static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
     }
     const int64_t per_req = (MODE == kLazy) ? P.n_chunks : static_cast<int64_t>(P.k_max + 1) * P.n_chunks;
     const int64_t n_items = static_cast<int64_t>(P.B) * per_req;
+    TSV_REQUIRE(n_items < (1ll << 31), "verify: too many work items");
     const int64_t want = (n_items + kRaceWarps - 1) / kRaceWarps;
-    const int64_t grid = std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * occ);
-    TSV_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(grid > 0 ? grid : 1)), dim3(kRaceThreads), 0, st, P),
-             "verify_race_kernel launch");
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * occ));
+    TSV_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kRaceThreads), 0, st, P), "verify_race_kernel launch");
     return TSV_OK;
 }
 
 template <int MODE>
 static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_t st) {
     const unsigned scan_blocks = static_cast<unsigned>((a->B + 7) / 8);
-    verify_scan_kernel<MODE><<<scan_blocks, 256, 0, st>>>(P);
-    TSV_CUDA(cudaGetLastError(), "verify_scan_kernel launch");
+    TSV_CUDA(launch_pdl(verify_scan_kernel<MODE>, dim3(scan_blocks), dim3(256), 0, st, P), "verify_scan_kernel launch");
     const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
     tsv_status rs;
     if (a->q) rs = prune ? launch_race<MODE, true, true>(P, st) : launch_race<MODE, true, false>(P, st);
     else rs = prune ? launch_race<MODE, false, true>(P, st) : launch_race<MODE, false, false>(P, st);
     TSV_TRY(rs);
-    const int64_t units = (MODE == kLazy) ? a->B : a->rows_p;
-    TSV_CUDA(launch_pdl(verify_emit_kernel<MODE>, dim3(static_cast<unsigned>((units + 7) / 8)), dim3(256), 0, st, P),
-             "verify_emit_kernel launch");
+    const unsigned emit_blocks = static_cast<unsigned>((a->B + 7) / 8);
+    if (prune) TSV_CUDA(launch_pdl(verify_emit_kernel<MODE, true>, dim3(emit_blocks), dim3(256), 0, st, P), "verify_emit_kernel launch");
+    else TSV_CUDA(launch_pdl(verify_emit_kernel<MODE, false>, dim3(emit_blocks), dim3(256), 0, st, P), "verify_emit_kernel launch");
     return TSV_OK;
 }
 
@@ -653,7 +657,8 @@ extern "C" tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const t
     RaceParams P = make_params(a);
     const int threads = 256;
     const int64_t blocks = (static_cast<int64_t>(a->B) + (threads / 32) - 1) / (threads / 32);
-    verify_shard_combine_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(P, gathered, num_shards, a->rows_p);
-    TSV_CUDA(cudaGetLastError(), "verify_shard_combine_kernel launch");
+    TSV_CUDA(launch_pdl(verify_shard_combine_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0,
+                        static_cast<cudaStream_t>(stream), P, gathered, num_shards, a->rows_p),
+             "verify_shard_combine_kernel launch");
     return TSV_OK;
 }

@@ -14,7 +14,7 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtsv.so")
+LIB_PATH = os.environ.get("TSV_LIB_PATH") or os.path.join(_HERE, "lib", "libtsv.so")  # override: experiments only
 
 TSV_OK = 0
 STATUS_NAMES = {1: "TSV_ERR_INVALID_ARG", 2: "TSV_ERR_CUDA", 3: "TSV_ERR_NCCL",

@@ -10,6 +10,6 @@ done
 if [[ -n "${NCU:-}" ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"verify|lookup|goodput|update" -c 300 --csv \
       --log-file gpurun_out/launches.csv python bench.py --steps 32 --warmup 3 --graph-steps 8 --sets 4 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_bench.log 2>&1; echo "ncu-launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-verify_race} -s 8 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-verify_race}" -s ${NCU_S:-8} -c ${NCU_C:-1} \
       -o gpurun_out/verify_full -f python bench.py --steps 16 --warmup 3 --graph-steps 4 --sets 4 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_full.log 2>&1; echo "ncu-full rc=$?"
 fi
