@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k and verify+update calls")
+    ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
     return ap.parse_args()
 
 
@@ -167,7 +169,7 @@ def run_ours(args, rank, world, local_rank):
         offs.append(torch.tensor(o, device=dev))
         lens.append(torch.tensor(np.diff(o).astype(np.int32), device=dev))
     inp = StepInputs(vbs, ctxs, offs, lens, K_MAX, seed=seed)
-    st = SpecStep(inp, device=dev, chunk=args.chunk)
+    st = SpecStep(inp, device=dev, chunk=args.chunk, fused=args.fused)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     footprint = sum(inp.input_bytes(s) for s in range(R))
 
@@ -264,6 +266,29 @@ def run_ours(args, rank, world, local_rank):
     except Exception:
         pass
 
+    # ---- optional: each step component alone, gl launches per graph (in-graph cost per launch)
+    breakdown = None
+    if args.breakdown:
+        breakdown = {}
+        for comp in ("lookup", "choose_k", "verify", "update"):
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                st.run_component(comp, 0, stream=side)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(cg, stream=side):
+                    for t in range(gl):
+                        st.run_component(comp, t, stream=side)
+            torch.cuda.synchronize()
+            cg.replay()
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            for _ in range(reps):
+                cg.replay()
+            c1.record(stream)
+            torch.cuda.synchronize()
+            breakdown[comp] = round(c0.elapsed_time(c1) / (reps * gl) * 1e3, 3)
+
     # ---- end to end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if args.e2e_steps > 0:
@@ -316,17 +341,19 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": WORKLOAD, "global_batch": B * world, "vocab": V, "k_max": K_MAX,
                    "ctx_len": L_CTX, "parallelism": f"request-sharded x{world}",
                    "l2_defeat": f"{R} rotating input sets, footprint {footprint / 1e6:.0f} MB vs L2 {l2 / 1e6:.0f} MB",
-                   "graph_steps": gl},
+                   "graph_steps": gl, "fused": bool(args.fused)},
         "roofline": {"kernel": "tsv_verify_accept (verify_scan + verify_race + verify_emit)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": vbytes, "launch_us": verify_ms * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),
-        "gpu_launches": SpecStep.LAUNCHES_PER_STEP * K,
+        "gpu_launches": st.launches_per_step * K,
         "e2e": e2e,
         "tokens_per_step": tokens_total / K,
         "requests_per_s": B * world * K / (t_max / 1e3),
         "device_status": st_status,
     }
+    if breakdown is not None:
+        line["breakdown_us_per_launch"] = breakdown
     return line
 
 

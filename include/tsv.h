@@ -138,9 +138,10 @@ typedef struct tsv_verify_args {
     int32_t vocab;                /* local columns in this shard (>= 1)             */
     int32_t vocab_offset;         /* global index of local column 0 (% 4 == 0)      */
     int32_t vocab_global;         /* global vocabulary size                         */
-    int32_t chunk;                /* 0 = auto (2048); else vocab columns per work    */
-                                  /* item, a multiple of 1024 up to 16384: a tuning */
-                                  /* / test knob that never changes results          */
+    int32_t chunk;                /* 0 = auto (~1 item per resident warp); else     */
+                                  /* vocab columns per work item, a multiple of 128 */
+                                  /* up to 16384: a tuning / test knob that never   */
+                                  /* changes results                                */
     int32_t flags;                /* TSV_VERIFY_* bits                              */
 } tsv_verify_args;
 
@@ -213,6 +214,24 @@ TSV_API tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_per_r
                                 int32_t* k_per_request, void* stream);
 
 /* --------------------------------------------------------------------------
+ * Fused Propose + GetVerificationLen for the PLD method (Listing 1 lines 15-16 +
+ * 22-23): tsv_propose_lookup followed by tsv_goodput_choose_k
+ * with policy TSV_POLICY_PLD, cap = the proposal lengths just found and
+ * k_max = k_fixed, in ONE kernel (the CTA that finishes its lookup last runs
+ * the selection).  Outputs are identical to the two separate calls.
+ *   counter  uint32 [1] device scratch, zero-filled once after allocation
+ *            (tsv_workspace_clear); every call leaves it zero.  One per stream.
+ * ------------------------------------------------------------------------ */
+TSV_API tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                                       int32_t n_min, int32_t n_max, int32_t k_fixed,
+                                       int32_t* proposals, int32_t* proposal_len,
+                                       const double* alpha, int32_t alpha_per_request,
+                                       const int32_t* ctx_len, tsv_latency_model target,
+                                       double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
+                                       double* goodput_out, int32_t* k_per_request,
+                                       uint32_t* counter, void* stream);
+
+/* --------------------------------------------------------------------------
  * Acceptance-rate update: UpdateGlobalAcceptance (Listing 1 line 19,
  * PAPER.md:219) with the moving average of PAPER.md:131-132:
  *   r = sum_i m_i / sum_i tested_i,  alpha' = fma(decay, alpha - r, r)   (R17)
@@ -227,6 +246,14 @@ TSV_API tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_per_r
 TSV_API tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, const int32_t* num_accepted,
                                  const int32_t* row_offsets, int32_t B, double decay,
                                  int32_t estimator, void* stream);
+
+/* Fused Accept + UpdateGlobalAcceptance (Listing 1 lines 18-19): tsv_verify_accept
+ * followed by tsv_update_acceptance(alpha, per_request, a->num_accepted,
+ * a->row_offsets, a->B, decay, estimator), with the update run by the last CTA of
+ * verify's final kernel.  Outputs identical to the two separate calls; same
+ * workspace as tsv_verify_accept. */
+TSV_API tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
+                                    double decay, int32_t estimator, void* stream);
 
 /* --------------------------------------------------------------------------
  * Communicator for the multi-GPU modes (NCCL over NVLink 5 / NVSwitch,

@@ -1,0 +1,229 @@
+// goodput.cuh -- ArgMaxGoodput and the acceptance update as CTA-wide device routines, shared by
+// the standalone kernels (goodput.cu) and the fused kernels (lookup + choose-k in lookup.cu,
+// verify emit + update in verify.cu).  See goodput.cu for the paper passages and readings.
+#pragma once
+
+#include "common.cuh"
+
+namespace tsv {
+
+constexpr int kGpThreads = 256;
+constexpr int kGpWarps = kGpThreads / 32;
+constexpr int kGpMaxK = TSV_MAX_K + 1;
+
+__device__ __forceinline__ long long warp_sum_i64(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double fwd_time(const tsv_latency_model& m, double n_ctx, double n_batched) {
+    return __fma_rn(m.batched_ms_per_tok, n_batched, __fma_rn(m.ctx_ms_per_tok, n_ctx, m.fixed_ms));
+}
+
+struct ChooseArgs {
+    const double* alpha;
+    const int32_t* ctx_len;
+    const int32_t* cap;
+    int32_t* k_out;
+    double* goodput_out;
+    int32_t* k_per_request;
+    tsv_latency_model target, draft;
+    double pld_cost_ms;
+    long long kv_free;
+    int32_t alpha_per_request, B, k_max, policy;
+};
+
+struct UpdateArgs {
+    double* alpha;
+    const int32_t* num_accepted;
+    const int32_t* row_offsets;
+    double decay;
+    int32_t per_request, B, estimator;
+};
+
+// ArgMaxGoodput over one CTA of kGpThreads threads (all threads must call).  Inputs are read
+// with ld.global.cg so values written by other CTAs of a fused kernel are seen.
+// Each thread accumulates, for every candidate k, the fixed-point token sum
+// L(k) = sum_i rint(2^32 l(alpha_i, min(k, cap_i))) and sum_i min(k, cap_i); one warp
+// reduction + one shared-memory step give the totals; lane k of warp 0 then evaluates
+// T(k) and G(k) in parallel and lane 0 runs Listing 2's strict-'>' scan over k.
+__device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
+    __shared__ long long sL[kGpWarps][kGpMaxK];
+    __shared__ long long sN[kGpWarps][kGpMaxK];
+    __shared__ long long sC[kGpWarps][3];
+    __shared__ int s_best;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t B = A.B, k_max = A.k_max;
+    long long Lk[kGpMaxK], Nk[kGpMaxK];
+#pragma unroll
+    for (int k = 0; k < kGpMaxK; ++k) Lk[k] = Nk[k] = 0;
+    long long n_ctx = 0, n_ctx_spec = 0, b_spec = 0;
+    const double a_glob = A.alpha_per_request ? 0.0 : __ldcg(A.alpha);
+    for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
+        const double a = A.alpha_per_request ? __ldcg(A.alpha + i) : a_glob;
+        const int32_t ci = __ldcg(A.cap + i);
+        const int32_t cl = __ldcg(A.ctx_len + i);
+        n_ctx += cl;
+        if (ci > 0) {
+            n_ctx_spec += cl;
+            b_spec += 1;
+        }
+        double l = 1.0;  // l(a, 0); Horner step l(a, j+1) = fma(a, l(a, j), 1)
+        long long fix = __double2ll_rn(l * 0x1p32);
+        int32_t jcur = 0;
+#pragma unroll
+        for (int k = 0; k < kGpMaxK; ++k) {
+            int32_t ki = k < ci ? k : ci;
+            if (ki < 0) ki = 0;
+            while (jcur < ki) {
+                l = __fma_rn(a, l, 1.0);
+                ++jcur;
+                fix = __double2ll_rn(l * 0x1p32);
+            }
+            Lk[k] += fix;
+            Nk[k] += ki;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kGpMaxK; ++k) {
+        if (k <= k_max) {
+            const long long l = warp_sum_i64(Lk[k]);
+            const long long n = warp_sum_i64(Nk[k]);
+            if (lane == 0) {
+                sL[warp][k] = l;
+                sN[warp][k] = n;
+            }
+        }
+    }
+    n_ctx = warp_sum_i64(n_ctx);
+    n_ctx_spec = warp_sum_i64(n_ctx_spec);
+    b_spec = warp_sum_i64(b_spec);
+    if (lane == 0) {
+        sC[warp][0] = n_ctx;
+        sC[warp][1] = n_ctx_spec;
+        sC[warp][2] = b_spec;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        long long c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+        for (int w = 0; w < kGpWarps; ++w) {
+            c0 += sC[w][0];
+            c1 += sC[w][1];
+            c2 += sC[w][2];
+        }
+        double g = -1.0;
+        bool valid = false;
+        if (lane <= k_max) {
+            long long L = 0, N = 0;
+#pragma unroll
+            for (int w = 0; w < kGpWarps; ++w) {
+                L += sL[w][lane];
+                N += sN[w][lane];
+            }
+            const long long n_batched = N + static_cast<long long>(B);
+            if (!(lane > 0 && A.kv_free >= 0 && n_batched > A.kv_free)) {  // Listing 2 line 5: OOM -> skip
+                const double t_target = fwd_time(A.target, static_cast<double>(c0), static_cast<double>(n_batched));
+                double t_draft;
+                if (A.policy == TSV_POLICY_PLD)
+                    t_draft = A.pld_cost_ms;
+                else
+                    t_draft = lane > 0 ? __dmul_rn(static_cast<double>(lane),
+                                                   fwd_time(A.draft, static_cast<double>(c1), static_cast<double>(c2)))
+                                       : 0.0;
+                g = __ddiv_rn(__dmul_rn(static_cast<double>(L), 0x1p-32), __dadd_rn(t_target, t_draft));
+                valid = true;
+            }
+            if (A.goodput_out) A.goodput_out[lane] = g;
+        }
+        // Listing 2: max_goodput = -1; for k: if goodput > max_goodput: take k (strict >)
+        double max_goodput = -1.0;
+        int best_k = 0;
+        for (int k = 0; k <= k_max; ++k) {
+            const double gk = __shfl_sync(0xFFFFFFFFu, g, k);
+            const bool vk = __shfl_sync(0xFFFFFFFFu, valid, k);
+            if (vk && gk > max_goodput) {
+                max_goodput = gk;
+                best_k = k;
+            }
+        }
+        if (lane == 0) {
+            *A.k_out = best_k;
+            s_best = best_k;
+        }
+    }
+    if (A.k_per_request) {
+        __syncthreads();
+        const int32_t kb = s_best;
+        for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
+            const int32_t ci = __ldcg(A.cap + i);
+            const int32_t ki = kb < ci ? kb : ci;
+            A.k_per_request[i] = ki < 0 ? 0 : ki;
+        }
+    }
+}
+
+// UpdateGlobalAcceptance over one CTA of kGpThreads threads (all threads must call).
+__device__ __forceinline__ void update_block(const UpdateArgs& A) {
+    __shared__ long long red[kGpWarps][2];
+    long long sm = 0, stt = 0;
+    for (int32_t i = threadIdx.x; i < A.B; i += kGpThreads) {
+        const int32_t k = A.row_offsets[i + 1] - A.row_offsets[i] - 1;
+        const int32_t m = __ldcg(A.num_accepted + i);
+        if (m < 0) continue;
+        const long long t = A.estimator == TSV_EST_PROPOSED ? k : (m + (m < k ? 1 : 0));
+        if (A.per_request) {
+            if (t > 0) {
+                const double r = __ddiv_rn(static_cast<double>(m), static_cast<double>(t));
+                A.alpha[i] = __fma_rn(A.decay, __dsub_rn(A.alpha[i], r), r);
+            }
+        } else {
+            sm += m;
+            stt += t;
+        }
+    }
+    if (A.per_request) return;
+    sm = warp_sum_i64(sm);
+    stt = warp_sum_i64(stt);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red[warp][0] = sm;
+        red[warp][1] = stt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long a = 0, b = 0;
+#pragma unroll
+        for (int w = 0; w < kGpWarps; ++w) {
+            a += red[w][0];
+            b += red[w][1];
+        }
+        if (b > 0) {
+            const double r = __ddiv_rn(static_cast<double>(a), static_cast<double>(b));
+            A.alpha[0] = __fma_rn(A.decay, __dsub_rn(A.alpha[0], r), r);
+        }
+    }
+}
+
+// "Last CTA done": every CTA calls this after its own results are written; returns true
+// (to every thread) in the one CTA that arrives last, which then sees all other CTAs'
+// writes.  The counter is left at zero again (self-cleaning).
+__device__ __forceinline__ bool last_cta_done(uint32_t* counter, uint32_t n_ctas) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(counter, 1u);
+        const int last = prev == n_ctas - 1;
+        if (last) {
+            atomicExch(counter, 0u);
+            __threadfence();
+        }
+        s_last = last;
+    }
+    __syncthreads();
+    return s_last != 0;
+}
+
+}  // namespace tsv

@@ -11,17 +11,20 @@
 // is staged into shared memory with a TMA bulk copy (cp.async.bulk) when it fits,
 // each thread scores a strided set of end positions against the query suffix held in
 // registers, and a warp REDUX + shared-memory step reduces the keys.
-#include "common.cuh"
+#include "goodput.cuh"
 
 namespace tsv {
 
 constexpr int kLookupThreads = 256;
-constexpr int kLookupSmemInts = 11776;  // 46 KB static smem: contexts up to ~11.7K tokens are staged
+constexpr int kLookupSmemInts = 11008;  // 43 KB static smem: contexts up to ~11K tokens are staged
 
+// FUSED: the CTA that finishes last also runs ArgMaxGoodput (PLD policy, cap_i = the
+// proposal lengths just written) -- GetVerificationLen right after Propose (Listing 1).
+template <bool FUSED>
 __global__ void __launch_bounds__(kLookupThreads)
     ngram_lookup_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ ctx_offsets, int32_t B,
                         int32_t n_min, int32_t n_max, int32_t K, int32_t* __restrict__ proposals,
-                        int32_t* __restrict__ proposal_len) {
+                        int32_t* __restrict__ proposal_len, ChooseArgs ca, uint32_t* counter) {
     __shared__ __align__(128) int32_t s_ctx[kLookupSmemInts];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_red[kLookupThreads / 32];
@@ -115,6 +118,7 @@ __global__ void __launch_bounds__(kLookupThreads)
         for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? src[e_star + 1 + t] : -1;
         if (tid == 0) proposal_len[i] = len;
     }
+    if (FUSED && last_cta_done(counter, static_cast<uint32_t>(B))) choose_k_block(ca);
 }
 
 }  // namespace tsv
@@ -131,8 +135,46 @@ extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_
     if (B == 0) return TSV_OK;
     TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len, "tsv_propose_lookup: a required array is NULL");
     TSV_TRY(check_device());
-    TSV_CUDA(launch_pdl(ngram_lookup_kernel, dim3(B), dim3(kLookupThreads), 0, static_cast<cudaStream_t>(stream),
-                        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len),
+    ChooseArgs none = {};
+    TSV_CUDA(launch_pdl(ngram_lookup_kernel<false>, dim3(B), dim3(kLookupThreads), 0, static_cast<cudaStream_t>(stream),
+                        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, none,
+                        static_cast<uint32_t*>(nullptr)),
+             "ngram_lookup_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                                                  int32_t n_min, int32_t n_max, int32_t k_fixed,
+                                                  int32_t* proposals, int32_t* proposal_len,
+                                                  const double* alpha, int32_t alpha_per_request,
+                                                  const int32_t* ctx_len, tsv_latency_model target,
+                                                  double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
+                                                  double* goodput_out, int32_t* k_per_request,
+                                                  uint32_t* counter, void* stream) {
+    TSV_REQUIRE(B >= 1, "tsv_propose_lookup_choose_k: B must be >= 1 (got %d)", B);
+    TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
+                "tsv_propose_lookup_choose_k: need 1 <= n_min (%d) <= n_max (%d) <= %d", n_min, n_max, TSV_MAX_NGRAM);
+    TSV_REQUIRE(k_fixed >= 1 && k_fixed <= TSV_MAX_K, "tsv_propose_lookup_choose_k: k_fixed %d outside [1, %d]", k_fixed, TSV_MAX_K);
+    TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len && alpha && ctx_len && k_out && counter,
+                "tsv_propose_lookup_choose_k: a required array is NULL");
+    TSV_TRY(check_device());
+    ChooseArgs A = {};
+    A.alpha = alpha;
+    A.ctx_len = ctx_len;
+    A.cap = proposal_len;
+    A.k_out = k_out;
+    A.goodput_out = goodput_out;
+    A.k_per_request = k_per_request;
+    A.target = target;
+    A.draft = target;
+    A.pld_cost_ms = pld_cost_ms;
+    A.kv_free = static_cast<long long>(kv_free_slots);
+    A.alpha_per_request = alpha_per_request;
+    A.B = B;
+    A.k_max = k_fixed;
+    A.policy = TSV_POLICY_PLD;
+    TSV_CUDA(launch_pdl(ngram_lookup_kernel<true>, dim3(B), dim3(kLookupThreads), 0, static_cast<cudaStream_t>(stream),
+                        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, A, counter),
              "ngram_lookup_kernel launch");
     return TSV_OK;
 }

@@ -23,7 +23,7 @@
 
 #include <algorithm>
 
-#include "common.cuh"
+#include "goodput.cuh"
 
 namespace tsv {
 
@@ -43,6 +43,7 @@ struct RaceParams {
     int32_t* out_tokens;
     int32_t* devstatus;
     ReqMeta* meta;             // [B]
+    uint32_t* counter;         // arrival counter of the fused emit + update (reset by the scan)
     uint32_t* rowT;            // [n_key_rows] shared race threshold per raced row (float bits)
     unsigned long long* rowkey;  // [n_key_rows] max race key per raced row (0: nothing evaluated)
     tsv_shard_tuple* tuples;   // shard mode
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     const uint32_t rej = ~accm & kmask;
     const int32_t m = rej ? (__ffs(rej) - 1) : (ok == 1 ? k : -1);
     const int32_t xm = __shfl_sync(0xFFFFFFFFu, x, (m >= 0 ? m : 0) & 31);
+    if (i == 0 && lane == 0) *P.counter = 0u;
     if (MODE == kLazy) {
         if (lane == 0) {
             P.rowT[i] = 0u;
@@ -310,10 +312,11 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
     const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
 
     for (int32_t item = warp_id; item < n_items; item += n_warps) {
-        const int32_t i = item / per_req;
-        const int32_t rem = item - i * per_req;
+        // request-minor order: neighbouring warps (same CTA / SM) race different requests
+        const int32_t i = item % P.B;
+        const int32_t rem = item / P.B;
+        const int32_t c = rem % P.n_chunks;
         const int32_t j = rem / P.n_chunks;
-        const int32_t c = rem - j * P.n_chunks;
         const ReqMeta rm = P.meta[i];
         if (rm.ok != 1) continue;
         const int32_t sel = (MODE == kLazy) ? rm.m : j;
@@ -410,24 +413,18 @@ __device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_
 }
 
 template <int MODE, bool PRUNE>
-__global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int32_t unit = blockIdx.x * 8 + (threadIdx.x >> 5);
+__device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
     const int lane = threadIdx.x & 31;
+    if (unit >= P.B) return;
+    const ReqMeta rm = P.meta[unit];
+    if (rm.ok != 1) return;  // lazy: emitted by the scan kernel; shard: flagged by the combine
     if (MODE == kLazy) {
-        if (unit >= P.B) return;
-        const ReqMeta rm = P.meta[unit];
-        if (rm.ok != 1) return;  // emitted by the scan kernel
         uint64_t key = P.rowkey[unit];
         if (key == 0 && rm.m < rm.k)  // R5: residual identically zero -> race over p_m
             key = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
         emit(P, unit, rm.qbase, rm.m, key ? key_index(key) : -1);
         if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
     } else {
-        if (unit >= P.B) return;
-        const ReqMeta rm = P.meta[unit];
-        if (rm.ok != 1) return;  // the combine flags invalid requests
         for (int32_t j = 0; j <= rm.k; ++j) {
             const int32_t row = rm.r0 + j;
             const uint64_t key = P.rowkey[row];
@@ -440,6 +437,16 @@ __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P) {
             }
         }
     }
+}
+
+// UPDATE: the CTA that finishes last also runs UpdateGlobalAcceptance (Listing 1 line 19)
+// on the accepted counts just emitted -- the alpha update fused into the verify call.
+template <int MODE, bool PRUNE, bool UPDATE>
+__global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P, UpdateArgs ua) {
+    pdl_wait();
+    pdl_launch_dependents();
+    emit_unit<MODE, PRUNE>(P, blockIdx.x * 8 + (threadIdx.x >> 5));
+    if (UPDATE && last_cta_done(P.counter, gridDim.x)) update_block(ua);
 }
 
 // ------------------------------------------------------------------------ shard combine
@@ -490,7 +497,19 @@ __global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_
 }
 
 // ------------------------------------------------------------------------ host side
-static int32_t auto_chunk(const tsv_verify_args* a) { return a->chunk > 0 ? a->chunk : kChunk; }
+static int sm_count();
+// Default work-item size: about one item per resident warp of the race kernel
+// (148 SMs x 4 CTAs x 8 warps), in whole 128-column iterations.  Never changes results.
+static int32_t auto_chunk(const tsv_verify_args* a) {
+    if (a->chunk > 0) return a->chunk;
+    const int64_t warps = static_cast<int64_t>(sm_count()) * 4 * 8;
+    const int64_t rows_x_cols = static_cast<int64_t>(a->B) * a->vocab;
+    int64_t c = (rows_x_cols + warps - 1) / warps;
+    c = (c + 127) / 128 * 128;
+    if (c < 512) c = 512;
+    if (c > kMaxChunk) c = kMaxChunk;
+    return static_cast<int32_t>(c);
+}
 
 static tsv_status validate(const tsv_verify_args* a) {
     TSV_REQUIRE(a != nullptr, "tsv_verify: args is NULL");
@@ -506,8 +525,8 @@ static tsv_status validate(const tsv_verify_args* a) {
     TSV_REQUIRE(a->vocab_offset >= 0 && a->vocab_offset % 4 == 0, "tsv_verify: vocab_offset must be a non-negative multiple of 4");
     TSV_REQUIRE(a->vocab_global >= a->vocab_offset + a->vocab, "tsv_verify: vocab_global < vocab_offset + vocab");
     TSV_REQUIRE(a->rows_p >= a->B, "tsv_verify: rows_p %d < B %d", a->rows_p, a->B);
-    TSV_REQUIRE(a->chunk == 0 || (a->chunk >= 1024 && a->chunk % 1024 == 0 && a->chunk <= kMaxChunk),
-                "tsv_verify: chunk must be 0 or a multiple of 1024 in [1024, %d]", kMaxChunk);
+    TSV_REQUIRE(a->chunk == 0 || (a->chunk >= 128 && a->chunk % 128 == 0 && a->chunk <= kMaxChunk),
+                "tsv_verify: chunk must be 0 or a multiple of 128 in [128, %d]", kMaxChunk);
     return TSV_OK;
 }
 
@@ -516,7 +535,7 @@ static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255);
 // workspace: [ReqMeta B][rowT rows][rowkey rows] (rows: max(B, rows_p))
 static size_t workspace_bytes(const tsv_verify_args* a) {
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);
-    return align256(sizeof(ReqMeta) * static_cast<size_t>(a->B)) + align256(sizeof(uint32_t) * rows) +
+    return 256 + align256(sizeof(ReqMeta) * static_cast<size_t>(a->B)) + align256(sizeof(uint32_t) * rows) +
            align256(sizeof(uint64_t) * rows);
 }
 
@@ -552,6 +571,8 @@ static RaceParams make_params(const tsv_verify_args* a) {
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);
     (void)n_chunks;
     char* ws = static_cast<char*>(a->workspace);
+    P.counter = reinterpret_cast<uint32_t*>(ws);
+    ws += 256;
     P.meta = reinterpret_cast<ReqMeta*>(ws);
     ws += align256(sizeof(ReqMeta) * static_cast<size_t>(a->B));
     P.rowT = reinterpret_cast<uint32_t*>(ws);
@@ -588,7 +609,7 @@ static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
 }
 
 template <int MODE>
-static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_t st) {
+static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_t st, const UpdateArgs* ua = nullptr) {
     const unsigned scan_blocks = static_cast<unsigned>((a->B + 7) / 8);
     TSV_CUDA(launch_pdl(verify_scan_kernel<MODE>, dim3(scan_blocks), dim3(256), 0, st, P), "verify_scan_kernel launch");
     const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
@@ -597,8 +618,13 @@ static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_
     else rs = prune ? launch_race<MODE, false, true>(P, st) : launch_race<MODE, false, false>(P, st);
     TSV_TRY(rs);
     const unsigned emit_blocks = static_cast<unsigned>((a->B + 7) / 8);
-    if (prune) TSV_CUDA(launch_pdl(verify_emit_kernel<MODE, true>, dim3(emit_blocks), dim3(256), 0, st, P), "verify_emit_kernel launch");
-    else TSV_CUDA(launch_pdl(verify_emit_kernel<MODE, false>, dim3(emit_blocks), dim3(256), 0, st, P), "verify_emit_kernel launch");
+    const UpdateArgs none = {};
+    cudaError_t e;
+    if (ua) e = prune ? launch_pdl(verify_emit_kernel<MODE, true, true>, dim3(emit_blocks), dim3(256), 0, st, P, *ua)
+                      : launch_pdl(verify_emit_kernel<MODE, false, true>, dim3(emit_blocks), dim3(256), 0, st, P, *ua);
+    else e = prune ? launch_pdl(verify_emit_kernel<MODE, true, false>, dim3(emit_blocks), dim3(256), 0, st, P, none)
+                   : launch_pdl(verify_emit_kernel<MODE, false, false>, dim3(emit_blocks), dim3(256), 0, st, P, none);
+    TSV_CUDA(e, "verify_emit_kernel launch");
     return TSV_OK;
 }
 
@@ -631,6 +657,30 @@ extern "C" tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream) 
                 "tsv_verify_accept: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
     return run_verify<kLazy>(a, make_params(a), static_cast<cudaStream_t>(stream));
+}
+
+extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
+                                               double decay, int32_t estimator, void* stream) {
+    TSV_TRY(validate(a));
+    TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
+                "tsv_verify_accept_update: unsharded call needs vocab_offset == 0 and vocab == vocab_global");
+    TSV_REQUIRE(alpha != nullptr, "tsv_verify_accept_update: alpha is NULL");
+    TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_verify_accept_update: decay %g outside [0, 1]", decay);
+    TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED, "tsv_verify_accept_update: unknown estimator");
+    TSV_TRY(check_device());
+    if (a->B == 0) return TSV_OK;
+    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+                "tsv_verify_accept_update: workspace too small (%llu < %llu bytes)",
+                (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    UpdateArgs ua;
+    ua.alpha = alpha;
+    ua.num_accepted = a->num_accepted;
+    ua.row_offsets = a->row_offsets;
+    ua.decay = decay;
+    ua.per_request = per_request;
+    ua.B = a->B;
+    ua.estimator = estimator;
+    return run_verify<kLazy>(a, make_params(a), static_cast<cudaStream_t>(stream), &ua);
 }
 
 extern "C" tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_shard_tuple* tuples_out,

@@ -70,11 +70,15 @@ class StepInputs:
 
 
 class SpecStep:
-    """Preallocated outputs + the four launches; eager ``run`` or CUDA-graph ``capture``/``replay``."""
+    """Preallocated outputs + the step's launches; eager ``run`` or CUDA-graph ``capture``/``replay``.
 
-    LAUNCHES_PER_STEP = 6  # lookup, choose-k, verify (scan + race + emit), update
+    fused=False (default): the four separate ABI calls, 6 kernels chained with PDL.
+    fused=True: tsv_propose_lookup_choose_k + tsv_verify_accept_update, 4 kernels (the last
+    CTA of lookup / emit runs choose-k / the update).  Identical outputs
+    (tests/test_gpu_parity.py); measured on B200 the PDL chain is ~2 us faster per step
+    than the last-CTA handshakes, hence the default."""
 
-    def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0):
+    def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0, fused: bool = False):
         self.inp = inp
         B, K = inp.B, inp.k_max
         dev = torch.device(device)
@@ -87,6 +91,8 @@ class SpecStep:
         self.num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
         self.out_tokens = torch.empty((B, K + 1), dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)  # fused lookup + choose-k
+        self.fused = fused
         self.args = []
         for vb in inp.verify:
             a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids,
@@ -100,12 +106,28 @@ class SpecStep:
             a.workspace_bytes = self.workspace.numel()
         self.graph: Optional[torch.cuda.CUDAGraph] = None
 
+    @property
+    def launches_per_step(self) -> int:
+        return 4 if self.fused else 6
+
     def run(self, step: int, stream=None):
-        """Launch one decode step (4 kernels) on ``stream`` (default: current)."""
+        """Launch one decode step on ``stream`` (default: current)."""
         inp = self.inp
         s = step % inp.sets
         st = tsv._stream(stream)
         L = tsv.lib()
+        if self.fused:
+            tsv._check(L.tsv_propose_lookup_choose_k(
+                inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B, inp.n_min, inp.n_max, inp.k_fixed,
+                self.proposals.data_ptr(), self.proposal_len.data_ptr(), self.alpha.data_ptr(), 0,
+                inp.ctx_len[s].data_ptr(), tsv.LatencyModel(*inp.target), float(inp.pld_cost_ms),
+                int(inp.kv_free_slots), self.k_star.data_ptr(), self.goodput.data_ptr(), self.k_req.data_ptr(),
+                self.counter.data_ptr(), st))
+            a = self.args[s]
+            a.step = step & 0xFFFFFFFF
+            tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
+                                                  tsv.EST_TESTED, st))
+            return
         tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
                                         inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
                                         self.proposal_len.data_ptr(), st))
@@ -121,6 +143,34 @@ class SpecStep:
         tsv._check(L.tsv_update_acceptance(self.alpha.data_ptr(), 0, self.num_accepted.data_ptr(),
                                            inp.verify[s].row_offsets.data_ptr(), inp.B, 0.9,
                                            tsv.EST_TESTED, st))
+
+    def run_component(self, name: str, step: int, stream=None):
+        """One launch of a single step component (timing breakdown only)."""
+        inp = self.inp
+        s = step % inp.sets
+        st = tsv._stream(stream)
+        L = tsv.lib()
+        if name == "lookup":
+            tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
+                                            inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
+                                            self.proposal_len.data_ptr(), st))
+        elif name == "choose_k":
+            tsv._check(L.tsv_goodput_choose_k(self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(),
+                                              self.proposal_len.data_ptr(), inp.B, inp.k_fixed,
+                                              tsv.POLICY_PLD, tsv.LatencyModel(*inp.target),
+                                              tsv.LatencyModel(*inp.draft), float(inp.pld_cost_ms),
+                                              int(inp.kv_free_slots), self.k_star.data_ptr(),
+                                              self.goodput.data_ptr(), self.k_req.data_ptr(), st))
+        elif name == "verify":
+            a = self.args[s]
+            a.step = step & 0xFFFFFFFF
+            tsv._check(L.tsv_verify_accept(tsv.ctypes.byref(a), st))
+        elif name == "update":
+            tsv._check(L.tsv_update_acceptance(self.alpha.data_ptr(), 0, self.num_accepted.data_ptr(),
+                                               inp.verify[s].row_offsets.data_ptr(), inp.B, 0.9,
+                                               tsv.EST_TESTED, st))
+        else:
+            raise ValueError(name)
 
     def capture(self, steps):
         """Capture ``steps`` consecutive decode steps into one CUDA graph."""

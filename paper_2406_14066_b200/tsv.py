@@ -35,6 +35,7 @@ EXPORTED = [
     "tsv_verify_shard_combine", "tsv_goodput_choose_k", "tsv_update_acceptance",
     "tsv_comm_get_unique_id", "tsv_comm_init", "tsv_comm_destroy",
     "tsv_verify_sharded_workspace_size", "tsv_verify_accept_sharded", "tsv_allreduce_i64",
+    "tsv_propose_lookup_choose_k", "tsv_verify_accept_update",
 ]
 
 
@@ -93,6 +94,9 @@ def _load() -> ctypes.CDLL:
                                               ctypes.c_int),
         "tsv_verify_accept_sharded": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
         "tsv_allreduce_i64": ([P, sz, P, P], ctypes.c_int),
+        "tsv_propose_lookup_choose_k": ([P, P, i32, i32, i32, i32, P, P, P, i32, P, LatencyModel, f64, i64,
+                                         P, P, P, P, P], ctypes.c_int),
+        "tsv_verify_accept_update": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -251,6 +255,42 @@ def tsv_verify_shard_partial(args: VerifyArgs, tuples_out: torch.Tensor, stream=
 def tsv_verify_shard_combine(args: VerifyArgs, gathered: torch.Tensor, num_shards: int, stream=None):
     _check(_lib.tsv_verify_shard_combine(ctypes.byref(args), _ptr(gathered), int(num_shards),
                                          _stream(stream)))
+
+
+def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, ctx_len, target,
+                                pld_cost_ms, counter, kv_free_slots=-1, alpha_per_request=None,
+                                proposals=None, proposal_len=None, k_out=None, goodput_out=None,
+                                k_per_request=None, stream=None):
+    """Fused prompt lookup + PLD goodput selection.  ``counter``: uint32 [1], zeroed once.
+    Returns (proposals, proposal_len, k_out, goodput_out)."""
+    B = ctx_offsets.numel() - 1
+    dev = ctx_offsets.device
+    _want(counter, torch.int32, 1, "counter")
+    if proposals is None:
+        proposals = torch.empty((B, k_fixed), dtype=torch.int32, device=dev)
+    if proposal_len is None:
+        proposal_len = torch.empty(B, dtype=torch.int32, device=dev)
+    if k_out is None:
+        k_out = torch.empty(1, dtype=torch.int32, device=dev)
+    if goodput_out is None:
+        goodput_out = torch.empty(k_fixed + 1, dtype=torch.float64, device=dev)
+    per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
+    ctx_p = _ptr(ctx) if ctx.numel() else _ptr(ctx_offsets)
+    _check(_lib.tsv_propose_lookup_choose_k(ctx_p, _ptr(ctx_offsets), B, n_min, n_max, k_fixed,
+                                            _ptr(proposals), _ptr(proposal_len), _ptr(alpha),
+                                            1 if per else 0, _ptr(ctx_len), LatencyModel(*target),
+                                            float(pld_cost_ms), int(kv_free_slots), _ptr(k_out),
+                                            _ptr(goodput_out), _ptr(k_per_request), _ptr(counter),
+                                            _stream(stream)))
+    return proposals, proposal_len, k_out, goodput_out
+
+
+def tsv_verify_accept_update(args: VerifyArgs, alpha, decay=0.9, estimator=EST_TESTED, per_request=False,
+                             stream=None):
+    """Fused verify/accept + acceptance update (alpha fp64 device, in place)."""
+    _want(alpha, torch.float64, 1, "alpha")
+    _check(_lib.tsv_verify_accept_update(ctypes.byref(args), _ptr(alpha), 1 if per_request else 0,
+                                         float(decay), int(estimator), _stream(stream)))
 
 
 # ----------------------------------------------------------------------------- goodput

@@ -78,7 +78,7 @@ def test_one_hot_drafts(tsv):
     assert_verify_parity(tsv, vb, step=3)
 
 
-@pytest.mark.parametrize("chunk", [1024, 3072, 4096, 8192, 16384])
+@pytest.mark.parametrize("chunk", [128, 640, 1792, 4096, 16384])
 def test_chunking_does_not_change_results(tsv, chunk):
     vb = synth.make_verify_batch(B=48, V=32000, k_max=8, lam=0.7, seed=5)
     assert_verify_parity(tsv, vb, step=2, chunk=chunk)
@@ -379,15 +379,59 @@ def test_update_parity(tsv):
                 assert (got.view(np.uint64) == np.atleast_1d(want).view(np.uint64)).all()
 
 
+# ------------------------------------------------------------------- fused entry points
+def test_fused_lookup_choose_k_equals_separate(tsv):
+    ctx, offs = synth.make_contexts(B=200, L=2048, seed=21, ragged=True)
+    c, o = torch.tensor(ctx, device=DEV), torch.tensor(offs, device=DEV)
+    ctx_len = torch.tensor(np.diff(offs).astype(np.int32), device=DEV)
+    counter = torch.zeros(1, dtype=torch.int32, device=DEV)
+    for a0 in (0.3, 0.7, 0.95):
+        alpha = torch.tensor([a0], dtype=torch.float64, device=DEV)
+        pr, pl = tsv.tsv_propose_lookup(c, o, 1, 4, 5)
+        k, g, kpr = tsv.tsv_goodput_choose_k(alpha, ctx_len, pl, 5, tsv.POLICY_PLD, synth.SPEC_DESK_TARGET,
+                                             synth.SPEC_DESK_DRAFT, 0.05, k_per_request=torch.empty_like(pl))
+        kpr2 = torch.empty_like(pl)
+        pr2, pl2, k2, g2 = tsv.tsv_propose_lookup_choose_k(c, o, 1, 4, 5, alpha, ctx_len, synth.SPEC_DESK_TARGET,
+                                                           0.05, counter, k_per_request=kpr2)
+        torch.cuda.synchronize()
+        assert torch.equal(pr, pr2) and torch.equal(pl, pl2) and torch.equal(k, k2)
+        assert torch.equal(g.view(torch.int64), g2.view(torch.int64)) and torch.equal(kpr, kpr2)
+        assert int(counter.item()) == 0
+        ok, og = oracle.choose_k(a0, np.diff(offs).astype(np.int32), _np(pl), 5, oracle.POLICY_PLD,
+                                 synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT, pld_cost_ms=0.05)
+        assert int(k2.item()) == ok
+
+
+def test_fused_verify_update_equals_separate(tsv):
+    vb = synth.make_verify_batch(B=256, V=32000, k_max=8, lam=0.7, seed=22).to(DEV)
+    for per in (False, True):
+        na = torch.empty(256, dtype=torch.int32, device=DEV)
+        out = torch.empty((256, 9), dtype=torch.int32, device=DEV)
+        a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 7, 3, 8, na, out)
+        ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+        a0 = torch.rand(256 if per else 1, dtype=torch.float64, device=DEV, generator=torch.Generator(DEV).manual_seed(1))
+        alpha1 = a0.clone()
+        tsv._check(tsv.lib().tsv_verify_accept(tsv.ctypes.byref(a), tsv._stream(None)))
+        tsv.tsv_update_acceptance(alpha1, na, vb.row_offsets, 0.9, per_request=per)
+        out1, na1 = out.clone(), na.clone()
+        alpha2 = a0.clone()
+        tsv.tsv_verify_accept_update(a, alpha2, 0.9, per_request=per)
+        torch.cuda.synchronize()
+        assert torch.equal(out1, out) and torch.equal(na1, na)
+        assert torch.equal(alpha1.view(torch.int64), alpha2.view(torch.int64))
+
+
 # ------------------------------------------------------------------- whole step in a graph
-def test_step_graph_capture_matches_eager(tsv):
+@pytest.mark.parametrize("fused", [False, True])
+def test_step_graph_capture_matches_eager(tsv, fused):
     from paper_2406_14066_b200.step import SpecStep, StepInputs
     inp = StepInputs.synthetic(B=64, V=32000, L=1024, k_max=8, seed=20, device=DEV)
-    st = SpecStep(inp)
+    st = SpecStep(inp, fused=fused)
     st.run(step=0)
     torch.cuda.synchronize()
     eager = {k: v.clone() for k, v in st.outputs().items()}
-    st2 = SpecStep(inp)
+    st2 = SpecStep(inp, fused=not fused)
     st2.capture(steps=[0])
     st2.replay()
     torch.cuda.synchronize()
