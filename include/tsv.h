@@ -274,6 +274,19 @@ TSV_API tsv_status tsv_verify_sharded_workspace_size(const tsv_verify_args* a, i
 TSV_API tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_comm* comm, void* stream);
 TSV_API tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* comm, void* stream);
 
+/* --------------------------------------------------------------------------
+ * Diagnostics (used by the GPU tests; not on the hot path).
+ * tsv_debug_race_E: out[t] = E(u) of the race uniform u = (2(m_begin+t)+1) 2^-24
+ *   exactly as the race kernels evaluate it (series near u = 1, double log
+ *   elsewhere), for t < n, m_begin + n <= 2^23.  out: fp32 [n] device.
+ * tsv_debug_philox: out[4t..4t+3] = Philox4x32-10(ctr[4t..4t+3], key[0..1]) on the
+ *   device; race_variant != 0 uses the row-specialised evaluation of the race
+ *   kernels (philox_race).  ctr: uint32 [4n], key: uint32 [2], out: uint32 [4n].
+ * ------------------------------------------------------------------------ */
+TSV_API tsv_status tsv_debug_race_E(uint32_t m_begin, uint32_t n, float* out, void* stream);
+TSV_API tsv_status tsv_debug_philox(const uint32_t* ctr, const uint32_t* key, uint32_t n, uint32_t* out,
+                                    int32_t race_variant, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -190,3 +190,60 @@ extern "C" tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* c
                                         static_cast<cudaStream_t>(stream)),
                        "ncclAllReduce");
 }
+
+// ------------------------------------------------------------------ diagnostics (tests)
+namespace tsv {
+__global__ void debug_race_E_kernel(uint32_t m_begin, uint32_t n, float* out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint32_t m = m_begin + t;  // race uniform u = (2m + 1) 2^-24, any word with low bits m
+    out[t] = race_E_omu(one_minus_u_race(m));
+}
+
+struct DebugKeys {
+    uint32_t ks0[10], ks1[10];
+};
+
+__global__ void debug_philox_kernel(const uint32_t* ctr, const uint32_t* key, uint32_t n, uint32_t* out,
+                                    int32_t race_variant) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint32_t* c = ctr + 4 * t;
+    uint4 r;
+    if (race_variant) {
+        DebugKeys ks;
+        for (uint32_t i = 0; i < 10; ++i) {
+            ks.ks0[i] = key[0] + i * kPhiloxW0;
+            ks.ks1[i] = key[1] + i * kPhiloxW1;
+        }
+        const RaceCtr rc = race_ctr(c[1], c[2], c[3], key[0], key[1]);
+        r = philox_race(rc, c[0], ks);
+    } else {
+        r = philox4x32_10(c[0], c[1], c[2], c[3], key[0], key[1]);
+    }
+    out[4 * t + 0] = r.x;
+    out[4 * t + 1] = r.y;
+    out[4 * t + 2] = r.z;
+    out[4 * t + 3] = r.w;
+}
+}  // namespace tsv
+
+extern "C" tsv_status tsv_debug_race_E(uint32_t m_begin, uint32_t n, float* out, void* stream) {
+    TSV_REQUIRE(out != nullptr, "tsv_debug_race_E: out is NULL");
+    TSV_REQUIRE(static_cast<uint64_t>(m_begin) + n <= (1ull << 23), "tsv_debug_race_E: range beyond 2^23");
+    TSV_TRY(check_device());
+    if (n == 0) return TSV_OK;
+    debug_race_E_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(m_begin, n, out);
+    TSV_CUDA(cudaGetLastError(), "debug_race_E_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_debug_philox(const uint32_t* ctr, const uint32_t* key, uint32_t n, uint32_t* out,
+                                       int32_t race_variant, void* stream) {
+    TSV_REQUIRE(ctr && key && out, "tsv_debug_philox: NULL argument");
+    TSV_TRY(check_device());
+    if (n == 0) return TSV_OK;
+    debug_philox_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(ctr, key, n, out, race_variant);
+    TSV_CUDA(cudaGetLastError(), "debug_philox_kernel launch");
+    return TSV_OK;
+}

@@ -35,7 +35,7 @@ EXPORTED = [
     "tsv_verify_shard_combine", "tsv_goodput_choose_k", "tsv_update_acceptance",
     "tsv_comm_get_unique_id", "tsv_comm_init", "tsv_comm_destroy",
     "tsv_verify_sharded_workspace_size", "tsv_verify_accept_sharded", "tsv_allreduce_i64",
-    "tsv_propose_lookup_choose_k", "tsv_verify_accept_update",
+    "tsv_propose_lookup_choose_k", "tsv_verify_accept_update", "tsv_debug_race_E", "tsv_debug_philox",
 ]
 
 
@@ -97,6 +97,8 @@ def _load() -> ctypes.CDLL:
         "tsv_propose_lookup_choose_k": ([P, P, i32, i32, i32, i32, P, P, P, i32, P, LatencyModel, f64, i64,
                                          P, P, P, P, P], ctypes.c_int),
         "tsv_verify_accept_update": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P], ctypes.c_int),
+        "tsv_debug_race_E": ([ctypes.c_uint32, ctypes.c_uint32, P, P], ctypes.c_int),
+        "tsv_debug_philox": ([P, P, ctypes.c_uint32, P, i32, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -367,3 +369,18 @@ def tsv_allreduce_i64(data: torch.Tensor, comm: Comm, stream=None):
     _want(data, torch.int64, None, "data")
     _check(_lib.tsv_allreduce_i64(_ptr(data), data.numel(), comm.handle, _stream(stream)))
     return data
+
+
+# ----------------------------------------------------------------------------- diagnostics
+def tsv_debug_race_E(m_begin: int, n: int, out=None, device="cuda"):
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=device)
+    _check(_lib.tsv_debug_race_E(int(m_begin), int(n), _ptr(out), _stream(None)))
+    return out
+
+
+def tsv_debug_philox(ctr: torch.Tensor, key: torch.Tensor, race_variant: bool = False):
+    n = ctr.numel() // 4
+    out = torch.empty(4 * n, dtype=torch.int32, device=ctr.device)
+    _check(_lib.tsv_debug_philox(_ptr(ctr), _ptr(key), n, _ptr(out), 1 if race_variant else 0, _stream(None)))
+    return out
