@@ -7,16 +7,83 @@
 // ONE max-reduction: for every end position e in [0, L-2] let c(e)
 // be the length of the common suffix of ctx[..e] and ctx[..L-1] capped at n_max;
 // key(e) = (c(e) << 20) | e.  The lexicographic max of (c, e) is exactly the longest
-// matching n and, among its matches, the latest one.  One CTA per request: the context
-// is staged into shared memory with a TMA bulk copy (cp.async.bulk) when it fits,
-// each thread scores a strided set of end positions against the query suffix held in
-// registers, and a warp REDUX + shared-memory step reduces the keys.
+// matching n and, among its matches, the latest one.
+//
+// One CTA per request reads the context straight from global memory in 16-byte groups
+// aligned to the ctx allocation (no staging, no barrier wait): thread t takes groups
+// g_lo+t, g_lo+t+256, ..., loading kUnroll groups before it compares any.  For the four
+// positions of a group it also needs the three tokens before them (the previous group,
+// an L1 hit: the neighbouring thread loads it too).  The first min(n_max, 4) suffix
+// comparisons are evaluated branch-free on that 7-token window; only a position whose
+// 4-token suffix already matches and n_max > 4 walks further (rarely).  A block max
+// reduction (redux.sync + shared memory) gives the request's key; warp 0 writes the
+// proposal.
 #include "goodput.cuh"
 
 namespace tsv {
 
-constexpr int kLookupThreads = 256;
-constexpr int kLookupSmemInts = 11008;  // 43 KB static smem: contexts up to ~11K tokens are staged
+constexpr int kLookupThreads = 256;  // == kGpThreads: the fused variant runs choose_k_block
+constexpr int kLookupUnroll = 4;     // groups in flight per thread
+
+struct Group {
+    int4 cur;   // ctx[4g .. 4g+3]
+    int4 prev;  // ctx[4g-4 .. 4g-1] (only .y .z .w are used)
+};
+
+// Loads group g; `last` is the absolute index of the request's last token (every index
+// read is <= last, so nothing past the request is touched; indices below the request's
+// offset are valid memory and are masked by e - j >= 0 in scan_group).
+__device__ __forceinline__ Group load_group(const int32_t* __restrict__ ctx, int64_t g, int64_t last, bool vec) {
+    Group G;
+    const int64_t a = 4 * g;
+    if (vec && a + 3 <= last) {
+        G.cur = __ldg(reinterpret_cast<const int4*>(ctx) + g);
+    } else {
+        G.cur.x = a <= last ? __ldg(ctx + a) : 0;
+        G.cur.y = a + 1 <= last ? __ldg(ctx + a + 1) : 0;
+        G.cur.z = a + 2 <= last ? __ldg(ctx + a + 2) : 0;
+        G.cur.w = a + 3 <= last ? __ldg(ctx + a + 3) : 0;
+    }
+    if (g == 0) {
+        G.prev = make_int4(0, 0, 0, 0);
+    } else if (vec) {
+        G.prev = __ldg(reinterpret_cast<const int4*>(ctx) + g - 1);
+    } else {
+        G.prev = make_int4(0, __ldg(ctx + a - 3), __ldg(ctx + a - 2), __ldg(ctx + a - 1));
+    }
+    return G;
+}
+
+struct Query {
+    int32_t q0, q1, q2, q3;  // q_j = ctx[L-1-j] (0 where j >= L: masked by e - j >= 0)
+    int32_t off, L, n_max;
+};
+
+// key(e) = (c(e) << 20) | e for the four positions of group g (0 when c(e) = 0 or e is
+// not an end position in [0, L-2]); returns their max.
+__device__ __forceinline__ uint32_t scan_group(const int32_t* __restrict__ ctx, const Group& G, int64_t g,
+                                               const Query& Q) {
+    const int32_t w[7] = {G.prev.y, G.prev.z, G.prev.w, G.cur.x, G.cur.y, G.cur.z, G.cur.w};
+    uint32_t best = 0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int64_t e = 4 * g + s - Q.off;
+        const bool m0 = e >= 0 && e <= Q.L - 2 && w[3 + s] == Q.q0;
+        const bool m1 = m0 && Q.n_max >= 2 && e >= 1 && w[2 + s] == Q.q1;
+        const bool m2 = m1 && Q.n_max >= 3 && e >= 2 && w[1 + s] == Q.q2;
+        const bool m3 = m2 && Q.n_max >= 4 && e >= 3 && w[s] == Q.q3;
+        int32_t cl = static_cast<int32_t>(m0) + static_cast<int32_t>(m1) + static_cast<int32_t>(m2) +
+                     static_cast<int32_t>(m3);
+        if (m3 && Q.n_max > 4) {  // rare: the 4-token suffix matches and longer n-grams count
+            const int32_t* c = ctx + Q.off;
+            const int32_t ee = static_cast<int32_t>(e);
+            while (cl < Q.n_max && cl <= ee && __ldg(c + ee - cl) == __ldg(c + Q.L - 1 - cl)) ++cl;
+        }
+        const uint32_t key = cl ? ((static_cast<uint32_t>(cl) << 20) | static_cast<uint32_t>(e)) : 0u;
+        best = key > best ? key : best;
+    }
+    return best;
+}
 
 // FUSED: the CTA that finishes last also runs ArgMaxGoodput (PLD policy, cap_i = the
 // proposal lengths just written) -- GetVerificationLen right after Propose (Listing 1).
@@ -25,81 +92,40 @@ __global__ void __launch_bounds__(kLookupThreads)
     ngram_lookup_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ ctx_offsets, int32_t B,
                         int32_t n_min, int32_t n_max, int32_t K, int32_t* __restrict__ proposals,
                         int32_t* __restrict__ proposal_len, ChooseArgs ca, uint32_t* counter) {
-    __shared__ __align__(128) int32_t s_ctx[kLookupSmemInts];
-    __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_red[kLookupThreads / 32];
     pdl_wait();
     pdl_launch_dependents();
     const int32_t i = blockIdx.x;
-    const int32_t off = ctx_offsets[i];
-    const int32_t L = ctx_offsets[i + 1] - off;
-    const int32_t* c = ctx + off;
     const int tid = threadIdx.x;
-
-    // ---- stage the context: aligned middle by one TMA bulk copy, ragged edges by LDG
-    const bool staged = L > 0 && L <= kLookupSmemInts - 8 && (reinterpret_cast<uintptr_t>(ctx) & 15u) == 0;
-    int32_t shift = 0;  // s_ctx[shift + t] == c[t]; shift = off & 3 keeps int4 groups aligned
-    if (staged) {
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(c);
-        const uintptr_t a_lo = (a0 + 15) & ~static_cast<uintptr_t>(15);         // first aligned byte inside
-        const uintptr_t a_hi = (a0 + 4ull * L) & ~static_cast<uintptr_t>(15);   // last aligned byte inside
-        const int32_t head = static_cast<int32_t>((a_lo - a0) >> 2);            // elements before a_lo
-        shift = (4 - head) & 3;  // so that s_ctx + shift + head is 16-byte aligned
-        const bool has_mid = a_hi > a_lo;
-        const uint32_t mid_bytes = has_mid ? static_cast<uint32_t>(a_hi - a_lo) : 0u;
-        if (tid == 0) {
-            mbar_init(&s_bar, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-        if (tid == 0 && has_mid) {
-            mbar_expect_tx(&s_bar, mid_bytes);
-            bulk_g2s(s_ctx + shift + head, reinterpret_cast<const void*>(a_lo), mid_bytes, &s_bar);
-        }
-        const int32_t mid_elems = static_cast<int32_t>(mid_bytes >> 2);
-        const int32_t n_head = min(head, L);              // ragged edges by plain loads
-        const int32_t tail0 = head + mid_elems;
-        if (tid < n_head) s_ctx[shift + tid] = c[tid];
-        if (has_mid && tail0 + tid < L) s_ctx[shift + tail0 + tid] = c[tail0 + tid];
-        if (!has_mid)
-            for (int32_t t = n_head + tid; t < L; t += kLookupThreads) s_ctx[shift + t] = c[t];
-        if (has_mid) mbar_wait(&s_bar, 0);
-        __syncthreads();
-    }
-    const int32_t* src = staged ? (s_ctx + shift) : c;
-
-    // ---- key(e) = (min(c(e), n_max) << 20) | e over e in [0, L-2]; c(e) = common suffix
-    // length of ctx[..e] and ctx[..L-1].  Fast path: compare ctx[e] with the last token q0
-    // four positions at a time; only on a hit is the rest of the suffix compared.
+    const int32_t off = __ldg(ctx_offsets + i);
+    const int32_t L = __ldg(ctx_offsets + i + 1) - off;
+    const int32_t* c = ctx + off;
     uint32_t best = 0;
     if (L >= 2) {
-        const int32_t q0 = src[L - 1];
-        auto suffix_key = [&](int32_t e) -> uint32_t {  // ctx[e] == q0 already
-            int32_t cl = 1;
-            while (cl < n_max && cl <= e && src[e - cl] == src[L - 1 - cl]) ++cl;
-            return (static_cast<uint32_t>(cl) << 20) | static_cast<uint32_t>(e);
-        };
-        if (staged) {
-            const int4* s4 = reinterpret_cast<const int4*>(s_ctx);
-            const int32_t n_groups = (shift + L - 1 + 3) >> 2;  // smem ints [0, shift + L - 1) hold e <= L-2
-            for (int32_t g = tid; g < n_groups; g += kLookupThreads) {
-                const int4 v = s4[g];
-                const int32_t e0 = 4 * g - shift;
-                const int32_t vv[4] = {v.x, v.y, v.z, v.w};
+        const int64_t last = static_cast<int64_t>(off) + L - 1;
+        Query Q;
+        Q.q0 = __ldg(ctx + last);
+        Q.q1 = __ldg(ctx + last - 1);
+        Q.q2 = L >= 3 ? __ldg(ctx + last - 2) : 0;
+        Q.q3 = L >= 4 ? __ldg(ctx + last - 3) : 0;
+        Q.off = off;
+        Q.L = L;
+        Q.n_max = n_max;
+        const bool vec = (reinterpret_cast<uintptr_t>(ctx) & 15u) == 0;
+        const int64_t g_lo = off >> 2, g_hi = (last - 1) >> 2;  // groups holding e in [0, L-2]
+        for (int64_t g0 = g_lo + tid; g0 <= g_hi; g0 += kLookupUnroll * kLookupThreads) {
+            Group G[kLookupUnroll];
 #pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    const int32_t e = e0 + s;
-                    if (vv[s] == q0 && e >= 0 && e <= L - 2) {
-                        const uint32_t key = suffix_key(e);
-                        best = key > best ? key : best;
-                    }
-                }
+            for (int u = 0; u < kLookupUnroll; ++u) {
+                const int64_t g = g0 + u * kLookupThreads;
+                if (g <= g_hi) G[u] = load_group(ctx, g, last, vec);
             }
-        } else {
-            for (int32_t e = tid; e <= L - 2; e += kLookupThreads) {
-                if (src[e] == q0) {
-                    const uint32_t key = suffix_key(e);
-                    best = key > best ? key : best;
+#pragma unroll
+            for (int u = 0; u < kLookupUnroll; ++u) {
+                const int64_t g = g0 + u * kLookupThreads;
+                if (g <= g_hi) {
+                    const uint32_t k = scan_group(ctx, G[u], g, Q);
+                    best = k > best ? k : best;
                 }
             }
         }
@@ -115,7 +141,7 @@ __global__ void __launch_bounds__(kLookupThreads)
         int32_t len = 0;
         if (L >= 2 && n_star >= n_min) len = min(K, L - 1 - e_star);
         int32_t* out = proposals + static_cast<int64_t>(i) * K;
-        for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? src[e_star + 1 + t] : -1;
+        for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? __ldg(c + e_star + 1 + t) : -1;
         if (tid == 0) proposal_len[i] = len;
     }
     if (FUSED && last_cta_done(counter, static_cast<uint32_t>(B))) choose_k_block(ca);
@@ -136,9 +162,9 @@ extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_
     TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len, "tsv_propose_lookup: a required array is NULL");
     TSV_TRY(check_device());
     ChooseArgs none = {};
-    TSV_CUDA(launch_pdl(ngram_lookup_kernel<false>, dim3(B), dim3(kLookupThreads), 0, static_cast<cudaStream_t>(stream),
-                        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, none,
-                        static_cast<uint32_t*>(nullptr)),
+    TSV_CUDA(launch_pdl(ngram_lookup_kernel<false>, dim3(B), dim3(kLookupThreads), 0,
+                        static_cast<cudaStream_t>(stream), ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals,
+                        proposal_len, none, static_cast<uint32_t*>(nullptr)),
              "ngram_lookup_kernel launch");
     return TSV_OK;
 }
@@ -173,8 +199,9 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
     A.B = B;
     A.k_max = k_fixed;
     A.policy = TSV_POLICY_PLD;
-    TSV_CUDA(launch_pdl(ngram_lookup_kernel<true>, dim3(B), dim3(kLookupThreads), 0, static_cast<cudaStream_t>(stream),
-                        ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, A, counter),
+    TSV_CUDA(launch_pdl(ngram_lookup_kernel<true>, dim3(B), dim3(kLookupThreads), 0,
+                        static_cast<cudaStream_t>(stream), ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals,
+                        proposal_len, A, counter),
              "ngram_lookup_kernel launch");
     return TSV_OK;
 }

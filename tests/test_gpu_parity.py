@@ -314,6 +314,25 @@ def test_lookup_long_unstaged_and_unaligned(tsv):
     assert_lookup_parity(tsv, ctx, offs, 2, 4, 7)
 
 
+@pytest.mark.parametrize("n_min,n_max", [(1, 5), (3, 9), (1, 64), (64, 64)])
+def test_lookup_long_ngrams(tsv, n_min, n_max):
+    # periodic contexts with a small alphabet: suffix matches far longer than 4 tokens
+    # exercise the walk beyond the branch-free 4-token window
+    rng = np.random.Generator(np.random.PCG64(n_max))
+    ctxs = []
+    for b in range(40):
+        period = int(rng.integers(1, 90))
+        L = int(rng.integers(0, 700))
+        base = rng.integers(0, 3, period).astype(np.int32)
+        c = np.resize(base, L)
+        if L and b % 3 == 0:
+            c[rng.integers(0, L, 1 + L // 50)] = rng.integers(0, 3)  # break some repeats
+        ctxs.append(c.astype(np.int32))
+    offs = np.zeros(len(ctxs) + 1, np.int32)
+    offs[1:] = np.cumsum([len(c) for c in ctxs])
+    assert_lookup_parity(tsv, np.concatenate(ctxs), offs, n_min, n_max, 15)
+
+
 # --------------------------------------------------------------------------- goodput
 PROFILES = [(synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT), (synth.H100_CASE_TARGET, synth.H100_CASE_DRAFT)]
 
