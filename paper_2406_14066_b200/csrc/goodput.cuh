@@ -11,10 +11,19 @@ constexpr int kGpThreads = 256;
 constexpr int kGpWarps = kGpThreads / 32;
 constexpr int kGpMaxK = TSV_MAX_K + 1;
 
+// Exact warp sum of int64 values with three redux.sync adds: 21-bit limbs (the top one
+// signed) whose 32-lane sums fit in 32 bits; recombined mod 2^64, i.e. exact whenever the
+// true sum fits in int64.
 __device__ __forceinline__ long long warp_sum_i64(long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    return v;
+    const unsigned l0 = static_cast<unsigned>(v) & 0x1FFFFFu;
+    const unsigned l1 = static_cast<unsigned>(v >> 21) & 0x1FFFFFu;
+    const int l2 = static_cast<int>(v >> 42);
+    const unsigned s0 = __reduce_add_sync(0xFFFFFFFFu, l0);
+    const unsigned s1 = __reduce_add_sync(0xFFFFFFFFu, l1);
+    const int s2 = __reduce_add_sync(0xFFFFFFFFu, l2);
+    const unsigned long long r = static_cast<unsigned long long>(s0) + (static_cast<unsigned long long>(s1) << 21) +
+                                 (static_cast<unsigned long long>(static_cast<long long>(s2)) << 42);
+    return static_cast<long long>(r);
 }
 
 __device__ __forceinline__ double fwd_time(const tsv_latency_model& m, double n_ctx, double n_batched) {
@@ -55,10 +64,12 @@ __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
     __shared__ int s_best;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t B = A.B, k_max = A.k_max;
-    long long Lk[kGpMaxK], Nk[kGpMaxK];
+    long long Lk[kGpMaxK];
+    uint32_t Nk[kGpMaxK];  // sum_i min(k, cap_i) <= 15 B
 #pragma unroll
-    for (int k = 0; k < kGpMaxK; ++k) Lk[k] = Nk[k] = 0;
-    long long n_ctx = 0, n_ctx_spec = 0, b_spec = 0;
+    for (int k = 0; k < kGpMaxK; ++k) Lk[k] = 0, Nk[k] = 0;
+    long long n_ctx = 0, n_ctx_spec = 0;
+    uint32_t b_spec = 0;
     const double a_glob = A.alpha_per_request ? 0.0 : __ldcg(A.alpha);
     for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
         const double a = A.alpha_per_request ? __ldcg(A.alpha + i) : a_glob;
@@ -69,27 +80,27 @@ __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
             n_ctx_spec += cl;
             b_spec += 1;
         }
-        double l = 1.0;  // l(a, 0); Horner step l(a, j+1) = fma(a, l(a, j), 1)
+        // l(a, min(k, ci)) for k = 0, 1, ...: one Horner step l(a, j+1) = fma(a, l(a, j), 1)
+        // each time min(k, ci) grows (op-for-op the oracle's fresh evaluation)
+        double l = 1.0;
         long long fix = __double2ll_rn(l * 0x1p32);
-        int32_t jcur = 0;
 #pragma unroll
         for (int k = 0; k < kGpMaxK; ++k) {
-            int32_t ki = k < ci ? k : ci;
-            if (ki < 0) ki = 0;
-            while (jcur < ki) {
-                l = __fma_rn(a, l, 1.0);
-                ++jcur;
-                fix = __double2ll_rn(l * 0x1p32);
+            if (k <= k_max) {
+                if (k >= 1 && k <= ci) {
+                    l = __fma_rn(a, l, 1.0);
+                    fix = __double2ll_rn(l * 0x1p32);
+                }
+                Lk[k] += fix;
+                Nk[k] += static_cast<uint32_t>(k <= ci ? k : (ci > 0 ? ci : 0));
             }
-            Lk[k] += fix;
-            Nk[k] += ki;
         }
     }
 #pragma unroll
     for (int k = 0; k < kGpMaxK; ++k) {
         if (k <= k_max) {
             const long long l = warp_sum_i64(Lk[k]);
-            const long long n = warp_sum_i64(Nk[k]);
+            const long long n = __reduce_add_sync(0xFFFFFFFFu, Nk[k]);
             if (lane == 0) {
                 sL[warp][k] = l;
                 sN[warp][k] = n;
@@ -98,11 +109,11 @@ __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
     }
     n_ctx = warp_sum_i64(n_ctx);
     n_ctx_spec = warp_sum_i64(n_ctx_spec);
-    b_spec = warp_sum_i64(b_spec);
+    const long long b_spec_w = __reduce_add_sync(0xFFFFFFFFu, b_spec);
     if (lane == 0) {
         sC[warp][0] = n_ctx;
         sC[warp][1] = n_ctx_spec;
-        sC[warp][2] = b_spec;
+        sC[warp][2] = b_spec_w;
     }
     __syncthreads();
     if (warp == 0) {
