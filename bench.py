@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--chunk", type=int, default=0)
-    ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k and verify+update calls")
+    ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
     return ap.parse_args()
 
@@ -270,7 +270,7 @@ def run_ours(args, rank, world, local_rank):
     breakdown = None
     if args.breakdown:
         breakdown = {}
-        for comp in ("lookup", "choose_k", "verify", "update"):
+        for comp in ("lookup", "choose_k", "verify", "update", "verify_update"):
             cg = torch.cuda.CUDAGraph()
             with torch.cuda.stream(side):
                 st.run_component(comp, 0, stream=side)

@@ -249,9 +249,10 @@ TSV_API tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, con
 
 /* Fused Accept + UpdateGlobalAcceptance (Listing 1 lines 18-19): tsv_verify_accept
  * followed by tsv_update_acceptance(alpha, per_request, a->num_accepted,
- * a->row_offsets, a->B, decay, estimator), with the update run by the last CTA of
- * verify's final kernel.  Outputs identical to the two separate calls; same
- * workspace as tsv_verify_accept. */
+ * a->row_offsets, a->B, decay, estimator), with the update run by one extra CTA
+ * of verify's final (emit) kernel -- the accepted counts are final after the
+ * acceptance scan, so it needs no handshake.  Outputs identical to the two
+ * separate calls; same workspace as tsv_verify_accept. */
 TSV_API tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                     double decay, int32_t estimator, void* stream);
 

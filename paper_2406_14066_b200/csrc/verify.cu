@@ -43,7 +43,6 @@ struct RaceParams {
     int32_t* out_tokens;
     int32_t* devstatus;
     ReqMeta* meta;             // [B]
-    uint32_t* counter;         // arrival counter of the fused emit + update (reset by the scan)
     uint32_t* rowT;            // [n_key_rows] shared race threshold per raced row (float bits)
     unsigned long long* rowkey;  // [n_key_rows] max race key per raced row (0: nothing evaluated)
     tsv_shard_tuple* tuples;   // shard mode
@@ -254,7 +253,6 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     const uint32_t rej = ~accm & kmask;
     const int32_t m = rej ? (__ffs(rej) - 1) : (ok == 1 ? k : -1);
     const int32_t xm = __shfl_sync(0xFFFFFFFFu, x, (m >= 0 ? m : 0) & 31);
-    if (i == 0 && lane == 0) *P.counter = 0u;
     if (MODE == kLazy) {
         if (lane == 0) {
             P.rowT[i] = 0u;
@@ -277,6 +275,7 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
         P.meta[i] = rm;
     }
     if (MODE == kLazy) {
+        if (lane == 0) P.num_accepted[i] = m;  // final here (-1: bad request); the update may read it
         if (ok != 1) {
             emit(P, i, 0, -1, -1);
             if (lane == 0) report(P.devstatus, ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
@@ -439,14 +438,19 @@ __device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
     }
 }
 
-// UPDATE: the CTA that finishes last also runs UpdateGlobalAcceptance (Listing 1 line 19)
-// on the accepted counts just emitted -- the alpha update fused into the verify call.
+// UPDATE: one extra CTA (the last) runs UpdateGlobalAcceptance (Listing 1 line 19) next to
+// the emitting CTAs -- the alpha update fused into the verify call.  It needs only the
+// accepted counts, which the scan kernel already wrote (complete and visible here, two
+// kernels back), so no inter-CTA handshake is needed.
 template <int MODE, bool PRUNE, bool UPDATE>
 __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P, UpdateArgs ua) {
     pdl_wait();
     pdl_launch_dependents();
+    if (UPDATE && blockIdx.x == gridDim.x - 1) {
+        update_block(ua);
+        return;
+    }
     emit_unit<MODE, PRUNE>(P, blockIdx.x * 8 + (threadIdx.x >> 5));
-    if (UPDATE && last_cta_done(P.counter, gridDim.x)) update_block(ua);
 }
 
 // ------------------------------------------------------------------------ shard combine
@@ -571,8 +575,7 @@ static RaceParams make_params(const tsv_verify_args* a) {
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);
     (void)n_chunks;
     char* ws = static_cast<char*>(a->workspace);
-    P.counter = reinterpret_cast<uint32_t*>(ws);
-    ws += 256;
+    ws += 256;  // reserved header
     P.meta = reinterpret_cast<ReqMeta*>(ws);
     ws += align256(sizeof(ReqMeta) * static_cast<size_t>(a->B));
     P.rowT = reinterpret_cast<uint32_t*>(ws);
@@ -617,7 +620,7 @@ static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_
     if (a->q) rs = prune ? launch_race<MODE, true, true>(P, st) : launch_race<MODE, true, false>(P, st);
     else rs = prune ? launch_race<MODE, false, true>(P, st) : launch_race<MODE, false, false>(P, st);
     TSV_TRY(rs);
-    const unsigned emit_blocks = static_cast<unsigned>((a->B + 7) / 8);
+    const unsigned emit_blocks = static_cast<unsigned>((a->B + 7) / 8) + (ua ? 1u : 0u);
     const UpdateArgs none = {};
     cudaError_t e;
     if (ua) e = prune ? launch_pdl(verify_emit_kernel<MODE, true, true>, dim3(emit_blocks), dim3(256), 0, st, P, *ua)

@@ -72,11 +72,11 @@ class StepInputs:
 class SpecStep:
     """Preallocated outputs + the step's launches; eager ``run`` or CUDA-graph ``capture``/``replay``.
 
-    fused=False (default): the four separate ABI calls, 6 kernels chained with PDL.
-    fused=True: tsv_propose_lookup_choose_k + tsv_verify_accept_update, 4 kernels (the last
-    CTA of lookup / emit runs choose-k / the update).  Identical outputs
-    (tests/test_gpu_parity.py); measured on B200 the PDL chain is ~2 us faster per step
-    than the last-CTA handshakes, hence the default."""
+    fused=False (default): tsv_propose_lookup, tsv_goodput_choose_k, tsv_verify_accept_update
+    -- 5 kernels chained with PDL (the alpha update is an extra CTA of verify's emit kernel).
+    fused=True: tsv_propose_lookup_choose_k (the lookup CTA that finishes last runs choose-k)
+    + tsv_verify_accept_update, 4 kernels.  Identical outputs (tests/test_gpu_parity.py);
+    the last-CTA handshake costs more than the kernel boundary it saves on B200."""
 
     def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0, fused: bool = False):
         self.inp = inp
@@ -108,7 +108,7 @@ class SpecStep:
 
     @property
     def launches_per_step(self) -> int:
-        return 4 if self.fused else 6
+        return 4 if self.fused else 5
 
     def run(self, step: int, stream=None):
         """Launch one decode step on ``stream`` (default: current)."""
@@ -139,10 +139,8 @@ class SpecStep:
                                           self.goodput.data_ptr(), self.k_req.data_ptr(), st))
         a = self.args[s]
         a.step = step & 0xFFFFFFFF
-        tsv._check(L.tsv_verify_accept(tsv.ctypes.byref(a), st))
-        tsv._check(L.tsv_update_acceptance(self.alpha.data_ptr(), 0, self.num_accepted.data_ptr(),
-                                           inp.verify[s].row_offsets.data_ptr(), inp.B, 0.9,
-                                           tsv.EST_TESTED, st))
+        tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
+                                              tsv.EST_TESTED, st))
 
     def run_component(self, name: str, step: int, stream=None):
         """One launch of a single step component (timing breakdown only)."""
@@ -165,6 +163,11 @@ class SpecStep:
             a = self.args[s]
             a.step = step & 0xFFFFFFFF
             tsv._check(L.tsv_verify_accept(tsv.ctypes.byref(a), st))
+        elif name == "verify_update":
+            a = self.args[s]
+            a.step = step & 0xFFFFFFFF
+            tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
+                                                  tsv.EST_TESTED, st))
         elif name == "update":
             tsv._check(L.tsv_update_acceptance(self.alpha.data_ptr(), 0, self.num_accepted.data_ptr(),
                                                inp.verify[s].row_offsets.data_ptr(), inp.B, 0.9,
