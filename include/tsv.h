@@ -276,6 +276,50 @@ TSV_API tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_comm*
 TSV_API tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* comm, void* stream);
 
 /* --------------------------------------------------------------------------
+ * Request-sharded goodput and alpha update (one exchange step).
+ * Every batch-level quantity ArgMaxGoodput and
+ * UpdateGlobalAcceptance need is an exact integer sum over
+ * requests, so each rank reduces its own requests and the element-wise sum
+ * over ranks equals the unsharded batch's sums: k*, goodput and alpha are bit-
+ * identical to one device holding the whole batch, for any partition.
+ *
+ * tsv_goodput_partial: sums[TSV_GP_SUMS(k_max)] (int64, device) of this rank's
+ *   B >= 0 requests: [0..K] L(k) = sum_i rint(2^32 l(alpha_i, min(k, cap_i))),
+ *   [K+1..2K+1] N(k) = sum_i min(k, cap_i), then sum ctx_len, sum ctx_len over
+ *   cap_i > 0, #{cap_i > 0}, B.  Arguments as tsv_goodput_choose_k.
+ * tsv_goodput_finalize: ArgMaxGoodput on (summed) sums -> k_out, goodput_out
+ *   [k_max+1] (nullable); k_per_request[i] = min(k*, cap[i]) for this rank's
+ *   B_local requests (both nullable).
+ * tsv_goodput_choose_k_sharded: partial -> ncclAllReduce(sum) -> finalize on
+ *   `stream`; sums_ws: int64[TSV_GP_SUMS(k_max)] device scratch.
+ * tsv_update_partial: sums[2] = (sum_i m_i, sum_i t_i) over valid requests
+ *   (t_i per `estimator`); tsv_update_finalize: alpha' = fma(d, alpha - r, r),
+ *   r = sum_m / sum_t, unchanged when sum_t = 0 (global alpha only).
+ * tsv_update_acceptance_sharded: partial -> ncclAllReduce(sum) -> finalize;
+ *   sums_ws: int64[2] device scratch.
+ * ------------------------------------------------------------------------ */
+#define TSV_GP_SUMS(k_max) (2 * ((k_max) + 1) + 4)
+TSV_API tsv_status tsv_goodput_partial(const double* alpha, int32_t alpha_per_request, const int32_t* ctx_len,
+                                       const int32_t* cap, int32_t B, int32_t k_max, int64_t* sums, void* stream);
+TSV_API tsv_status tsv_goodput_finalize(const int64_t* sums, int32_t k_max, int32_t policy, tsv_latency_model target,
+                                        tsv_latency_model draft, double pld_cost_ms, int64_t kv_free_slots,
+                                        const int32_t* cap, int32_t B_local, int32_t* k_out, double* goodput_out,
+                                        int32_t* k_per_request, void* stream);
+TSV_API tsv_status tsv_goodput_choose_k_sharded(const double* alpha, int32_t alpha_per_request,
+                                                const int32_t* ctx_len, const int32_t* cap, int32_t B, int32_t k_max,
+                                                int32_t policy, tsv_latency_model target, tsv_latency_model draft,
+                                                double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
+                                                double* goodput_out, int32_t* k_per_request, int64_t* sums_ws,
+                                                tsv_comm* comm, void* stream);
+TSV_API tsv_status tsv_update_partial(const int32_t* num_accepted, const int32_t* row_offsets, int32_t B,
+                                      int32_t estimator, int64_t* sums, void* stream);
+TSV_API tsv_status tsv_update_finalize(double* alpha, const int64_t* sums, double decay, void* stream);
+TSV_API tsv_status tsv_update_acceptance_sharded(double* alpha, const int32_t* num_accepted,
+                                                 const int32_t* row_offsets, int32_t B, double decay,
+                                                 int32_t estimator, int64_t* sums_ws, tsv_comm* comm,
+                                                 void* stream);
+
+/* --------------------------------------------------------------------------
  * Diagnostics (used by the GPU tests; not on the hot path).
  * tsv_debug_race_E: out[t] = E(u) of the race uniform u = (2(m_begin+t)+1) 2^-24
  *   exactly as the race kernels evaluate it (series near u = 1, double log

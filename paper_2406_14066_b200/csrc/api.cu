@@ -191,6 +191,32 @@ extern "C" tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* c
                        "ncclAllReduce");
 }
 
+extern "C" tsv_status tsv_goodput_choose_k_sharded(const double* alpha, int32_t alpha_per_request,
+                                                   const int32_t* ctx_len, const int32_t* cap, int32_t B,
+                                                   int32_t k_max, int32_t policy, tsv_latency_model target,
+                                                   tsv_latency_model draft, double pld_cost_ms,
+                                                   int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
+                                                   int32_t* k_per_request, int64_t* sums_ws, tsv_comm* comm,
+                                                   void* stream) {
+    TSV_REQUIRE(comm && sums_ws, "tsv_goodput_choose_k_sharded: NULL argument");
+    TSV_TRY(nccl_ready());
+    TSV_TRY(tsv_goodput_partial(alpha, alpha_per_request, ctx_len, cap, B, k_max, sums_ws, stream));
+    TSV_TRY(tsv_allreduce_i64(sums_ws, TSV_GP_SUMS(k_max), comm, stream));
+    return tsv_goodput_finalize(sums_ws, k_max, policy, target, draft, pld_cost_ms, kv_free_slots, cap, B, k_out,
+                                goodput_out, k_per_request, stream);
+}
+
+extern "C" tsv_status tsv_update_acceptance_sharded(double* alpha, const int32_t* num_accepted,
+                                                    const int32_t* row_offsets, int32_t B, double decay,
+                                                    int32_t estimator, int64_t* sums_ws, tsv_comm* comm,
+                                                    void* stream) {
+    TSV_REQUIRE(comm && sums_ws && alpha, "tsv_update_acceptance_sharded: NULL argument");
+    TSV_TRY(nccl_ready());
+    TSV_TRY(tsv_update_partial(num_accepted, row_offsets, B, estimator, sums_ws, stream));
+    TSV_TRY(tsv_allreduce_i64(sums_ws, 2, comm, stream));
+    return tsv_update_finalize(alpha, sums_ws, decay, stream);
+}
+
 // ------------------------------------------------------------------ diagnostics (tests)
 namespace tsv {
 __global__ void debug_race_E_kernel(uint32_t m_begin, uint32_t n, float* out) {

@@ -27,9 +27,153 @@ __global__ void __launch_bounds__(kGpThreads) update_acceptance_kernel(const Upd
     update_block(A);
 }
 
+// Request-sharded mode: the batch sums of this rank's requests ...
+__global__ void __launch_bounds__(kGpThreads) goodput_partial_kernel(const ChooseArgs A, long long* sums) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const GpTotals t = gp_sums_block(A);
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) == 0) {
+        if (lane <= A.k_max) {
+            sums[lane] = t.L;
+            sums[A.k_max + 1 + lane] = t.N;
+        }
+        if (lane == 0) {
+            long long* c = sums + 2 * (A.k_max + 1);
+            c[0] = t.c0;
+            c[1] = t.c1;
+            c[2] = t.c2;
+            c[3] = t.c3;
+        }
+    }
+}
+
+// ... and, after the element-wise sum over ranks, the argmax on the global sums.
+__global__ void __launch_bounds__(kGpThreads) goodput_finalize_kernel(const ChooseArgs A, const long long* sums) {
+    __shared__ int s_best;
+    pdl_wait();
+    pdl_launch_dependents();
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) == 0) {
+        const long long* c = sums + 2 * (A.k_max + 1);
+        GpTotals t;
+        t.L = lane <= A.k_max ? sums[lane] : 0;
+        t.N = lane <= A.k_max ? sums[A.k_max + 1 + lane] : 0;
+        t.c0 = c[0];
+        t.c1 = c[1];
+        t.c2 = c[2];
+        t.c3 = c[3];
+        const int kb = gp_argmax_warp(A, t);
+        if (lane == 0) s_best = kb;
+    }
+    if (A.k_per_request && A.cap && A.B > 0) {
+        __syncthreads();
+        gp_write_k_per_request(A, s_best);
+    }
+}
+
+__global__ void __launch_bounds__(kGpThreads) update_partial_kernel(const UpdateArgs A, long long* sums) {
+    pdl_wait();
+    pdl_launch_dependents();
+    update_block(A, sums);
+}
+
+__global__ void update_finalize_kernel(double* alpha, const long long* sums, double decay) {
+    pdl_wait();
+    pdl_launch_dependents();
+    if (threadIdx.x == 0) ewma_apply(alpha, sums[0], sums[1], decay);
+}
+
 }  // namespace tsv
 
 using namespace tsv;
+
+extern "C" tsv_status tsv_goodput_partial(const double* alpha, int32_t alpha_per_request, const int32_t* ctx_len,
+                                          const int32_t* cap, int32_t B, int32_t k_max, int64_t* sums,
+                                          void* stream) {
+    TSV_REQUIRE(B >= 0, "tsv_goodput_partial: B < 0 (%d)", B);
+    TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_partial: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
+    TSV_REQUIRE(sums != nullptr, "tsv_goodput_partial: sums is NULL");
+    TSV_REQUIRE(B == 0 || (alpha && ctx_len && cap), "tsv_goodput_partial: a required array is NULL");
+    TSV_TRY(check_device());
+    ChooseArgs A = {};
+    A.alpha = alpha;
+    A.ctx_len = ctx_len;
+    A.cap = cap;
+    A.alpha_per_request = alpha_per_request;
+    A.B = B;
+    A.k_max = k_max;
+    if (B == 0) {  // an empty request set: all sums are zero (alpha is not read)
+        TSV_CUDA(cudaMemsetAsync(sums, 0, sizeof(int64_t) * TSV_GP_SUMS(k_max), static_cast<cudaStream_t>(stream)),
+                 "cudaMemsetAsync");
+        return TSV_OK;
+    }
+    TSV_CUDA(launch_pdl(goodput_partial_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream), A,
+                        reinterpret_cast<long long*>(sums)),
+             "goodput_partial_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_goodput_finalize(const int64_t* sums, int32_t k_max, int32_t policy,
+                                           tsv_latency_model target, tsv_latency_model draft, double pld_cost_ms,
+                                           int64_t kv_free_slots, const int32_t* cap, int32_t B_local,
+                                           int32_t* k_out, double* goodput_out, int32_t* k_per_request,
+                                           void* stream) {
+    TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_finalize: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
+    TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_finalize: unknown policy %d", policy);
+    TSV_REQUIRE(sums && k_out, "tsv_goodput_finalize: a required array is NULL");
+    TSV_REQUIRE(B_local >= 0, "tsv_goodput_finalize: B_local < 0");
+    TSV_REQUIRE(!k_per_request || B_local == 0 || cap, "tsv_goodput_finalize: k_per_request needs cap");
+    TSV_TRY(check_device());
+    ChooseArgs A = {};
+    A.cap = cap;
+    A.k_out = k_out;
+    A.goodput_out = goodput_out;
+    A.k_per_request = k_per_request;
+    A.target = target;
+    A.draft = draft;
+    A.pld_cost_ms = pld_cost_ms;
+    A.kv_free = static_cast<long long>(kv_free_slots);
+    A.B = B_local;
+    A.k_max = k_max;
+    A.policy = policy;
+    TSV_CUDA(launch_pdl(goodput_finalize_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream), A,
+                        reinterpret_cast<const long long*>(sums)),
+             "goodput_finalize_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_update_partial(const int32_t* num_accepted, const int32_t* row_offsets, int32_t B,
+                                         int32_t estimator, int64_t* sums, void* stream) {
+    TSV_REQUIRE(B >= 0, "tsv_update_partial: B < 0");
+    TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED, "tsv_update_partial: unknown estimator");
+    TSV_REQUIRE(sums != nullptr, "tsv_update_partial: sums is NULL");
+    TSV_REQUIRE(B == 0 || (num_accepted && row_offsets), "tsv_update_partial: a required array is NULL");
+    TSV_TRY(check_device());
+    if (B == 0) {
+        TSV_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(int64_t), static_cast<cudaStream_t>(stream)), "cudaMemsetAsync");
+        return TSV_OK;
+    }
+    UpdateArgs A = {};
+    A.num_accepted = num_accepted;
+    A.row_offsets = row_offsets;
+    A.B = B;
+    A.estimator = estimator;
+    TSV_CUDA(launch_pdl(update_partial_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream), A,
+                        reinterpret_cast<long long*>(sums)),
+             "update_partial_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_update_finalize(double* alpha, const int64_t* sums, double decay, void* stream) {
+    TSV_REQUIRE(alpha && sums, "tsv_update_finalize: NULL argument");
+    TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_update_finalize: decay %g outside [0, 1]", decay);
+    TSV_TRY(check_device());
+    TSV_CUDA(launch_pdl(update_finalize_kernel, dim3(1), dim3(32), 0, static_cast<cudaStream_t>(stream), alpha,
+                        reinterpret_cast<const long long*>(sums), decay),
+             "update_finalize_kernel launch");
+    return TSV_OK;
+}
 
 extern "C" tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_per_request,
                                            const int32_t* ctx_len, const int32_t* cap, int32_t B,

@@ -51,17 +51,23 @@ struct UpdateArgs {
     int32_t per_request, B, estimator;
 };
 
-// ArgMaxGoodput over one CTA of kGpThreads threads (all threads must call).  Inputs are read
-// with ld.global.cg so values written by other CTAs of a fused kernel are seen.
-// Each thread accumulates, for every candidate k, the fixed-point token sum
-// L(k) = sum_i rint(2^32 l(alpha_i, min(k, cap_i))) and sum_i min(k, cap_i); one warp
-// reduction + one shared-memory step give the totals; lane k of warp 0 then evaluates
-// T(k) and G(k) in parallel and lane 0 runs Listing 2's strict-'>' scan over k.
-__device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
+// Batch sums of ArgMaxGoodput, exact int64 (fixed point 2^-32 for the token sums):
+//   L[k] = sum_i rint(2^32 l(alpha_i, min(k, cap_i))),  N[k] = sum_i min(k, cap_i),
+//   c[0] = sum_i ctx_len_i,  c[1] = sum over cap_i > 0 of ctx_len_i,  c[2] = #{cap_i > 0},
+//   c[3] = B.
+// Sums over disjoint request sets add up to the sums of their union (request-sharded mode).
+struct GpTotals {  // per lane k of warp 0: L[k], N[k]; every lane: c[0..3]
+    long long L, N, c0, c1, c2, c3;
+};
+
+// CTA-wide (all kGpThreads threads call); the result is valid in warp 0.
+// Each thread accumulates its requests for every candidate k (the Horner recurrence
+// l(a, j+1) = fma(a, l(a, j), 1) advanced once each time min(k, cap_i) grows, op-for-op a
+// fresh evaluation); warp sums are exact redux.sync limb sums, then one shared-memory step.
+__device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A) {
     __shared__ long long sL[kGpWarps][kGpMaxK];
     __shared__ long long sN[kGpWarps][kGpMaxK];
     __shared__ long long sC[kGpWarps][3];
-    __shared__ int s_best;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t B = A.B, k_max = A.k_max;
     long long Lk[kGpMaxK];
@@ -80,8 +86,6 @@ __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
             n_ctx_spec += cl;
             b_spec += 1;
         }
-        // l(a, min(k, ci)) for k = 0, 1, ...: one Horner step l(a, j+1) = fma(a, l(a, j), 1)
-        // each time min(k, ci) grows (op-for-op the oracle's fresh evaluation)
         double l = 1.0;
         long long fix = __double2ll_rn(l * 0x1p32);
 #pragma unroll
@@ -116,67 +120,100 @@ __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
         sC[warp][2] = b_spec_w;
     }
     __syncthreads();
+    GpTotals t = {0, 0, 0, 0, 0, static_cast<long long>(B)};
     if (warp == 0) {
-        long long c0 = 0, c1 = 0, c2 = 0;
 #pragma unroll
         for (int w = 0; w < kGpWarps; ++w) {
-            c0 += sC[w][0];
-            c1 += sC[w][1];
-            c2 += sC[w][2];
+            t.c0 += sC[w][0];
+            t.c1 += sC[w][1];
+            t.c2 += sC[w][2];
         }
-        double g = -1.0;
-        bool valid = false;
         if (lane <= k_max) {
-            long long L = 0, N = 0;
 #pragma unroll
             for (int w = 0; w < kGpWarps; ++w) {
-                L += sL[w][lane];
-                N += sN[w][lane];
-            }
-            const long long n_batched = N + static_cast<long long>(B);
-            if (!(lane > 0 && A.kv_free >= 0 && n_batched > A.kv_free)) {  // Listing 2 line 5: OOM -> skip
-                const double t_target = fwd_time(A.target, static_cast<double>(c0), static_cast<double>(n_batched));
-                double t_draft;
-                if (A.policy == TSV_POLICY_PLD)
-                    t_draft = A.pld_cost_ms;
-                else
-                    t_draft = lane > 0 ? __dmul_rn(static_cast<double>(lane),
-                                                   fwd_time(A.draft, static_cast<double>(c1), static_cast<double>(c2)))
-                                       : 0.0;
-                g = __ddiv_rn(__dmul_rn(static_cast<double>(L), 0x1p-32), __dadd_rn(t_target, t_draft));
-                valid = true;
-            }
-            if (A.goodput_out) A.goodput_out[lane] = g;
-        }
-        // Listing 2: max_goodput = -1; for k: if goodput > max_goodput: take k (strict >)
-        double max_goodput = -1.0;
-        int best_k = 0;
-        for (int k = 0; k <= k_max; ++k) {
-            const double gk = __shfl_sync(0xFFFFFFFFu, g, k);
-            const bool vk = __shfl_sync(0xFFFFFFFFu, valid, k);
-            if (vk && gk > max_goodput) {
-                max_goodput = gk;
-                best_k = k;
+                t.L += sL[w][lane];
+                t.N += sN[w][lane];
             }
         }
-        if (lane == 0) {
-            *A.k_out = best_k;
-            s_best = best_k;
+    }
+    return t;
+}
+
+// Warp 0 only: lane k evaluates T(k) and G(k) from the totals, lane 0 runs Listing 2's
+// strict-'>' scan over k = 0..k_max (k = 0 included, reading R12); writes k_out and
+// goodput_out; returns k* in every lane.
+__device__ __forceinline__ int gp_argmax_warp(const ChooseArgs& A, const GpTotals& t) {
+    const int lane = threadIdx.x & 31;
+    const int32_t k_max = A.k_max;
+    double g = -1.0;
+    bool valid = false;
+    if (lane <= k_max) {
+        const long long n_batched = t.N + t.c3;
+        if (!(lane > 0 && A.kv_free >= 0 && n_batched > A.kv_free)) {  // Listing 2 line 5: OOM -> skip
+            const double t_target = fwd_time(A.target, static_cast<double>(t.c0), static_cast<double>(n_batched));
+            double t_draft;
+            if (A.policy == TSV_POLICY_PLD)
+                t_draft = A.pld_cost_ms;
+            else
+                t_draft = lane > 0 ? __dmul_rn(static_cast<double>(lane),
+                                               fwd_time(A.draft, static_cast<double>(t.c1), static_cast<double>(t.c2)))
+                                   : 0.0;
+            g = __ddiv_rn(__dmul_rn(static_cast<double>(t.L), 0x1p-32), __dadd_rn(t_target, t_draft));
+            valid = true;
         }
+        if (A.goodput_out) A.goodput_out[lane] = g;
+    }
+    // Listing 2: max_goodput = -1; for k: if goodput > max_goodput: take k (strict >)
+    double max_goodput = -1.0;
+    int best_k = 0;
+    for (int k = 0; k <= k_max; ++k) {
+        const double gk = __shfl_sync(0xFFFFFFFFu, g, k);
+        const bool vk = __shfl_sync(0xFFFFFFFFu, valid, k);
+        if (vk && gk > max_goodput) {
+            max_goodput = gk;
+            best_k = k;
+        }
+    }
+    if (lane == 0) *A.k_out = best_k;
+    return best_k;
+}
+
+// k_i = min(k*, cap_i) for this CTA's requests (all threads; k* from shared memory).
+__device__ __forceinline__ void gp_write_k_per_request(const ChooseArgs& A, int kb) {
+    for (int32_t i = threadIdx.x; i < A.B; i += kGpThreads) {
+        const int32_t ci = __ldcg(A.cap + i);
+        const int32_t ki = kb < ci ? kb : ci;
+        A.k_per_request[i] = ki < 0 ? 0 : ki;
+    }
+}
+
+// ArgMaxGoodput over one CTA of kGpThreads threads (all threads must call).  Inputs are read
+// with ld.global.cg so values written by other CTAs of a fused kernel are seen.
+__device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
+    __shared__ int s_best;
+    const GpTotals t = gp_sums_block(A);
+    if ((threadIdx.x >> 5) == 0) {
+        const int kb = gp_argmax_warp(A, t);
+        if (threadIdx.x == 0) s_best = kb;
     }
     if (A.k_per_request) {
         __syncthreads();
-        const int32_t kb = s_best;
-        for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
-            const int32_t ci = __ldcg(A.cap + i);
-            const int32_t ki = kb < ci ? kb : ci;
-            A.k_per_request[i] = ki < 0 ? 0 : ki;
-        }
+        gp_write_k_per_request(A, s_best);
+    }
+}
+
+// alpha' = fma(d, alpha - r, r), r = RN64(sum_m / sum_t); no update when sum_t == 0.
+__device__ __forceinline__ void ewma_apply(double* alpha, long long sum_m, long long sum_t, double decay) {
+    if (sum_t > 0) {
+        const double r = __ddiv_rn(static_cast<double>(sum_m), static_cast<double>(sum_t));
+        *alpha = __fma_rn(decay, __dsub_rn(*alpha, r), r);
     }
 }
 
 // UpdateGlobalAcceptance over one CTA of kGpThreads threads (all threads must call).
-__device__ __forceinline__ void update_block(const UpdateArgs& A) {
+// Global mode: the exact int64 sums (sum_m, sum_t) land in thread 0 and are either applied
+// (sums_out == nullptr) or written to sums_out[0..1] (request-sharded partial).
+__device__ __forceinline__ void update_block(const UpdateArgs& A, long long* sums_out = nullptr) {
     __shared__ long long red[kGpWarps][2];
     long long sm = 0, stt = 0;
     for (int32_t i = threadIdx.x; i < A.B; i += kGpThreads) {
@@ -210,9 +247,11 @@ __device__ __forceinline__ void update_block(const UpdateArgs& A) {
             a += red[w][0];
             b += red[w][1];
         }
-        if (b > 0) {
-            const double r = __ddiv_rn(static_cast<double>(a), static_cast<double>(b));
-            A.alpha[0] = __fma_rn(A.decay, __dsub_rn(A.alpha[0], r), r);
+        if (sums_out) {
+            sums_out[0] = a;
+            sums_out[1] = b;
+        } else {
+            ewma_apply(A.alpha, a, b, A.decay);
         }
     }
 }

@@ -36,7 +36,14 @@ EXPORTED = [
     "tsv_comm_get_unique_id", "tsv_comm_init", "tsv_comm_destroy",
     "tsv_verify_sharded_workspace_size", "tsv_verify_accept_sharded", "tsv_allreduce_i64",
     "tsv_propose_lookup_choose_k", "tsv_verify_accept_update", "tsv_debug_race_E", "tsv_debug_philox",
+    "tsv_goodput_partial", "tsv_goodput_finalize", "tsv_goodput_choose_k_sharded", "tsv_update_partial",
+    "tsv_update_finalize", "tsv_update_acceptance_sharded",
 ]
+
+
+def gp_sums_len(k_max: int) -> int:
+    """TSV_GP_SUMS(k_max): int64 words of a request-sharded goodput partial."""
+    return 2 * (k_max + 1) + 4
 
 
 class TsvError(RuntimeError):
@@ -99,6 +106,14 @@ def _load() -> ctypes.CDLL:
         "tsv_verify_accept_update": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P], ctypes.c_int),
         "tsv_debug_race_E": ([ctypes.c_uint32, ctypes.c_uint32, P, P], ctypes.c_int),
         "tsv_debug_philox": ([P, P, ctypes.c_uint32, P, i32, P], ctypes.c_int),
+        "tsv_goodput_partial": ([P, i32, P, P, i32, i32, P, P], ctypes.c_int),
+        "tsv_goodput_finalize": ([P, i32, i32, LatencyModel, LatencyModel, f64, i64, P, i32, P, P, P, P],
+                                 ctypes.c_int),
+        "tsv_goodput_choose_k_sharded": ([P, i32, P, P, i32, i32, i32, LatencyModel, LatencyModel, f64, i64,
+                                          P, P, P, P, P, P], ctypes.c_int),
+        "tsv_update_partial": ([P, P, i32, i32, P, P], ctypes.c_int),
+        "tsv_update_finalize": ([P, P, f64, P], ctypes.c_int),
+        "tsv_update_acceptance_sharded": ([P, P, P, i32, f64, i32, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -331,6 +346,57 @@ def tsv_update_acceptance(alpha, num_accepted, row_offsets, decay=0.9, estimator
     return alpha
 
 
+# ------------------------------------------------------------- request-sharded goodput / update
+def tsv_goodput_partial(alpha, ctx_len, cap, k_max, alpha_per_request=None, sums=None, stream=None):
+    """This rank's exact int64 batch sums for ArgMaxGoodput (TSV_GP_SUMS(k_max) words)."""
+    B = ctx_len.numel()
+    dev = ctx_len.device
+    _want(ctx_len, torch.int32, None, "ctx_len")
+    _want(cap, torch.int32, B, "cap")
+    per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
+    if sums is None:
+        sums = torch.empty(gp_sums_len(k_max), dtype=torch.int64, device=dev)
+    _check(_lib.tsv_goodput_partial(_ptr(alpha), 1 if per else 0, _ptr(ctx_len), _ptr(cap), B, int(k_max),
+                                    _ptr(sums), _stream(stream)))
+    return sums
+
+
+def tsv_goodput_finalize(sums, k_max, policy, target, draft=(0.0, 0.0, 0.0), pld_cost_ms=0.0,
+                         kv_free_slots=-1, cap=None, k_out=None, goodput_out=None, k_per_request=None,
+                         stream=None):
+    """ArgMaxGoodput on (rank-summed) sums; k_per_request = min(k*, cap) for the local requests."""
+    dev = sums.device
+    _want(sums, torch.int64, gp_sums_len(k_max), "sums")
+    if k_out is None:
+        k_out = torch.empty(1, dtype=torch.int32, device=dev)
+    if goodput_out is None:
+        goodput_out = torch.empty(k_max + 1, dtype=torch.float64, device=dev)
+    B_local = 0 if cap is None else cap.numel()
+    _check(_lib.tsv_goodput_finalize(_ptr(sums), int(k_max), int(policy), LatencyModel(*target),
+                                     LatencyModel(*draft), float(pld_cost_ms), int(kv_free_slots), _ptr(cap),
+                                     B_local, _ptr(k_out), _ptr(goodput_out), _ptr(k_per_request),
+                                     _stream(stream)))
+    return k_out, goodput_out, k_per_request
+
+
+def tsv_update_partial(num_accepted, row_offsets, estimator=EST_TESTED, sums=None, stream=None):
+    """This rank's (sum m_i, sum t_i) as int64[2]."""
+    B = num_accepted.numel()
+    _want(row_offsets, torch.int32, B + 1, "row_offsets")
+    if sums is None:
+        sums = torch.empty(2, dtype=torch.int64, device=num_accepted.device)
+    _check(_lib.tsv_update_partial(_ptr(num_accepted), _ptr(row_offsets), B, int(estimator), _ptr(sums),
+                                   _stream(stream)))
+    return sums
+
+
+def tsv_update_finalize(alpha, sums, decay=0.9, stream=None):
+    _want(alpha, torch.float64, 1, "alpha")
+    _want(sums, torch.int64, 2, "sums")
+    _check(_lib.tsv_update_finalize(_ptr(alpha), _ptr(sums), float(decay), _stream(stream)))
+    return alpha
+
+
 # ----------------------------------------------------------------------------- comm
 class Comm:
     """NCCL communicator owned by libtsv; the unique id travels over torch.distributed."""
@@ -363,6 +429,40 @@ def tsv_verify_sharded_workspace_size(args: VerifyArgs, world: int) -> int:
 
 def tsv_verify_accept_sharded(args: VerifyArgs, comm: Comm, stream=None):
     _check(_lib.tsv_verify_accept_sharded(ctypes.byref(args), comm.handle, _stream(stream)))
+
+
+def tsv_goodput_choose_k_sharded(alpha, ctx_len, cap, k_max, policy, target, comm: "Comm",
+                                 draft=(0.0, 0.0, 0.0), pld_cost_ms=0.0, kv_free_slots=-1,
+                                 alpha_per_request=None, k_out=None, goodput_out=None, k_per_request=None,
+                                 sums_ws=None, stream=None):
+    """Request-sharded ArgMaxGoodput: partial -> ncclAllReduce(sum, int64) -> finalize."""
+    B = ctx_len.numel()
+    dev = ctx_len.device
+    per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
+    if k_out is None:
+        k_out = torch.empty(1, dtype=torch.int32, device=dev)
+    if goodput_out is None:
+        goodput_out = torch.empty(k_max + 1, dtype=torch.float64, device=dev)
+    if sums_ws is None:
+        sums_ws = torch.empty(gp_sums_len(k_max), dtype=torch.int64, device=dev)
+    _check(_lib.tsv_goodput_choose_k_sharded(_ptr(alpha), 1 if per else 0, _ptr(ctx_len), _ptr(cap), B,
+                                             int(k_max), int(policy), LatencyModel(*target),
+                                             LatencyModel(*draft), float(pld_cost_ms), int(kv_free_slots),
+                                             _ptr(k_out), _ptr(goodput_out), _ptr(k_per_request),
+                                             _ptr(sums_ws), comm.handle, _stream(stream)))
+    return k_out, goodput_out, k_per_request
+
+
+def tsv_update_acceptance_sharded(alpha, num_accepted, row_offsets, comm: "Comm", decay=0.9,
+                                  estimator=EST_TESTED, sums_ws=None, stream=None):
+    """Request-sharded global alpha update: partial -> ncclAllReduce(sum, int64) -> finalize."""
+    B = num_accepted.numel()
+    if sums_ws is None:
+        sums_ws = torch.empty(2, dtype=torch.int64, device=num_accepted.device)
+    _check(_lib.tsv_update_acceptance_sharded(_ptr(alpha), _ptr(num_accepted), _ptr(row_offsets), B,
+                                              float(decay), int(estimator), _ptr(sums_ws), comm.handle,
+                                              _stream(stream)))
+    return alpha
 
 
 def tsv_allreduce_i64(data: torch.Tensor, comm: Comm, stream=None):

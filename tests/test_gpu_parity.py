@@ -398,6 +398,101 @@ def test_update_parity(tsv):
                 assert (got.view(np.uint64) == np.atleast_1d(want).view(np.uint64)).all()
 
 
+# ------------------------------------------------------- request-sharded goodput / update (8e)
+def _random_partition(rng, B, G):
+    """G disjoint request subsets (some possibly empty), contiguous or scattered."""
+    if rng.random() < 0.5:
+        cuts = np.sort(rng.integers(0, B + 1, G - 1))
+        bounds = np.concatenate([[0], cuts, [B]])
+        return [np.arange(bounds[g], bounds[g + 1]) for g in range(G)]
+    owner = rng.integers(0, G, B)
+    return [np.flatnonzero(owner == g) for g in range(G)]
+
+
+def test_goodput_sharded_sums_equal_oracle(tsv):
+    # each "rank" reduces its own requests; the element-wise sum of the partials, finalized,
+    # must give the oracle's k* and goodput bit for bit for any partition (exact int64 sums)
+    rng = np.random.Generator(np.random.PCG64(8))
+    for trial in range(60):
+        B = int(rng.integers(1, 400))
+        K = int(rng.integers(1, 9))
+        ctx, _ = synth.make_goodput_instance(B, K, seed=100 + trial)
+        cap = rng.integers(0, K + 1, B).astype(np.int32)
+        per = trial % 2 == 1
+        alpha = rng.uniform(0, 1, B) if per else float(rng.uniform(0.05, 0.95))
+        kv = int(rng.integers(-1, 3 * B)) if trial % 3 == 0 else -1
+        pol = trial % 2
+        target, draft = PROFILES[trial % 2]
+        ok, og = oracle.choose_k(alpha, ctx, cap, K, pol, target, draft, pld_cost_ms=0.05, kv_free_slots=kv)
+        G = int(rng.integers(1, 9))
+        parts = _random_partition(rng, B, G)
+        total = torch.zeros(tsv.gp_sums_len(K), dtype=torch.int64, device=DEV)
+        a_all = np.atleast_1d(np.asarray(alpha, np.float64))
+        for idx in parts:
+            a = torch.tensor(a_all[idx] if per else a_all, device=DEV)
+            c = torch.tensor(ctx[idx], device=DEV)
+            cp = torch.tensor(cap[idx], device=DEV)
+            total += tsv.tsv_goodput_partial(a, c, cp, K, alpha_per_request=per)
+        kpr_parts = []
+        for idx in parts:  # every rank finalizes the same global sums; k_i for its own requests
+            cp = torch.tensor(cap[idx], device=DEV)
+            kpr = torch.empty_like(cp)
+            k, g, _ = tsv.tsv_goodput_finalize(total, K, pol, target, draft, 0.05, kv, cap=cp, k_per_request=kpr)
+            torch.cuda.synchronize()
+            assert int(k.item()) == ok, (trial, G)
+            assert (_np(g).view(np.uint64) == og.view(np.uint64)).all(), trial
+            kpr_parts.append((idx, _np(kpr)))
+        for idx, kp in kpr_parts:
+            assert (kp == np.maximum(np.minimum(ok, cap[idx]), 0)).all()
+
+
+def test_update_sharded_sums_equal_oracle(tsv):
+    rng = np.random.Generator(np.random.PCG64(9))
+    for trial in range(40):
+        B = int(rng.integers(1, 500))
+        ks = rng.integers(0, 9, B)
+        m = np.minimum(rng.geometric(0.3, B) - 1, ks).astype(np.int32)
+        m[rng.random(B) < 0.02] = -1
+        est = trial % 2
+        a0 = float(rng.uniform(0, 1))
+        want = oracle.update(a0, m, np.concatenate([[0], np.cumsum(ks + 1)]).astype(np.int32), 0.9, est)
+        total = torch.zeros(2, dtype=torch.int64, device=DEV)
+        for idx in _random_partition(rng, B, int(rng.integers(1, 9))):
+            ro = np.zeros(len(idx) + 1, np.int32)
+            ro[1:] = np.cumsum(ks[idx] + 1)
+            total += tsv.tsv_update_partial(torch.tensor(m[idx], device=DEV), torch.tensor(ro, device=DEV), est)
+        a = torch.tensor([a0], dtype=torch.float64, device=DEV)
+        tsv.tsv_update_finalize(a, total, 0.9)
+        assert (_np(a).view(np.uint64) == np.atleast_1d(want).view(np.uint64)).all()
+
+
+def test_sharded_goodput_and_update_nccl_world1(tsv):
+    # the NCCL plumbing (partial -> ncclAllReduce -> finalize) on a one-rank communicator
+    comm = tsv.Comm(0, 1)
+    try:
+        B, K = 300, 5
+        ctx, _ = synth.make_goodput_instance(B, K, seed=5)
+        cap = np.random.Generator(np.random.PCG64(5)).integers(0, K + 1, B).astype(np.int32)
+        for pol in (0, 1):
+            ok, og = oracle.choose_k(0.7, ctx, cap, K, pol, synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT,
+                                     pld_cost_ms=0.05)
+            a = torch.tensor([0.7], dtype=torch.float64, device=DEV)
+            k, g, _ = tsv.tsv_goodput_choose_k_sharded(a, torch.tensor(ctx, device=DEV),
+                                                       torch.tensor(cap, device=DEV), K, pol,
+                                                       synth.SPEC_DESK_TARGET, comm, synth.SPEC_DESK_DRAFT, 0.05)
+            torch.cuda.synchronize()
+            assert int(k.item()) == ok and (_np(g).view(np.uint64) == og.view(np.uint64)).all()
+        ks = np.full(B, K)
+        m = np.minimum(np.arange(B) % 7, K).astype(np.int32)
+        ro = np.concatenate([[0], np.cumsum(ks + 1)]).astype(np.int32)
+        want = oracle.update(0.5, m, ro, 0.9, 0)
+        a = torch.tensor([0.5], dtype=torch.float64, device=DEV)
+        tsv.tsv_update_acceptance_sharded(a, torch.tensor(m, device=DEV), torch.tensor(ro, device=DEV), comm)
+        assert (_np(a).view(np.uint64) == np.atleast_1d(want).view(np.uint64)).all()
+    finally:
+        comm.close()
+
+
 # ------------------------------------------------------------------- fused entry points
 def test_fused_lookup_choose_k_equals_separate(tsv):
     ctx, offs = synth.make_contexts(B=200, L=2048, seed=21, ragged=True)
