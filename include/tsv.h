@@ -146,6 +146,7 @@ typedef struct tsv_verify_args {
 } tsv_verify_args;
 
 #define TSV_VERIFY_NO_PRUNE 1     /* evaluate every race element exactly (test)     */
+#define TSV_VERIFY_SHARD_DENSE 2  /* tsv_verify_accept_sharded: one-round dense mode  */
 
 /* Workspace: device scratch for per-request scan results and per-chunk race
  * keys (size from tsv_verify_workspace_size; no initialisation needed).  One
@@ -178,6 +179,28 @@ TSV_API tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_shard_
                                     void* stream);
 TSV_API tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const tsv_shard_tuple* gathered,
                                     int32_t num_shards, void* stream);
+
+/* Lazy two-round vocab sharding (SURVEY.md 8(e) variant; the default of
+ * tsv_verify_accept_sharded): each rank streams only the selected row m_i of
+ * its columns (about 1.6 rows per request at alpha = 0.7 instead of 2k+1).
+ *  flags: masks_out[i] (uint64, device [B]) = (owner bits << 32) | accept bits
+ *         of the drafts x_j (j < k_i) whose column this shard holds.  Owners
+ *         are disjoint, so the integer SUM of the ranks' words is their OR.
+ *  race:  from the summed masks (identical on every rank) forms m_i (first
+ *         rejection; a draft owned by no shard makes the request bad), races
+ *         row m_i over this shard's columns and writes keys_out[2i] = local
+ *         packed key, keys_out[2i+1] = local fallback key (only when the local
+ *         residual is all zero); device [2B].  Needs the verify workspace.
+ *  emit:  from the summed masks and the element-wise MAX of the ranks' keys,
+ *         writes num_accepted / out_tokens / device_status exactly as
+ *         tsv_verify_accept.
+ * Exchanges: ncclAllReduce(sum, uint64, B) after flags, ncclAllReduce(max,
+ * uint64, 2B) after race (or any exact sum / max, e.g. loopback). */
+TSV_API tsv_status tsv_verify_shard_flags(const tsv_verify_args* a, uint64_t* masks_out, void* stream);
+TSV_API tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint64_t* masks, uint64_t* keys_out,
+                                         void* stream);
+TSV_API tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_t* masks, const uint64_t* keys,
+                                         void* stream);
 
 /* --------------------------------------------------------------------------
  * Goodput k selection: ArgMaxGoodput (Listing 2) over
@@ -260,9 +283,11 @@ TSV_API tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* al
  * Communicator for the multi-GPU modes (NCCL over NVLink 5 / NVSwitch,
  * resolved at run time from the process's libnccl.so.2).
  * tsv_comm_get_unique_id: rank 0 only; the 128 bytes are broadcast by the
- * caller (torch.distributed).  tsv_verify_accept_sharded: partial ->
- * ncclAllGather of tsv_shard_tuple rows -> combine, all on `stream`;
- * workspace >= tsv_verify_sharded_workspace_size.
+ * caller (torch.distributed).  tsv_verify_accept_sharded: lazy two rounds
+ * (flags -> ncclAllReduce sum -> race -> ncclAllReduce max -> emit), or with
+ * flags & TSV_VERIFY_SHARD_DENSE one round (partial -> ncclAllGather of
+ * tsv_shard_tuple rows -> combine), all on `stream`; workspace >=
+ * tsv_verify_sharded_workspace_size.
  * tsv_allreduce_i64: in-place sum of `count` int64 on `stream` (request-
  * sharded global sums for the alpha update and choose-k).
  * ------------------------------------------------------------------------ */

@@ -149,6 +149,7 @@ extern "C" tsv_status tsv_comm_destroy(tsv_comm* comm) {
     return s;
 }
 
+// Sharded workspace: [verify slots][dense: tuples local + gathered G x rows_p | lazy: masks B, keys 2B]
 extern "C" tsv_status tsv_verify_sharded_workspace_size(const tsv_verify_args* a, int32_t world, size_t* bytes) {
     TSV_REQUIRE(a && bytes, "tsv_verify_sharded_workspace_size: NULL argument");
     TSV_REQUIRE(world >= 1, "tsv_verify_sharded_workspace_size: world < 1");
@@ -156,7 +157,9 @@ extern "C" tsv_status tsv_verify_sharded_workspace_size(const tsv_verify_args* a
     TSV_TRY(tsv_verify_workspace_size(a, &slots));
     const size_t rows = static_cast<size_t>(a->rows_p);
     slots = (slots + 255) & ~static_cast<size_t>(255);
-    *bytes = slots + rows * sizeof(tsv_shard_tuple) * (1 + static_cast<size_t>(world));
+    const size_t dense = rows * sizeof(tsv_shard_tuple) * (1 + static_cast<size_t>(world));
+    const size_t lazy = 3 * sizeof(uint64_t) * static_cast<size_t>(a->B);
+    *bytes = slots + (dense > lazy ? dense : lazy);
     return TSV_OK;
 }
 
@@ -171,16 +174,27 @@ extern "C" tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_co
     TSV_TRY(tsv_verify_workspace_size(a, &slots));
     slots = (slots + 255) & ~static_cast<size_t>(255);
     char* ws = static_cast<char*>(a->workspace);
-    tsv_shard_tuple* local = reinterpret_cast<tsv_shard_tuple*>(ws + slots);
-    tsv_shard_tuple* gathered = local + a->rows_p;
     tsv_verify_args b = *a;
     b.workspace_bytes = slots;
-    TSV_TRY(tsv_verify_shard_partial(&b, local, stream));
-    const size_t words = static_cast<size_t>(a->rows_p) * sizeof(tsv_shard_tuple) / sizeof(uint64_t);
-    TSV_TRY(nccl_status(g_nccl.AllGather(local, gathered, words, ncclUint64, comm->comm,
-                                         static_cast<cudaStream_t>(stream)),
-                        "ncclAllGather"));
-    return tsv_verify_shard_combine(&b, gathered, comm->world, stream);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (a->flags & TSV_VERIFY_SHARD_DENSE) {  // one round: every row of every request
+        tsv_shard_tuple* local = reinterpret_cast<tsv_shard_tuple*>(ws + slots);
+        tsv_shard_tuple* gathered = local + a->rows_p;
+        TSV_TRY(tsv_verify_shard_partial(&b, local, stream));
+        const size_t words = static_cast<size_t>(a->rows_p) * sizeof(tsv_shard_tuple) / sizeof(uint64_t);
+        TSV_TRY(nccl_status(g_nccl.AllGather(local, gathered, words, ncclUint64, comm->comm, st), "ncclAllGather"));
+        return tsv_verify_shard_combine(&b, gathered, comm->world, stream);
+    }
+    // lazy two rounds: flags -> sum -> race of row m_i only -> max -> emit
+    uint64_t* masks = reinterpret_cast<uint64_t*>(ws + slots);
+    uint64_t* keys = masks + a->B;
+    TSV_TRY(tsv_verify_shard_flags(&b, masks, stream));
+    TSV_TRY(nccl_status(g_nccl.AllReduce(masks, masks, static_cast<size_t>(a->B), ncclUint64, ncclSum, comm->comm, st),
+                        "ncclAllReduce(sum)"));
+    TSV_TRY(tsv_verify_shard_race(&b, masks, keys, stream));
+    TSV_TRY(nccl_status(g_nccl.AllReduce(keys, keys, 2 * static_cast<size_t>(a->B), ncclUint64, ncclMax, comm->comm, st),
+                        "ncclAllReduce(max)"));
+    return tsv_verify_shard_emit(&b, masks, keys, stream);
 }
 
 extern "C" tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* comm, void* stream) {

@@ -500,6 +500,129 @@ __global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_
     if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
 }
 
+// ------------------------------------------------------------ lazy two-round vocab sharding
+// Round 1 (flags): per request, the accept and owner bits of the drafts this shard owns;
+// ownership is disjoint across shards, so the integer sum of the G mask words is their OR.
+// Round 2 (race): from the summed masks every shard forms the same m_i, races row m_i over
+// its columns and publishes (local key, local fallback key); the element-wise max over
+// shards is the unsharded row key.  Emit: from summed masks + maxed keys.
+__global__ void __launch_bounds__(256) verify_shard_flags_kernel(const RaceParams P, unsigned long long* masks) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t r0 = P.row_offsets[i];
+    const int32_t r1 = P.row_offsets[i + 1];
+    const int32_t k = r1 - r0 - 1;
+    const int32_t qbase = r0 - i;
+    const bool ok = k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p;
+    bool acc = false, own = false;
+    if (ok && lane < k) {
+        const int32_t x = P.drafts[qbase + lane];
+        const int32_t xl = x - P.vocab_offset;
+        own = x >= 0 && x < P.vocab_global && xl >= 0 && xl < P.vocab;
+        if (own) {
+            const uint32_t rid = P.rids[i];
+            const uint4 rr = philox4x32_10(0u, (kPurposeAccept << 16) | static_cast<uint32_t>(lane), rid, P.step,
+                                           P.k0, P.k1);
+            const float u = u_acc_from_word(rr.x);
+            const float qx = P.q ? P.q[static_cast<int64_t>(qbase + lane) * P.ld + xl] : 1.0f;
+            const float px = P.p[static_cast<int64_t>(r0 + lane) * P.ld + xl];
+            acc = __fmul_rn(u, qx) < px;  // strict; NaN rejects
+        }
+    }
+    const uint32_t accm = __ballot_sync(0xFFFFFFFFu, acc);
+    const uint32_t ownm = __ballot_sync(0xFFFFFFFFu, own);
+    if (lane == 0) masks[i] = (static_cast<unsigned long long>(ownm) << 32) | accm;
+}
+
+// The request's ReqMeta from the summed mask word (every lane; identical on every shard).
+// ok: 1 valid, 0 bad k, 2 bad draft (outside [0, vocab_global) or owned by no shard).
+__device__ __forceinline__ ReqMeta shard_meta_from_masks(const RaceParams& P, int32_t i, unsigned long long mask) {
+    const int lane = threadIdx.x & 31;
+    const int32_t r0 = P.row_offsets[i];
+    const int32_t r1 = P.row_offsets[i + 1];
+    const int32_t k = r1 - r0 - 1;
+    const int32_t qbase = r0 - i;
+    int32_t ok = (k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p) ? 1 : 0;
+    int32_t x = -1;
+    bool bad = false;
+    if (ok && lane < k) {
+        x = P.drafts[qbase + lane];
+        bad = x < 0 || x >= P.vocab_global;
+    }
+    const uint32_t accm = static_cast<uint32_t>(mask);
+    const uint32_t ownm = static_cast<uint32_t>(mask >> 32);
+    const uint32_t kmask = (ok == 1 && k > 0) ? ((1u << k) - 1u) : 0u;
+    if (__ballot_sync(0xFFFFFFFFu, bad) || (ownm & kmask) != kmask) ok = ok ? 2 : 0;
+    const uint32_t rej = ~accm & kmask;
+    const int32_t m = ok == 1 ? (rej ? (__ffs(rej) - 1) : k) : -1;
+    const int32_t xm = __shfl_sync(0xFFFFFFFFu, x, (m >= 0 ? m : 0) & 31);
+    ReqMeta rm;
+    rm.r0 = r0;
+    rm.k = k;
+    rm.qbase = qbase;
+    rm.m = m;
+    rm.xm = (m >= 0 && m < k) ? xm : -1;
+    rm.ok = ok;
+    rm.rid = P.rids[i];
+    rm.pad = 0;
+    return rm;
+}
+
+__global__ void __launch_bounds__(256) verify_shard_meta_kernel(const RaceParams P, const unsigned long long* masks) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const ReqMeta rm = shard_meta_from_masks(P, i, masks[i]);
+    if ((threadIdx.x & 31) == 0) {
+        P.meta[i] = rm;
+        P.rowT[i] = 0u;
+        P.rowkey[i] = 0ull;
+    }
+}
+
+template <bool PRUNE>
+__global__ void __launch_bounds__(256) verify_shard_keys_kernel(const RaceParams P, unsigned long long* keys) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const int lane = threadIdx.x & 31;
+    const ReqMeta rm = P.meta[i];
+    uint64_t key = 0, fb = 0;
+    if (rm.ok == 1) {
+        key = P.rowkey[i];
+        if (key == 0 && rm.m < rm.k)  // this shard's residual is zero: its share of the R5 fallback
+            fb = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
+    }
+    if (lane == 0) {
+        keys[2 * i] = key;
+        keys[2 * i + 1] = fb;
+    }
+}
+
+__global__ void __launch_bounds__(256) verify_shard_emit_kernel(const RaceParams P, const unsigned long long* masks,
+                                                                const unsigned long long* keys) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const int lane = threadIdx.x & 31;
+    const ReqMeta rm = shard_meta_from_masks(P, i, masks[i]);
+    if (rm.ok != 1) {
+        emit(P, i, 0, -1, -1);
+        if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
+        return;
+    }
+    uint64_t key = keys[2 * i];
+    if (key == 0 && rm.m < rm.k) key = keys[2 * i + 1];
+    emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
+    if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+}
+
 // ------------------------------------------------------------------------ host side
 static int sm_count();
 // Default work-item size: about one item per resident warp of the race kernel
@@ -713,5 +836,58 @@ extern "C" tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const t
     TSV_CUDA(launch_pdl(verify_shard_combine_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0,
                         static_cast<cudaStream_t>(stream), P, gathered, num_shards, a->rows_p),
              "verify_shard_combine_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_verify_shard_flags(const tsv_verify_args* a, uint64_t* masks_out, void* stream) {
+    TSV_TRY(validate(a));
+    TSV_TRY(check_device());
+    if (a->B == 0) return TSV_OK;
+    TSV_REQUIRE(masks_out != nullptr, "tsv_verify_shard_flags: masks_out is NULL");
+    RaceParams P = make_params(a);
+    TSV_CUDA(launch_pdl(verify_shard_flags_kernel, dim3(static_cast<unsigned>((a->B + 7) / 8)), dim3(256), 0,
+                        static_cast<cudaStream_t>(stream), P, reinterpret_cast<unsigned long long*>(masks_out)),
+             "verify_shard_flags_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint64_t* masks, uint64_t* keys_out,
+                                            void* stream) {
+    TSV_TRY(validate(a));
+    TSV_TRY(check_device());
+    if (a->B == 0) return TSV_OK;
+    TSV_REQUIRE(masks && keys_out, "tsv_verify_shard_race: NULL argument");
+    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+                "tsv_verify_shard_race: workspace too small (%llu < %llu bytes)",
+                (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    RaceParams P = make_params(a);
+    const dim3 grid(static_cast<unsigned>((a->B + 7) / 8));
+    TSV_CUDA(launch_pdl(verify_shard_meta_kernel, grid, dim3(256), 0, st, P,
+                        reinterpret_cast<const unsigned long long*>(masks)),
+             "verify_shard_meta_kernel launch");
+    const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
+    tsv_status rs;
+    if (a->q) rs = prune ? launch_race<kLazy, true, true>(P, st) : launch_race<kLazy, true, false>(P, st);
+    else rs = prune ? launch_race<kLazy, false, true>(P, st) : launch_race<kLazy, false, false>(P, st);
+    TSV_TRY(rs);
+    auto* k = reinterpret_cast<unsigned long long*>(keys_out);
+    TSV_CUDA(prune ? launch_pdl(verify_shard_keys_kernel<true>, grid, dim3(256), 0, st, P, k)
+                   : launch_pdl(verify_shard_keys_kernel<false>, grid, dim3(256), 0, st, P, k),
+             "verify_shard_keys_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_t* masks, const uint64_t* keys,
+                                            void* stream) {
+    TSV_TRY(validate(a));
+    TSV_TRY(check_device());
+    if (a->B == 0) return TSV_OK;
+    TSV_REQUIRE(masks && keys, "tsv_verify_shard_emit: NULL argument");
+    RaceParams P = make_params(a);
+    TSV_CUDA(launch_pdl(verify_shard_emit_kernel, dim3(static_cast<unsigned>((a->B + 7) / 8)), dim3(256), 0,
+                        static_cast<cudaStream_t>(stream), P, reinterpret_cast<const unsigned long long*>(masks),
+                        reinterpret_cast<const unsigned long long*>(keys)),
+             "verify_shard_emit_kernel launch");
     return TSV_OK;
 }

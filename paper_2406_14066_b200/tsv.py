@@ -23,6 +23,7 @@ DEVSTATUS_BAD_TOKEN = 1
 DEVSTATUS_BAD_K = 2
 DEVSTATUS_NO_WEIGHT = 4
 VERIFY_NO_PRUNE = 1
+VERIFY_SHARD_DENSE = 2
 POLICY_DRAFT = 0
 POLICY_PLD = 1
 EST_TESTED = 0
@@ -37,7 +38,8 @@ EXPORTED = [
     "tsv_verify_sharded_workspace_size", "tsv_verify_accept_sharded", "tsv_allreduce_i64",
     "tsv_propose_lookup_choose_k", "tsv_verify_accept_update", "tsv_debug_race_E", "tsv_debug_philox",
     "tsv_goodput_partial", "tsv_goodput_finalize", "tsv_goodput_choose_k_sharded", "tsv_update_partial",
-    "tsv_update_finalize", "tsv_update_acceptance_sharded",
+    "tsv_update_finalize", "tsv_update_acceptance_sharded", "tsv_verify_shard_flags", "tsv_verify_shard_race",
+    "tsv_verify_shard_emit",
 ]
 
 
@@ -114,6 +116,9 @@ def _load() -> ctypes.CDLL:
         "tsv_update_partial": ([P, P, i32, i32, P, P], ctypes.c_int),
         "tsv_update_finalize": ([P, P, f64, P], ctypes.c_int),
         "tsv_update_acceptance_sharded": ([P, P, P, i32, f64, i32, P, P, P], ctypes.c_int),
+        "tsv_verify_shard_flags": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
+        "tsv_verify_shard_race": ([ctypes.POINTER(VerifyArgs), P, P, P], ctypes.c_int),
+        "tsv_verify_shard_emit": ([ctypes.POINTER(VerifyArgs), P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -272,6 +277,21 @@ def tsv_verify_shard_partial(args: VerifyArgs, tuples_out: torch.Tensor, stream=
 def tsv_verify_shard_combine(args: VerifyArgs, gathered: torch.Tensor, num_shards: int, stream=None):
     _check(_lib.tsv_verify_shard_combine(ctypes.byref(args), _ptr(gathered), int(num_shards),
                                          _stream(stream)))
+
+
+def tsv_verify_shard_flags(args: VerifyArgs, masks_out: torch.Tensor, stream=None):
+    """Lazy sharding round 1: int64 [B] (owner bits << 32 | accept bits) of this shard's drafts."""
+    _check(_lib.tsv_verify_shard_flags(ctypes.byref(args), _ptr(masks_out), _stream(stream)))
+
+
+def tsv_verify_shard_race(args: VerifyArgs, masks: torch.Tensor, keys_out: torch.Tensor, stream=None):
+    """Lazy sharding round 2: race row m_i (from the summed masks) -> int64 [2B] (key, fallback key)."""
+    _check(_lib.tsv_verify_shard_race(ctypes.byref(args), _ptr(masks), _ptr(keys_out), _stream(stream)))
+
+
+def tsv_verify_shard_emit(args: VerifyArgs, masks: torch.Tensor, keys: torch.Tensor, stream=None):
+    """Emit from the summed masks and the max-reduced keys."""
+    _check(_lib.tsv_verify_shard_emit(ctypes.byref(args), _ptr(masks), _ptr(keys), _stream(stream)))
 
 
 def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, ctx_len, target,

@@ -232,6 +232,69 @@ def shard_loopback(tsv, vb, G, seed, step, chunk=0):
     return _np(na), _np(out)
 
 
+def _u64max(a, b):
+    """Element-wise unsigned max of int64 tensors holding u64 bit patterns."""
+    flip = torch.tensor(-(2 ** 63), dtype=torch.int64, device=a.device)
+    return torch.maximum(a ^ flip, b ^ flip) ^ flip
+
+
+def lazy_shard_loopback(tsv, vb, G, seed, step, chunk=0):
+    """Two-round lazy sharding on one device: flags (sum) -> race (max) -> emit."""
+    g = vb.to(DEV)
+    B, V = vb.B, vb.vocab
+    assert V % (4 * G) == 0
+    Vs = V // G
+    na = torch.empty(B, dtype=torch.int32, device=DEV)
+    out = torch.empty((B, vb.k_max + 1), dtype=torch.int32, device=DEV)
+    args = []
+    for s in range(G):
+        lo = s * Vs
+        a = tsv.make_verify_args(g.p[:, lo:lo + Vs], None if g.q is None else g.q[:, lo:lo + Vs],
+                                 g.row_offsets, g.draft_tokens, g.request_ids, seed, step, vb.k_max,
+                                 na, out, vocab=Vs, vocab_offset=lo, vocab_global=V, chunk=chunk)
+        ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+        a.workspace = ws.data_ptr()
+        a.workspace_bytes = ws.numel()
+        args.append((a, ws))
+    masks = torch.zeros(B, dtype=torch.int64, device=DEV)
+    for a, _ in args:
+        m = torch.empty(B, dtype=torch.int64, device=DEV)
+        tsv.tsv_verify_shard_flags(a, m)
+        masks += m
+    keys = torch.zeros(2 * B, dtype=torch.int64, device=DEV)
+    for a, _ in args:
+        k = torch.empty(2 * B, dtype=torch.int64, device=DEV)
+        tsv.tsv_verify_shard_race(a, masks, k)
+        keys = _u64max(keys, k)
+    tsv.tsv_verify_shard_emit(args[0][0], masks, keys)
+    torch.cuda.synchronize()
+    return _np(na), _np(out)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_lazy_vocab_shard_loopback_equals_oracle(tsv, G):
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=24)
+    ona, oout, _ = oracle_verify(vb, 21, 3)
+    na, out = lazy_shard_loopback(tsv, vb, G, 21, 3)
+    assert (na == ona).all() and (out == oout).all()
+
+
+def test_lazy_vocab_shard_one_hot_and_adversarial(tsv):
+    vb = synth.make_verify_batch(B=40, V=4096, k_max=6, lam=0.7, seed=25, dense_q=False)
+    ona, oout, _ = oracle_verify(vb, 2, 2)
+    for G in (2, 4):
+        na, out = lazy_shard_loopback(tsv, vb, G, 2, 2, chunk=1024)
+        assert (na == ona).all() and (out == oout).all()
+    adv = _adversarial_batch()
+    adv.vocab = 256
+    adv.p = adv.p[:, :256].contiguous(); adv.q = adv.q[:, :256].contiguous()
+    adv.draft_tokens = adv.draft_tokens.clamp(max=255)
+    for step in range(4):
+        ona, oout, _ = oracle_verify(adv, 4, step)
+        na, out = lazy_shard_loopback(tsv, adv, 4, 4, step)
+        assert (na == ona).all() and (out == oout).all()
+
+
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_vocab_shard_loopback_equals_oracle(tsv, G):
     vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=17)
@@ -255,6 +318,31 @@ def test_vocab_shard_loopback_one_hot_and_adversarial(tsv):
     assert (na == ona).all() and (out == oout).all()
 
 
+def test_verify_accept_sharded_nccl_world1(tsv):
+    # partial -> ncclAllGather of the shard tuples -> combine, on a one-rank communicator
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=23)
+    ona, oout, _ = oracle_verify(vb, 5, 9)
+    g = vb.to(DEV)
+    na = torch.empty(vb.B, dtype=torch.int32, device=DEV)
+    out = torch.empty((vb.B, vb.k_max + 1), dtype=torch.int32, device=DEV)
+    a = tsv.make_verify_args(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, 5, 9, vb.k_max, na, out,
+                             vocab=vb.vocab, vocab_global=vb.vocab)
+    comm = tsv.Comm(0, 1)
+    try:
+        ws = tsv.alloc_workspace(tsv.tsv_verify_sharded_workspace_size(a, 1), DEV)
+        a.workspace = ws.data_ptr()
+        a.workspace_bytes = ws.numel()
+        for flags in (0, tsv.VERIFY_SHARD_DENSE):  # lazy two rounds (default), one-round dense
+            na.fill_(-7)
+            out.fill_(-7)
+            a.flags = flags
+            tsv.tsv_verify_accept_sharded(a, comm)
+            torch.cuda.synchronize()
+            assert (_np(na) == ona).all() and (_np(out) == oout).all(), flags
+    finally:
+        comm.close()
+
+
 @pytest.mark.slow
 def test_config4_llama3_vocab_sharded(tsv):
     # V = 128256 (Llama-3), B = 256, ragged k: one-round dense shard partials, G = 2/4/8
@@ -264,6 +352,8 @@ def test_config4_llama3_vocab_sharded(tsv):
     assert (gna == ona).all() and (gout == oout).all()
     for G in (2, 4, 8):
         na, out = shard_loopback(tsv, vb, G, 240614066, 0)
+        assert (na == ona).all() and (out == oout).all()
+        na, out = lazy_shard_loopback(tsv, vb, G, 240614066, 0)
         assert (na == ona).all() and (out == oout).all()
 
 
