@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
+    ap.add_argument("--workload", default="step", choices=["step", "config4"],
+                    help="step: the default decode step; config4: Llama-3 vocab-sharded verify (V=128256) "
+                         "through tsv_verify_accept_sharded over the N ranks (strong scaling)")
+    ap.add_argument("--shard-mode", default="lazy", choices=["lazy", "dense"], help="config4 sharding mode")
     return ap.parse_args()
 
 
@@ -357,6 +361,125 @@ def run_ours(args, rank, world, local_rank):
     return line
 
 
+# ------------------------------------------------------------------ config 4 (vocab sharded)
+V4 = 128256
+
+
+def run_config4(args, rank, world, local_rank):
+    """BASELINE config 4: one B = 256 batch at V = 128256, vocab-sharded over the N ranks as under a
+    tensor-parallel LM head (rank g holds columns [g V/N, (g+1) V/N) of every p/q row); one step =
+    tsv_verify_accept_sharded (lazy: flags -> NCCL all-reduce(sum) -> race of row m -> NCCL
+    all-reduce(max) -> emit; dense: partial -> NCCL all-gather -> combine).  Strong scaling."""
+    import torch
+
+    import synth
+    from paper_2406_14066_b200 import dist as pdist
+    from paper_2406_14066_b200 import tsv
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    R = max(2, args.sets)
+    seed = synth.DEFAULT_SEED
+    lo, Vs = pdist.vocab_shards(V4, world)[rank]
+    hi = lo + Vs
+    comm = tsv.Comm(rank, world)
+    flags = tsv.VERIFY_SHARD_DENSE if args.shard_mode == "dense" else 0
+    na = torch.empty(B, dtype=torch.int32, device=dev)
+    outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
+    sets, footprint = [], 0
+    for s in range(R):  # the same logical batch on every rank (same seed), this rank's columns kept
+        vb = synth.make_verify_batch(B=B, V=V4, k_max=K_MAX, lam=0.7, seed=seed + 104729 * s, device=dev)
+        p = vb.p[:, lo:hi].contiguous()
+        q = vb.q[:, lo:hi].contiguous()
+        footprint += (p.numel() + q.numel()) * 4
+        sets.append((vb, p, q))
+        del vb.p, vb.q
+    torch.cuda.empty_cache()
+    args_list = []
+    W, K = max(3, args.warmup), args.steps
+    gl = max(1, min(args.graph_steps, K))
+    for t in range(gl):
+        vb, p, q = sets[t % R]
+        a = tsv.make_verify_args(p, q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t, K_MAX, na, outt,
+                                 None, None, vocab=Vs, vocab_offset=lo, vocab_global=V4, chunk=args.chunk,
+                                 flags=flags)
+        args_list.append(a)
+    ws = tsv.alloc_workspace(max(tsv.tsv_verify_sharded_workspace_size(a, world) for a in args_list), dev)
+    for a in args_list:
+        a.workspace = ws.data_ptr()
+        a.workspace_bytes = ws.numel()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        tsv.tsv_verify_accept_sharded(args_list[0], comm, stream=side)  # warm-up outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for a in args_list:
+            tsv._check(tsv.lib().tsv_verify_accept_sharded(tsv.ctypes.byref(a), comm.handle, side.cuda_stream))
+    torch.cuda.synchronize()
+    for _ in range((W + gl - 1) // gl):
+        g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(1, K // gl)
+    sampler = ClockSampler(local_rank)
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(device_ids=[local_rank])
+
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    t_ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    steps = reps * gl
+    # tokens and algorithmic bytes of the timed steps (identical on every rank)
+    tok, vbytes = 0, 0.0
+    for t in range(gl):
+        a = args_list[t]
+        tsv.tsv_verify_accept_sharded(a, comm)
+        torch.cuda.synchronize()
+        m = na.cpu().numpy()
+        k = sets[t % R][0].k.cpu().numpy()
+        tok += int((m + 1).sum())
+        dense = flags != 0
+        rows = (2 * k + 1) if dense else (1 + (m < k))  # rows streamed per request (all ranks together)
+        vbytes += float((rows * V4 * 4).sum()) / world
+    tok_per_step, vbytes = tok / gl, vbytes / gl
+    ms_step = t_ms / steps
+    comm.close()
+    if rank != 0:
+        return None
+    peak, peak_src = load_peaks()
+    achieved = vbytes / (ms_step * 1e-3) / 1e9
+    return {
+        "metric": METRIC, "value": tok_per_step / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
+        "config": {"workload": f"config4 Llama-3 verify (B={B}, k~U{{0..{K_MAX}}}, V={V4}, fp32 p+q, lambda=0.7), "
+                               f"vocab-sharded x{world} ({args.shard_mode})",
+                   "global_batch": B, "vocab": V4, "k_max": K_MAX, "parallelism": f"vocab-sharded x{world}",
+                   "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank",
+                   "graph_steps": gl},
+        "roofline": {"kernel": "tsv_verify_accept_sharded (per rank)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
+        "clocks": sampler.summary(),
+        "gpu_launches": (3 if flags else 5) * steps,
+        "e2e": None,
+        "tokens_per_step": tok_per_step,
+        "requests_per_s": B / (ms_step * 1e-3),
+    }
+
+
 # ------------------------------------------------------------------------- oracle (CPU)
 def oracle_step_sample(n_req, seed, step, data):
     """One bounded oracle step over the first n_req requests of the workload (CPU)."""
@@ -446,6 +569,15 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.workload == "config4":
+        line = run_config4(args, rank, world, local_rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     line = run_ours(args, rank, world, local_rank)
     if line is not None:
         if world == 1 and not args.no_cpu_baseline:
