@@ -54,7 +54,6 @@ struct RaceParams {
 
 enum Mode { kLazy = 0, kShard = 1 };
 
-constexpr int kChunk = 2048;                      // columns per work item (default)
 constexpr int kMaxChunk = 16384;
 constexpr float kPruneC = 0x1.fffffap-1f;        // 1 - 3*2^-24 <= (1-2^-23)(1-2^-24)
 constexpr float kLbC = 0x1.ffffe0p-1f;           // 1 - 2^-20
@@ -299,6 +298,26 @@ constexpr int kRaceThreads = 256;
 constexpr int kRaceWarps = kRaceThreads / 32;
 constexpr int kUnroll = 2;
 
+#ifndef TSV_TRACE
+#define TSV_TRACE 0
+#endif
+#if TSV_TRACE
+// Diagnostic builds only (-DTSV_TRACE=1, scripts/diag_trace.py): per work item, globaltimer at
+// the start (after the meta load), after streaming, at the end; CTA, SM and row type.
+constexpr int kTraceMax = 65536;
+__device__ unsigned long long g_trace[kTraceMax][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
+#endif
+
 template <int MODE, bool DENSE_Q, bool PRUNE>
 __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const RaceParams P) {
     pdl_wait();  // the scan kernel's ReqMeta / rowT / rowkey are complete and visible
@@ -318,6 +337,9 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
         const int32_t j = rem / P.n_chunks;
         const ReqMeta rm = P.meta[i];
         if (rm.ok != 1) continue;
+#if TSV_TRACE
+        const unsigned long long tr0 = gtimer();
+#endif
         const int32_t sel = (MODE == kLazy) ? rm.m : j;
         if (MODE == kShard && sel > rm.k) continue;  // no such row
         const bool residual = sel < rm.k;
@@ -369,6 +391,9 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
             R.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
             if (PRUNE) R.sync_T();
         }
+#if TSV_TRACE
+        const unsigned long long tr1 = gtimer();
+#endif
         if (PRUNE) {  // share this chunk's bound, then flush against the row's best bound
             if (lane == 0) atomicMax(P.rowT + key_row, __float_as_uint(R.T));
             const float t = __uint_as_float(*reinterpret_cast<volatile uint32_t*>(P.rowT + key_row));
@@ -376,6 +401,14 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
         }
         const uint64_t best = warp_max_u64(R.best);
         if (lane == 0 && best) atomicMax(P.rowkey + key_row, static_cast<unsigned long long>(best));
+#if TSV_TRACE
+        if (lane == 0 && item < kTraceMax) {
+            g_trace[item][0] = tr0;
+            g_trace[item][1] = tr1;
+            g_trace[item][2] = gtimer();
+            g_trace[item][3] = (static_cast<unsigned long long>(blockIdx.x) << 32) | (smid() << 1) | (residual ? 1u : 0u);
+        }
+#endif
     }
 }
 
@@ -891,3 +924,15 @@ extern "C" tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint
              "verify_shard_emit_kernel launch");
     return TSV_OK;
 }
+
+#if TSV_TRACE
+extern "C" TSV_API tsv_status tsv_debug_trace(unsigned long long* out, int32_t n) {
+    TSV_CUDA(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 4 * static_cast<size_t>(n)), "trace copy");
+    return TSV_OK;
+}
+extern "C" TSV_API tsv_status tsv_debug_trace_clear() {
+    static unsigned long long zeros[kTraceMax][4];
+    TSV_CUDA(cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros)), "trace clear");
+    return TSV_OK;
+}
+#endif
