@@ -9,6 +9,7 @@ shares no code with, and never imports, ``paper_2406_14066_b200``.
 Functions (each cites its passage in oracle.c):
   philox4x32_10, u_acc, u_race, E, E_table  -- RNG and race uniforms (R6, R9)
   verify       -- rejection-sampling accept + residual/bonus race
+  verify_greedy -- temperature-0 verify: keep drafts equal to the target argmax
   lookup       -- prompt-lookup n-gram proposal
   expected_len, forward_time, choose_k -- goodput adaptor
   update       -- moving-average acceptance update
@@ -68,6 +69,8 @@ def _load():
         lib.oracle_E_table.restype = None
         lib.oracle_verify.argtypes = [P, P, i64, i32, P, P, P, u64, u32, i32, i32, P, P, P, P]
         lib.oracle_verify.restype = i32
+        lib.oracle_verify_greedy.argtypes = [P, i64, i32, P, P, i32, i32, P, P]
+        lib.oracle_verify_greedy.restype = i32
         lib.oracle_lookup.argtypes = [P, P, i32, i32, i32, i32, P, P]
         lib.oracle_lookup.restype = None
         lib.oracle_expected_len.argtypes = [f64, i32]
@@ -145,6 +148,23 @@ def verify(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max,
     st = lib.oracle_verify(_ptr(p), _ptr(q), ld, V, _ptr(ro), _ptr(dt), _ptr(rid),
                            int(seed), int(step), B, int(k_max), _ptr(ia), _ptr(ie),
                            _ptr(na), _ptr(out))
+    return na, out, int(st)
+
+
+def verify_greedy(p, row_offsets, draft_tokens, k_max, vocab=None):
+    """Greedy (temperature-0) verify: returns (num_accepted[B], out_tokens[B, k_max+1], status)."""
+    lib = _load()
+    p = _c(p, np.float32)
+    ro = _c(row_offsets, np.int32)
+    dt = _c(draft_tokens, np.int32)
+    if dt.size == 0:
+        dt = np.zeros(1, np.int32)
+    B = ro.size - 1
+    ld = p.shape[1]
+    V = ld if vocab is None else int(vocab)
+    na = np.zeros(B, np.int32)
+    out = np.zeros((B, k_max + 1), np.int32)
+    st = lib.oracle_verify_greedy(_ptr(p), ld, V, _ptr(ro), _ptr(dt), B, int(k_max), _ptr(na), _ptr(out))
     return na, out, int(st)
 
 

@@ -238,6 +238,61 @@ int32_t oracle_verify(const float* p, const float* q, int64_t ld, int32_t V,
  * match proposes nothing).  Reading R20: for n = n_max down to n_min, the
  * latest start s < L-n with ctx[s..s+n-1] == ctx[L-n..L-1]; propose
  * ctx[s+n .. min(s+n+K, L)-1]; no match for any n => length 0.            */
+/* Greedy verification (temperature 0): the paper's dynamic-
+ * workload and appendix runs use greedy decoding, under which
+ * speculative decoding keeps a draft token iff it is the target's argmax, and the
+ * correction / bonus token is the target's argmax at the first position that does not
+ * match (or after the last draft).  Reading (R24): argmax over v < V of the
+ * float values, NaN never selected, ties -> lowest index; a row with no non-NaN value has
+ * no argmax (token -1, NO_WEIGHT).  Written out as the definition: one loop per row. */
+static int32_t greedy_argmax(const float* row, int32_t V)
+{
+    int32_t v, best = -1;
+    for (v = 0; v < V; ++v) {
+        if (row[v] != row[v]) continue;            /* NaN */
+        if (best < 0 || row[v] > row[best]) best = v;  /* strict: first maximum wins */
+    }
+    return best;
+}
+
+int32_t oracle_verify_greedy(const float* p, int64_t ld, int32_t V, const int32_t* row_offsets,
+                             const int32_t* draft_tokens, int32_t B, int32_t k_max,
+                             int32_t* num_accepted, int32_t* out_tokens)
+{
+    int32_t status = 0, i, j;
+    for (i = 0; i < B; ++i) {
+        int32_t r0 = row_offsets[i], r1 = row_offsets[i + 1];
+        int32_t k = r1 - r0 - 1, qbase = r0 - i, m, t, bad = 0;
+        int32_t* out = out_tokens + (int64_t)i * (k_max + 1);
+        for (j = 0; j <= k_max; ++j) out[j] = -1;
+        num_accepted[i] = -1;
+        if (k < 0 || k > k_max || qbase < 0) {
+            status |= ORACLE_STATUS_BAD_K;
+            continue;
+        }
+        for (j = 0; j < k; ++j) {
+            int32_t x = draft_tokens[qbase + j];
+            if (x < 0 || x >= V) bad = 1;
+        }
+        if (bad) {
+            status |= ORACLE_STATUS_BAD_TOKEN;
+            continue;
+        }
+        m = k;  /* accept while the draft is the target's argmax */
+        for (j = 0; j < k; ++j)
+            if (draft_tokens[qbase + j] != greedy_argmax(p + (int64_t)(r0 + j) * ld, V)) {
+                m = j;
+                break;
+            }
+        t = greedy_argmax(p + (int64_t)(r0 + m) * ld, V);  /* correction (m < k) or bonus (m = k) */
+        for (j = 0; j < m; ++j) out[j] = draft_tokens[qbase + j];
+        out[m] = t;
+        num_accepted[i] = m;
+        if (t < 0) status |= ORACLE_STATUS_NO_WEIGHT;
+    }
+    return status;
+}
+
 /* ------------------------------------------------------------------------ */
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,

@@ -28,6 +28,10 @@ int32_t oracle_verify(const float* p, const float* q, int64_t ld, int32_t V,
                       const float* inj_u_acc, const float* inj_E,
                       int32_t* num_accepted, int32_t* out_tokens);
 
+int32_t oracle_verify_greedy(const float* p, int64_t ld, int32_t V, const int32_t* row_offsets,
+                             const int32_t* draft_tokens, int32_t B, int32_t k_max,
+                             int32_t* num_accepted, int32_t* out_tokens);
+
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,
                    int32_t* proposals, int32_t* proposal_len);
