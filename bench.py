@@ -49,9 +49,10 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
-    ap.add_argument("--workload", default="step", choices=["step", "config4"],
+    ap.add_argument("--workload", default="step", choices=["step", "config4", "greedy"],
                     help="step: the default decode step; config4: Llama-3 vocab-sharded verify (V=128256) "
-                         "through tsv_verify_accept_sharded over the N ranks (strong scaling)")
+                         "through tsv_verify_accept_sharded over the N ranks (strong scaling); greedy: the "
+                         "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling)")
     ap.add_argument("--shard-mode", default="lazy", choices=["lazy", "dense"], help="config4 sharding mode")
     return ap.parse_args()
 
@@ -480,6 +481,107 @@ def run_config4(args, rank, world, local_rank):
     }
 
 
+# ------------------------------------------------------------------ greedy verify (NEXT 2)
+def run_greedy(args, rank, world, local_rank):
+    """tsv_verify_greedy on the config-2 batch (B = 256, k ~ U{0..8}, V = 32000, fp32 p; drafts
+    equal the target argmax w.p. 0.7).  Every p row is streamed (each needs its argmax)."""
+    import torch
+
+    import synth
+    from paper_2406_14066_b200 import dist as pdist
+    from paper_2406_14066_b200 import tsv
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    R = max(2, args.sets)
+    sets, footprint = [], 0
+    for s in range(R):
+        vb = synth.make_verify_batch(B=B, V=V, k_max=K_MAX, lam=0.7, seed=synth.DEFAULT_SEED + 31 * s + rank,
+                                     device=dev, request_id_base=rank * B)
+        am = vb.p.argmax(dim=1).to(torch.int32)
+        ro = vb.row_offsets.long()
+        g = torch.Generator(device="cpu").manual_seed(1000 + s + 7 * rank)
+        keep = torch.rand(vb.draft_tokens.numel(), generator=g) < 0.7
+        rows = torch.cat([torch.arange(int(ro[i]), int(ro[i + 1]) - 1) for i in range(B)]).to(dev)
+        d = torch.where(keep.to(dev), am[rows], vb.draft_tokens)
+        footprint += vb.p.numel() * 4
+        sets.append((vb.p, vb.row_offsets, d.contiguous(), vb.k))
+        del vb.q
+    torch.cuda.empty_cache()
+    na = torch.empty(B, dtype=torch.int32, device=dev)
+    outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
+    W, K = max(3, args.warmup), args.steps
+    gl = max(1, min(args.graph_steps, K))
+    args_list = []
+    for t in range(gl):
+        p, ro, d, _ = sets[t % R]
+        rids = torch.zeros(B, dtype=torch.int32, device=dev)
+        args_list.append(tsv.make_verify_args(p, None, ro, d, rids, 0, 0, K_MAX, na, outt, None, None,
+                                              chunk=args.chunk))
+    ws = tsv.alloc_workspace(max(tsv.tsv_verify_workspace_size(a) for a in args_list), dev)
+    for a in args_list:
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        tsv._check(tsv.lib().tsv_verify_greedy(tsv.ctypes.byref(args_list[0]), side.cuda_stream))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for a in args_list:
+            tsv._check(tsv.lib().tsv_verify_greedy(tsv.ctypes.byref(a), side.cuda_stream))
+    for _ in range((W + gl - 1) // gl):
+        g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(1, K // gl)
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local_rank])
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    t_ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    steps = reps * gl
+    tok, vbytes = 0, 0.0
+    for t in range(gl):
+        tsv._check(tsv.lib().tsv_verify_greedy(tsv.ctypes.byref(args_list[t]), None))
+        torch.cuda.synchronize()
+        k = sets[t % R][3].cpu().numpy()
+        tok += int((na.cpu().numpy() + 1).sum())
+        vbytes += float(((k + 1) * V * 4).sum() + 4 * (k.sum() + 2 * B + 1) + 4 * B * (K_MAX + 2))
+    tok_total = pdist.sum_over_ranks(tok, dev) / gl
+    vbytes /= gl
+    ms_step = t_ms / steps
+    if rank != 0:
+        return None
+    peak, peak_src = load_peaks()
+    achieved = vbytes / (ms_step * 1e-3) / 1e9
+    return {
+        "metric": METRIC, "value": tok_total / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
+        "config": {"workload": f"greedy verify (temperature 0, NEXT 2): B={B}, k~U{{0..{K_MAX}}}, V={V}, fp32 p, "
+                               f"drafts = target argmax w.p. 0.7", "global_batch": B * world, "vocab": V,
+                   "k_max": K_MAX, "parallelism": f"request-sharded x{world}",
+                   "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank", "graph_steps": gl},
+        "roofline": {"kernel": "tsv_verify_greedy (argmax + emit)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
+        "clocks": sampler.summary(),
+        "gpu_launches": 2 * steps,
+        "e2e": None,
+        "tokens_per_step": tok_total,
+        "requests_per_s": B * world / (ms_step * 1e-3),
+    }
+
+
 # ------------------------------------------------------------------------- oracle (CPU)
 def oracle_step_sample(n_req, seed, step, data):
     """One bounded oracle step over the first n_req requests of the workload (CPU)."""
@@ -569,8 +671,8 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.workload == "config4":
-        line = run_config4(args, rank, world, local_rank)
+    if args.workload in ("config4", "greedy"):
+        line = (run_config4 if args.workload == "config4" else run_greedy)(args, rank, world, local_rank)
         if line is not None:
             print(json.dumps(line), flush=True)
         if world > 1:

@@ -155,6 +155,15 @@ TSV_API tsv_status tsv_verify_workspace_size(const tsv_verify_args* a, size_t* b
 TSV_API tsv_status tsv_workspace_clear(void* workspace, size_t bytes, void* stream);
 TSV_API tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream);
 
+/* Greedy (temperature-0) verify, reading R24 (SURVEY.md
+ * 8(f) NEXT(2)): keep draft j iff x_j = argmax_v p_j[v] (first maximum, NaN never
+ * selected), emit the argmax of row m (correction at the first mismatch, or the
+ * bonus after k accepted drafts).  Same arguments as tsv_verify_accept; q, seed,
+ * step and request_ids are not used (request_ids may be NULL); vocab_offset must be
+ * 0.  Streams every p row of the batch (each needs its full argmax).  Outputs and
+ * device_status exactly as tsv_verify_accept (NO_WEIGHT: an all-NaN row). */
+TSV_API tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream);
+
 /* Vocab-sharded verify (the target's LM head split over G ranks as under
  * tensor parallelism).  Rank g holds columns
  * [vocab_offset, vocab_offset + vocab) of every p and q row.

@@ -656,6 +656,104 @@ __global__ void __launch_bounds__(256) verify_shard_emit_kernel(const RaceParams
     if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
 }
 
+// ------------------------------------------------------------------ greedy verify (NEXT 2)
+// Temperature 0 (reading R24): keep draft j iff x_j = argmax_v p_j[v]; emit the argmax of
+// row m.  Every row up to the first mismatch needs its full argmax, so the rows are streamed
+// densely: work items (row, chunk) grid-stride over all p rows of the batch; a lane keeps its
+// first maximum (strict >, NaN never selected), the warp combines packed keys
+// (monotone(value) << 32 | ~v: max value, then lowest index) and red.max-es them into the
+// row's slot; one warp per request then scans for the first mismatch and emits.
+__device__ __forceinline__ uint64_t greedy_key(float f, int32_t v) {  // v < 0: none
+    if (v < 0) return 0ull;
+    uint32_t u = __float_as_uint(f == 0.0f ? 0.0f : f);  // +0 == -0
+    u = (u >> 31) ? ~u : (u | 0x80000000u);               // order-preserving for non-NaN floats
+    return (static_cast<uint64_t>(u) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(v));
+}
+
+__global__ void __launch_bounds__(256, 4) verify_greedy_argmax_kernel(const RaceParams P) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int lane = threadIdx.x & 31;
+    const int32_t warp_id = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int32_t n_warps = gridDim.x * 8;
+    const int32_t rows = P.row_offsets[P.B];  // p rows that belong to requests
+    const int64_t n_items = static_cast<int64_t>(rows > 0 ? rows : 0) * P.n_chunks;
+    for (int64_t item = warp_id; item < n_items; item += n_warps) {
+        const int32_t r = static_cast<int32_t>(item % rows);  // row-minor: neighbours stream different rows
+        const int32_t c = static_cast<int32_t>(item / rows);
+        const int32_t col_begin = c * P.chunk;
+        const int32_t col_end = min(P.vocab, col_begin + P.chunk);
+        const float4* prow = reinterpret_cast<const float4*>(P.p + static_cast<int64_t>(r) * P.ld + col_begin);
+        const int32_t nq = (col_end - col_begin + 3) >> 2;
+        const int32_t nq_full = (col_end - col_begin) >> 2;  // float4s entirely inside the row
+        float best_f = 0.0f;
+        int32_t best_v = -1;
+        auto take = [&](float f, int32_t v) {
+            if (f == f && (best_v < 0 || f > best_f)) {
+                best_f = f;
+                best_v = v;
+            }
+        };
+        int32_t f = lane;
+        for (; f + 32 < nq_full; f += 64) {  // two float4 per lane in flight
+            const float4 a = ldg_stream(prow + f);
+            const float4 b = ldg_stream(prow + f + 32);
+            const int32_t v = col_begin + 4 * f;
+            take(a.x, v);
+            take(a.y, v + 1);
+            take(a.z, v + 2);
+            take(a.w, v + 3);
+            take(b.x, v + 128);
+            take(b.y, v + 129);
+            take(b.z, v + 130);
+            take(b.w, v + 131);
+        }
+        for (; f < nq; f += 32) {
+            const float4 a = ldg_stream(prow + f);
+            const int32_t v = col_begin + 4 * f;
+            const float e[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (v + t < col_end) take(e[t], v + t);
+        }
+        const uint64_t key = warp_max_u64(greedy_key(best_f, best_v));
+        if (lane == 0 && key) atomicMax(P.rowkey + r, static_cast<unsigned long long>(key));
+    }
+}
+
+__global__ void __launch_bounds__(256) verify_greedy_emit_kernel(const RaceParams P) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t r0 = P.row_offsets[i];
+    const int32_t r1 = P.row_offsets[i + 1];
+    const int32_t k = r1 - r0 - 1;
+    const int32_t qbase = r0 - i;
+    const bool ok = k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p;
+    int32_t x = -1, g = -1;
+    bool bad = false;
+    if (ok && lane <= k) {
+        const uint64_t key = P.rowkey[r0 + lane];
+        g = key ? key_index(key) : -1;
+        if (lane < k) {
+            x = P.drafts[qbase + lane];
+            bad = x < 0 || x >= P.vocab;
+        }
+    }
+    if (!ok || __ballot_sync(0xFFFFFFFFu, bad)) {
+        emit(P, i, 0, -1, -1);
+        if (lane == 0) report(P.devstatus, ok ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
+        return;
+    }
+    const uint32_t mism = __ballot_sync(0xFFFFFFFFu, lane < k && x != g);
+    const int32_t m = mism ? __ffs(mism) - 1 : k;
+    const int32_t t = __shfl_sync(0xFFFFFFFFu, g, m);
+    emit(P, i, qbase, m, t);
+    if (lane == 0 && t < 0) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+}
+
 // ------------------------------------------------------------------------ host side
 static int sm_count();
 // Default work-item size: about one item per resident warp of the race kernel
@@ -936,3 +1034,41 @@ extern "C" TSV_API tsv_status tsv_debug_trace_clear() {
     return TSV_OK;
 }
 #endif
+
+extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) {
+    TSV_REQUIRE(a != nullptr, "tsv_verify_greedy: args is NULL");
+    TSV_REQUIRE(a->B >= 0, "tsv_verify_greedy: B < 0 (%d)", a->B);
+    TSV_REQUIRE(a->k_max >= 0 && a->k_max <= TSV_MAX_K, "tsv_verify_greedy: k_max %d outside [0, %d]", a->k_max, TSV_MAX_K);
+    if (a->B == 0) return TSV_OK;
+    TSV_REQUIRE(a->p && a->row_offsets && a->num_accepted && a->out_tokens, "tsv_verify_greedy: a required array is NULL");
+    TSV_REQUIRE(a->draft_tokens || a->rows_p == a->B, "tsv_verify_greedy: draft_tokens is NULL");
+    TSV_REQUIRE(a->ld > 0 && a->ld % 4 == 0, "tsv_verify_greedy: ld %lld must be a positive multiple of 4", (long long)a->ld);
+    TSV_REQUIRE(aligned16(a->p), "tsv_verify_greedy: p must be 16-byte aligned");
+    TSV_REQUIRE(a->vocab >= 1 && a->vocab <= a->ld, "tsv_verify_greedy: vocab %d outside [1, ld]", a->vocab);
+    TSV_REQUIRE(a->vocab_offset == 0, "tsv_verify_greedy: vocab sharding is not supported");
+    TSV_REQUIRE(a->rows_p >= a->B, "tsv_verify_greedy: rows_p %d < B %d", a->rows_p, a->B);
+    TSV_REQUIRE(a->chunk == 0 || (a->chunk >= 128 && a->chunk % 128 == 0 && a->chunk <= kMaxChunk),
+                "tsv_verify_greedy: chunk must be 0 or a multiple of 128 in [128, %d]", kMaxChunk);
+    TSV_TRY(check_device());
+    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+                "tsv_verify_greedy: workspace too small (%llu < %llu bytes)",
+                (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    tsv_verify_args b = *a;
+    if (b.chunk == 0) {  // about one item per resident warp over all rows
+        const int64_t warps = static_cast<int64_t>(sm_count()) * 32;
+        int64_t c = (static_cast<int64_t>(a->rows_p) * a->vocab + warps - 1) / warps;
+        c = (c + 127) / 128 * 128;
+        b.chunk = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(c, 1024), kMaxChunk));
+    }
+    RaceParams P = make_params(&b);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TSV_CUDA(cudaMemsetAsync(P.rowkey, 0, sizeof(unsigned long long) * static_cast<size_t>(a->rows_p), st),
+             "cudaMemsetAsync");
+    const int64_t n_items = static_cast<int64_t>(a->rows_p) * P.n_chunks;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * 4));
+    TSV_CUDA(launch_pdl(verify_greedy_argmax_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, P),
+             "verify_greedy_argmax_kernel launch");
+    TSV_CUDA(launch_pdl(verify_greedy_emit_kernel, dim3(static_cast<unsigned>((a->B + 7) / 8)), dim3(256), 0, st, P),
+             "verify_greedy_emit_kernel launch");
+    return TSV_OK;
+}

@@ -39,7 +39,7 @@ EXPORTED = [
     "tsv_propose_lookup_choose_k", "tsv_verify_accept_update", "tsv_debug_race_E", "tsv_debug_philox",
     "tsv_goodput_partial", "tsv_goodput_finalize", "tsv_goodput_choose_k_sharded", "tsv_update_partial",
     "tsv_update_finalize", "tsv_update_acceptance_sharded", "tsv_verify_shard_flags", "tsv_verify_shard_race",
-    "tsv_verify_shard_emit",
+    "tsv_verify_shard_emit", "tsv_verify_greedy",
 ]
 
 
@@ -119,6 +119,7 @@ def _load() -> ctypes.CDLL:
         "tsv_verify_shard_flags": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
         "tsv_verify_shard_race": ([ctypes.POINTER(VerifyArgs), P, P, P], ctypes.c_int),
         "tsv_verify_shard_emit": ([ctypes.POINTER(VerifyArgs), P, P, P], ctypes.c_int),
+        "tsv_verify_greedy": ([ctypes.POINTER(VerifyArgs), P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -266,6 +267,26 @@ def tsv_verify_accept(p, q, row_offsets, draft_tokens, request_ids, seed, step, 
         a.workspace = workspace.data_ptr()
         a.workspace_bytes = workspace.numel()
     _check(_lib.tsv_verify_accept(ctypes.byref(a), _stream(stream)))
+    return num_accepted, out_tokens
+
+
+def tsv_verify_greedy(p, row_offsets, draft_tokens, k_max, num_accepted=None, out_tokens=None,
+                      device_status=None, workspace=None, vocab=None, chunk=0, stream=None):
+    """Greedy (temperature-0) verify (reading R24).  Returns (num_accepted, out_tokens)."""
+    B = row_offsets.numel() - 1
+    dev = p.device
+    if num_accepted is None:
+        num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
+    if out_tokens is None:
+        out_tokens = torch.empty((B, k_max + 1), dtype=torch.int32, device=dev)
+    rids = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)  # unused by the greedy rule
+    a = make_verify_args(p, None, row_offsets, draft_tokens, rids[:B] if B else rids, 0, 0, k_max,
+                         num_accepted, out_tokens, device_status, workspace, vocab=vocab, chunk=chunk)
+    if workspace is None and B > 0:
+        workspace = alloc_workspace(tsv_verify_workspace_size(a), dev)
+        a.workspace = workspace.data_ptr()
+        a.workspace_bytes = workspace.numel()
+    _check(_lib.tsv_verify_greedy(ctypes.byref(a), _stream(stream)))
     return num_accepted, out_tokens
 
 

@@ -641,3 +641,64 @@ def test_step_graph_capture_matches_eager(tsv, fused):
     torch.cuda.synchronize()
     for k, v in st2.outputs().items():
         assert torch.equal(v, eager[k]), k
+
+
+# ------------------------------------------------------------------- greedy verify (NEXT 2)
+def assert_greedy_parity(tsv, p, ro, drafts, k_max, vocab=None, chunk=0):
+    ona, oout, ost = oracle.verify_greedy(p, ro, drafts, k_max, vocab=vocab)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    dt = torch.tensor(drafts if len(drafts) else np.zeros(0, np.int32), dtype=torch.int32, device=DEV)
+    na, out = tsv.tsv_verify_greedy(torch.tensor(p, device=DEV), torch.tensor(ro, device=DEV), dt, k_max,
+                                    device_status=st, vocab=vocab, chunk=chunk)
+    torch.cuda.synchronize()
+    assert (_np(na) == ona).all() and (_np(out) == oout).all()
+    assert int(st.item()) == ost
+    return ona
+
+
+def _greedy_batch(B, V, k_max, seed, accept=0.7, ld=None, ties=False):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    ks = rng.integers(0, k_max + 1, B)
+    ro = np.zeros(B + 1, np.int32)
+    ro[1:] = np.cumsum(ks + 1)
+    R = int(ro[-1])
+    ld = (V + 3) // 4 * 4 if ld is None else ld  # rows padded to a multiple of 4 (tsv_verify_args.ld)
+    if ties:
+        p = rng.integers(0, 5, (R, ld)).astype(np.float32)
+    else:
+        p = rng.standard_normal((R, ld)).astype(np.float32)
+    am = p[:, :V].argmax(axis=1)
+    drafts = []
+    for i in range(B):
+        for j in range(ks[i]):
+            r = ro[i] + j
+            drafts.append(int(am[r]) if rng.random() < accept else int(rng.integers(0, V)))
+    return p, ro, np.array(drafts, np.int32)
+
+
+@pytest.mark.parametrize("B,V,k_max", [(4, 32000, 4), (256, 32000, 8), (37, 4099, 15), (9, 13, 3), (5, 1, 2)])
+def test_greedy_parity(tsv, B, V, k_max):
+    p, ro, d = _greedy_batch(B, V, k_max, seed=B + V)
+    na = assert_greedy_parity(tsv, p, ro, d, k_max, vocab=V)
+    assert (na >= 0).all()
+
+
+def test_greedy_ties_nan_padded_chunks(tsv):
+    p, ro, d = _greedy_batch(50, 3000, 6, seed=3, ties=True, ld=3008)
+    p[:, 3000:] = 1e30  # beyond vocab: never read
+    for chunk in (0, 128, 640):
+        assert_greedy_parity(tsv, p, ro, d, 6, vocab=3000, chunk=chunk)
+    p2, ro2, d2 = _greedy_batch(20, 700, 4, seed=4)
+    p2[::3, ::7] = np.nan
+    p2[5] = np.nan                       # all-NaN row -> NO_WEIGHT if it is emitted
+    p2[7] = -np.inf
+    p2[9, :] = 0.0
+    p2[9, 350] = -0.0
+    assert_greedy_parity(tsv, p2, ro2, d2, 4)
+
+
+def test_greedy_bad_tokens(tsv):
+    p, ro, d = _greedy_batch(12, 500, 3, seed=5)
+    if len(d):
+        d[0] = 500
+    assert_greedy_parity(tsv, p, ro, d, 3)
