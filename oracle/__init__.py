@@ -10,6 +10,7 @@ Functions (each cites its passage in oracle.c):
   philox4x32_10, u_acc, u_race, E, E_table  -- RNG and race uniforms (R6, R9)
   verify       -- rejection-sampling accept + residual/bonus race
   verify_greedy -- temperature-0 verify: keep drafts equal to the target argmax
+  softmax_rows, verify_logits -- probabilities from logits (reading R23), then verify
   lookup       -- prompt-lookup n-gram proposal
   expected_len, forward_time, choose_k -- goodput adaptor
   update       -- moving-average acceptance update
@@ -71,6 +72,8 @@ def _load():
         lib.oracle_verify.restype = i32
         lib.oracle_verify_greedy.argtypes = [P, i64, i32, P, P, i32, i32, P, P]
         lib.oracle_verify_greedy.restype = i32
+        lib.oracle_softmax_rows.argtypes = [P, i64, i32, i32, ctypes.c_float, P]
+        lib.oracle_softmax_rows.restype = None
         lib.oracle_lookup.argtypes = [P, P, i32, i32, i32, i32, P, P]
         lib.oracle_lookup.restype = None
         lib.oracle_expected_len.argtypes = [f64, i32]
@@ -166,6 +169,25 @@ def verify_greedy(p, row_offsets, draft_tokens, k_max, vocab=None):
     out = np.zeros((B, k_max + 1), np.int32)
     st = lib.oracle_verify_greedy(_ptr(p), ld, V, _ptr(ro), _ptr(dt), B, int(k_max), _ptr(na), _ptr(out))
     return na, out, int(st)
+
+
+def softmax_rows(z, temperature=1.0, vocab=None):
+    """Reading R23: fp32 exp, fp64 row sum, p = RN32(e * RN32(1/S)).  z: float32 [rows, ld]."""
+    lib = _load()
+    z = _c(z, np.float32)
+    rows, ld = z.shape
+    V = ld if vocab is None else int(vocab)
+    out = np.zeros_like(z)
+    lib.oracle_softmax_rows(_ptr(z), ld, V, rows, float(temperature), _ptr(out))
+    return out
+
+
+def verify_logits(zp, zq, row_offsets, draft_tokens, request_ids, seed, step, k_max, temperature=1.0,
+                  vocab=None):
+    """Fused-logits verify (NEXT 1): softmax_rows of the target and draft logits, then verify."""
+    p = softmax_rows(zp, temperature, vocab)
+    q = None if zq is None else softmax_rows(zq, temperature, vocab)
+    return verify(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max, vocab=vocab)
 
 
 def lookup(ctx, ctx_offsets, n_min, n_max, K):

@@ -293,6 +293,40 @@ int32_t oracle_verify_greedy(const float* p, int64_t ld, int32_t V, const int32_
     return status;
 }
 
+/* Softmax from logits with temperature (reading R23: "p = softmax(z)
+ * with fp32 exp, fp64 row sums"; the sampler of PAPER.md:493 receives the target / draft
+ * distributions, which a serving stack holds as logits).  Per row, written out:
+ *   inv_tau = RN32(1 / tau);  M = max_{v<V} z_v;
+ *   e_v = expf(RN32(RN32(z_v - M) * inv_tau));  S = sum_v e_v in binary64 (ascending v);
+ *   inv_S = RN32(1 / S);  p_v = RN32(e_v * inv_S).
+ * Logits are finite (or -inf).  The verify of R1-R9 then runs on these p (and q) rows. */
+void oracle_softmax_rows(const float* z, int64_t ld, int32_t V, int32_t rows, float temperature,
+                         float* p_out)
+{
+    int32_t r, v;
+    const float inv_tau = (float)(1.0 / (double)temperature);
+    for (r = 0; r < rows; ++r) {
+        const float* zr = z + (int64_t)r * ld;
+        float* pr = p_out + (int64_t)r * ld;
+        float M = zr[0], inv_S;
+        double S = 0.0;
+        for (v = 1; v < V; ++v)
+            if (zr[v] > M) M = zr[v];
+        for (v = 0; v < V; ++v) {
+            float d = zr[v] - M;
+            float a = d * inv_tau;
+            S += (double)expf(a);
+        }
+        inv_S = (float)(1.0 / S);
+        for (v = 0; v < V; ++v) {
+            float d = zr[v] - M;
+            float a = d * inv_tau;
+            pr[v] = expf(a) * inv_S;
+        }
+        for (v = V; v < ld; ++v) pr[v] = 0.0f;
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,

@@ -32,6 +32,9 @@ int32_t oracle_verify_greedy(const float* p, int64_t ld, int32_t V, const int32_
                              const int32_t* draft_tokens, int32_t B, int32_t k_max,
                              int32_t* num_accepted, int32_t* out_tokens);
 
+void oracle_softmax_rows(const float* z, int64_t ld, int32_t V, int32_t rows, float temperature,
+                         float* p_out);
+
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,
                    int32_t* proposals, int32_t* proposal_len);
