@@ -49,10 +49,11 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
-    ap.add_argument("--workload", default="step", choices=["step", "config4", "greedy"],
+    ap.add_argument("--workload", default="step", choices=["step", "config4", "greedy", "logits"],
                     help="step: the default decode step; config4: Llama-3 vocab-sharded verify (V=128256) "
                          "through tsv_verify_accept_sharded over the N ranks (strong scaling); greedy: the "
-                         "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling)")
+                         "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling); logits: the fused "
+                         "softmax-from-logits verify (NEXT 1) on the config-2 batch given as logits")
     ap.add_argument("--shard-mode", default="lazy", choices=["lazy", "dense"], help="config4 sharding mode")
     return ap.parse_args()
 
@@ -582,6 +583,103 @@ def run_greedy(args, rank, world, local_rank):
     }
 
 
+# ------------------------------------------------------------ fused softmax from logits (NEXT 1)
+def run_logits(args, rank, world, local_rank):
+    """tsv_verify_accept_logits on the config-2 batch with p and q given as logits (temperature 1):
+    one dense statistics pass over every p and q row, then the lazy race of row m from logits."""
+    import torch
+
+    import synth
+    from paper_2406_14066_b200 import dist as pdist
+    from paper_2406_14066_b200 import tsv
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    R = max(2, args.sets)
+    seed = synth.DEFAULT_SEED
+    sets, footprint = [], 0
+    for s in range(R):
+        vb = synth.make_logits_batch(B=B, V=V, k_max=K_MAX, lam=0.7, seed=seed + 53 * s + rank, device=dev)
+        vb.request_ids += rank * B
+        footprint += (vb.p.numel() + vb.q.numel()) * 4
+        sets.append(vb)
+    na = torch.empty(B, dtype=torch.int32, device=dev)
+    outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
+    W, K = max(3, args.warmup), args.steps
+    gl = max(1, min(args.graph_steps, K))
+    args_list = []
+    for t in range(gl):
+        vb = sets[t % R]
+        args_list.append(tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t,
+                                              K_MAX, na, outt, None, None, chunk=args.chunk))
+    ws = tsv.alloc_workspace(max(tsv.tsv_verify_logits_workspace_size(a) for a in args_list), dev)
+    for a in args_list:
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    L = tsv.lib()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        tsv._check(L.tsv_verify_accept_logits(tsv.ctypes.byref(args_list[0]), 1.0, side.cuda_stream))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for a in args_list:
+            tsv._check(L.tsv_verify_accept_logits(tsv.ctypes.byref(a), 1.0, side.cuda_stream))
+    for _ in range((W + gl - 1) // gl):
+        g.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(1, K // gl)
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier(device_ids=[local_rank])
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    t_ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    steps = reps * gl
+    tok, vbytes = 0, 0.0
+    for t in range(gl):
+        tsv._check(L.tsv_verify_accept_logits(tsv.ctypes.byref(args_list[t]), 1.0, None))
+        torch.cuda.synchronize()
+        vb = sets[t % R]
+        m = na.cpu().numpy()
+        k = vb.k.cpu().numpy()
+        tok += int((m + 1).sum())
+        # every p and q row once (statistics) + row m of p (and q on a rejection) again (the race)
+        vbytes += float(((2 * k + 1) * V * 4).sum() + verify_alg_bytes(m, k, True, V, K_MAX))
+    tok_total = pdist.sum_over_ranks(tok, dev) / gl
+    vbytes /= gl
+    ms_step = t_ms / steps
+    if rank != 0:
+        return None
+    peak, peak_src = load_peaks()
+    achieved = vbytes / (ms_step * 1e-3) / 1e9
+    return {
+        "metric": METRIC, "value": tok_total / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
+        "config": {"workload": f"fused softmax-from-logits verify (NEXT 1): B={B}, k~U{{0..{K_MAX}}}, V={V}, "
+                               f"fp32 target and draft logits, temperature 1, lambda=0.7",
+                   "global_batch": B * world, "vocab": V, "k_max": K_MAX, "parallelism": f"request-sharded x{world}",
+                   "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank", "graph_steps": gl},
+        "roofline": {"kernel": "tsv_verify_accept_logits (stats + scan + race + emit)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
+        "clocks": sampler.summary(),
+        "gpu_launches": 4 * steps,
+        "e2e": None,
+        "tokens_per_step": tok_total,
+        "requests_per_s": B * world / (ms_step * 1e-3),
+    }
+
+
 # ------------------------------------------------------------------------- oracle (CPU)
 def oracle_step_sample(n_req, seed, step, data):
     """One bounded oracle step over the first n_req requests of the workload (CPU)."""
@@ -671,8 +769,9 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.workload in ("config4", "greedy"):
-        line = (run_config4 if args.workload == "config4" else run_greedy)(args, rank, world, local_rank)
+    if args.workload in ("config4", "greedy", "logits"):
+        fn = {"config4": run_config4, "greedy": run_greedy, "logits": run_logits}[args.workload]
+        line = fn(args, rank, world, local_rank)
         if line is not None:
             print(json.dumps(line), flush=True)
         if world > 1:

@@ -164,6 +164,24 @@ TSV_API tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream);
  * device_status exactly as tsv_verify_accept (NO_WEIGHT: an all-NaN row). */
 TSV_API tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream);
 
+/* Fused softmax-from-logits verify, reading R23: a->p and
+ * a->q hold LOGITS (same layout as the probability rows; q may be NULL for one-hot
+ * drafts).  Per row p_v = RN32(expf(RN32(RN32(z_v - M) * RN32(1/temperature))) *
+ * RN32(1/S)), M = max z, S = binary64 sum of the exponentials; then exactly the
+ * verify of tsv_verify_accept on those probabilities.  The probabilities are never
+ * written: one dense pass over every p and q row of the batch computes per-chunk
+ * online softmax partials, the acceptance scan combines them per tested row, and the
+ * lazy race forms row m's probabilities from its logits while streaming it.
+ * Parity with the CPU oracle is within 1e-6 relative on probabilities (CUDA expf is
+ * within 2 ulp, the sums are reordered); decisions inside that margin may flip.
+ * Workspace: tsv_verify_logits_workspace_size (zero-filled not required).
+ * tsv_softmax_rows: the same probabilities written out for `rows` rows of z
+ * (fp32 [rows, ld]; columns >= vocab of p_out are set to 0). */
+TSV_API tsv_status tsv_verify_logits_workspace_size(const tsv_verify_args* a, size_t* bytes);
+TSV_API tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float temperature, void* stream);
+TSV_API tsv_status tsv_softmax_rows(const float* z, int64_t ld, int32_t vocab, int32_t rows, float temperature,
+                                    float* p_out, void* stream);
+
 /* Vocab-sharded verify (the target's LM head split over G ranks as under
  * tensor parallelism).  Rank g holds columns
  * [vocab_offset, vocab_offset + vocab) of every p and q row.

@@ -299,7 +299,8 @@ int32_t oracle_verify_greedy(const float* p, int64_t ld, int32_t V, const int32_
  *   inv_tau = RN32(1 / tau);  M = max_{v<V} z_v;
  *   e_v = expf(RN32(RN32(z_v - M) * inv_tau));  S = sum_v e_v in binary64 (ascending v);
  *   inv_S = RN32(1 / S);  p_v = RN32(e_v * inv_S).
- * Logits are finite (or -inf).  The verify of R1-R9 then runs on these p (and q) rows. */
+ * Logits are finite or -inf, at least one finite per row.  The verify of R1-R9 then runs on
+ * these p (and q) rows. */
 void oracle_softmax_rows(const float* z, int64_t ld, int32_t V, int32_t rows, float temperature,
                          float* p_out)
 {

@@ -46,6 +46,8 @@ struct RaceParams {
     uint32_t* rowT;            // [n_key_rows] shared race threshold per raced row (float bits)
     unsigned long long* rowkey;  // [n_key_rows] max race key per raced row (0: nothing evaluated)
     tsv_shard_tuple* tuples;   // shard mode
+    const float4* lstats;      // logits mode: per request (M_p, 1/S_p, M_q, 1/S_q) of row m
+    float inv_tau;             // logits mode: RN32(1 / temperature)
     int64_t ld;
     uint32_t k0, k1, step;
     int32_t B, k_max, vocab, vocab_offset, vocab_global, chunk, n_chunks, rows_p;
@@ -53,6 +55,16 @@ struct RaceParams {
 };
 
 enum Mode { kLazy = 0, kShard = 1 };
+
+// Logits mode (reading R23): p = RN32(expf(RN32(RN32(z - M) * inv_tau)) * inv_S), CUDA's
+// accurate expf (<= 2 ulp; the oracle's glibc expf is correctly rounded).
+__device__ __forceinline__ float to_prob(float z, float M, float inv_S, float inv_tau) {
+    return __fmul_rn(expf(__fmul_rn(__fsub_rn(z, M), inv_tau)), inv_S);
+}
+__device__ __forceinline__ float4 to_prob4(const float4& z, float M, float inv_S, float inv_tau) {
+    return make_float4(to_prob(z.x, M, inv_S, inv_tau), to_prob(z.y, M, inv_S, inv_tau),
+                       to_prob(z.z, M, inv_S, inv_tau), to_prob(z.w, M, inv_S, inv_tau));
+}
 
 constexpr int kMaxChunk = 16384;
 constexpr float kPruneC = 0x1.fffffap-1f;        // 1 - 3*2^-24 <= (1-2^-23)(1-2^-24)
@@ -318,7 +330,7 @@ __device__ __forceinline__ uint32_t smid() {
 }
 #endif
 
-template <int MODE, bool DENSE_Q, bool PRUNE>
+template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false>
 __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const RaceParams P) {
     pdl_wait();  // the scan kernel's ReqMeta / rowT / rowkey are complete and visible
     pdl_launch_dependents();
@@ -355,6 +367,7 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
         const int32_t nq = (col_end - col_begin + 3) >> 2;
         const int32_t iters = (nq + 31) >> 5;
         const RaceCtr rc = race_ctr((kPurposeRace << 16) | static_cast<uint32_t>(sel), rm.rid, P.step, P.k0, P.k1);
+        const float4 ls = LOGITS ? P.lstats[i] : make_float4(0.f, 0.f, 0.f, 0.f);  // row m's softmax stats
         Race R;
         R.init();
         const int32_t nfull = (col_end - col_begin) >> 7;  // iterations with all 128 columns in range
@@ -365,6 +378,13 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
             for (int u = 0; u < kUnroll; ++u) a[u] = ldg_stream(prow + (it + u) * 32 + lane);
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) b[u] = use_q ? ldg_stream(qrow + (it + u) * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (LOGITS) {
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    a[u] = to_prob4(a[u], ls.x, ls.y, P.inv_tau);
+                    if (use_q) b[u] = to_prob4(b[u], ls.z, ls.w, P.inv_tau);
+                }
+            }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
                 const int32_t col = col_begin + 4 * ((it + u) * 32 + lane);
@@ -382,8 +402,12 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
             float w[4] = {0.f, 0.f, 0.f, 0.f};
             uint4 r = make_uint4(0, 0, 0, 0);
             if (f < nq) {
-                const float4 a = ldg_stream(prow + f);
-                const float4 b = use_q ? ldg_stream(qrow + f) : a;
+                float4 a = ldg_stream(prow + f);
+                float4 b = use_q ? ldg_stream(qrow + f) : a;
+                if (LOGITS) {
+                    a = to_prob4(a, ls.x, ls.y, P.inv_tau);
+                    if (use_q) b = to_prob4(b, ls.z, ls.w, P.inv_tau);
+                }
                 quad_weights<DENSE_Q>(w, a, b, residual, col, col_end, xm_local);
                 r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col >> 2), P);
             }
@@ -418,8 +442,9 @@ __global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const Race
 // element of a row is always evaluated), i.e. the residual is identically zero: the
 // warp then races max(0, p_m) over the row itself (R5; measure-zero, not performance
 // relevant).
-template <bool PRUNE>
-__device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_t sel, uint32_t rid) {
+template <bool PRUNE, bool LOGITS = false>
+__device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_t sel, uint32_t rid,
+                                  float M = 0.f, float inv_S = 0.f) {
     const RaceCtr rc = race_ctr((kPurposeRace << 16) | static_cast<uint32_t>(sel), rid, P.step, P.k0, P.k1);
     const int lane = threadIdx.x & 31;
     const float4* p4 = reinterpret_cast<const float4*>(prow);
@@ -433,7 +458,8 @@ __device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_
         float w[4] = {0.f, 0.f, 0.f, 0.f};
         uint4 r = make_uint4(0, 0, 0, 0);
         if (f < nq) {
-            const float4 a = p4[f];
+            float4 a = p4[f];
+            if (LOGITS) a = to_prob4(a, M, inv_S, P.inv_tau);
             quad_weights<true>(w, a, a, false, col, P.vocab, -1);
             r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(f), P);
         }
@@ -444,7 +470,7 @@ __device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_
     return warp_max_u64(F.best);
 }
 
-template <int MODE, bool PRUNE>
+template <int MODE, bool PRUNE, bool LOGITS = false>
 __device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
     const int lane = threadIdx.x & 31;
     if (unit >= P.B) return;
@@ -452,8 +478,11 @@ __device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
     if (rm.ok != 1) return;  // lazy: emitted by the scan kernel; shard: flagged by the combine
     if (MODE == kLazy) {
         uint64_t key = P.rowkey[unit];
-        if (key == 0 && rm.m < rm.k)  // R5: residual identically zero -> race over p_m
-            key = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
+        if (key == 0 && rm.m < rm.k) {  // R5: residual identically zero -> race over p_m
+            const float4 ls = LOGITS ? P.lstats[unit] : make_float4(0.f, 0.f, 0.f, 0.f);
+            key = warp_race_row<PRUNE, LOGITS>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid,
+                                               ls.x, ls.y);
+        }
         emit(P, unit, rm.qbase, rm.m, key ? key_index(key) : -1);
         if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
     } else {
@@ -475,7 +504,7 @@ __device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
 // the emitting CTAs -- the alpha update fused into the verify call.  It needs only the
 // accepted counts, which the scan kernel already wrote (complete and visible here, two
 // kernels back), so no inter-CTA handshake is needed.
-template <int MODE, bool PRUNE, bool UPDATE>
+template <int MODE, bool PRUNE, bool UPDATE, bool LOGITS = false>
 __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P, UpdateArgs ua) {
     pdl_wait();
     pdl_launch_dependents();
@@ -483,7 +512,7 @@ __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P, Up
         update_block(ua);
         return;
     }
-    emit_unit<MODE, PRUNE>(P, blockIdx.x * 8 + (threadIdx.x >> 5));
+    emit_unit<MODE, PRUNE, LOGITS>(P, blockIdx.x * 8 + (threadIdx.x >> 5));
 }
 
 // ------------------------------------------------------------------------ shard combine
@@ -754,6 +783,182 @@ __global__ void __launch_bounds__(256) verify_greedy_emit_kernel(const RaceParam
     if (lane == 0 && t < 0) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
 }
 
+// ------------------------------------------------------------ fused softmax from logits (NEXT 1)
+// p and q arrive as logits (reading R23).  Pass 1 (dense, every p and q row of the batch):
+// per (row, chunk) item the warp's online softmax partial (m_c = max z, s_c = sum of
+// expf((z - m_c) / tau) in binary64) goes to a partials table.  Pass 2 (one warp per
+// request): lanes combine the partials of rows j (M = max m_c, S = sum s_c exp((m_c - M)/tau)),
+// run the acceptance test on p_j[x_j], q_j[x_j] computed from the logits, and publish
+// row m's (M_p, 1/S_p, M_q, 1/S_q) next to ReqMeta.  Then the lazy race streams row m's logits
+// and forms the probabilities on the fly -- p and q are never written out.
+struct LogitPartial {
+    float m;
+    float pad;
+    double s;
+};
+
+__device__ __forceinline__ void online_push(float z, float inv_tau, float& m, double& s) {
+    if (z > m) {  // new running max: rescale the sum (also the first finite value: s = 0)
+        s = s * exp(static_cast<double>(__fmul_rn(__fsub_rn(m, z), inv_tau))) + 1.0;
+        m = z;
+    } else {
+        s += static_cast<double>(expf(__fmul_rn(__fsub_rn(z, m), inv_tau)));
+    }
+}
+
+__global__ void __launch_bounds__(256, 4) verify_logit_stats_kernel(const RaceParams P, LogitPartial* part,
+                                                                    int32_t rows_q_max) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int lane = threadIdx.x & 31;
+    const int32_t warp_id = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int32_t n_warps = gridDim.x * 8;
+    const int32_t rp = P.row_offsets[P.B];  // p rows in use; q rows: rp - B
+    const int32_t rq = (P.q != nullptr) ? rp - P.B : 0;
+    const int64_t n_items = static_cast<int64_t>(rp + rq) * P.n_chunks;
+    for (int64_t item = warp_id; item < n_items; item += n_warps) {
+        const int32_t r = static_cast<int32_t>(item % (rp + rq));
+        const int32_t c = static_cast<int32_t>(item / (rp + rq));
+        const bool isq = r >= rp;
+        const float* row = isq ? P.q + static_cast<int64_t>(r - rp) * P.ld : P.p + static_cast<int64_t>(r) * P.ld;
+        const int32_t col_begin = c * P.chunk;
+        const int32_t col_end = min(P.vocab, col_begin + P.chunk);
+        const float4* z4 = reinterpret_cast<const float4*>(row + col_begin);
+        const int32_t nq = (col_end - col_begin + 3) >> 2;
+        float m = -INFINITY;
+        double s = 0.0;
+        for (int32_t f = lane; f < nq; f += 32) {
+            const float4 z = ldg_stream(z4 + f);
+            const int32_t v = col_begin + 4 * f;
+            const float e[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (v + t < col_end && e[t] > -INFINITY) online_push(e[t], P.inv_tau, m, s);
+        }
+        // warp combine: M = max m, S = sum s exp((m - M)/tau)
+        float M = m;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
+        double sc = (m > -INFINITY) ? s * exp(static_cast<double>(__fmul_rn(__fsub_rn(m, M), P.inv_tau))) : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xFFFFFFFFu, sc, o);
+        if (lane == 0) {
+            const int64_t slot = (isq ? static_cast<int64_t>(P.rows_p) + (r - rp) : r) * P.n_chunks + c;
+            part[slot].m = M;
+            part[slot].pad = 0.f;
+            part[slot].s = sc;
+        }
+    }
+    (void)rows_q_max;
+}
+
+// (M, RN32(1/S)) of one row from its chunk partials.
+__device__ __forceinline__ float2 logit_row_stats(const RaceParams& P, const LogitPartial* part, int64_t slot0) {
+    float M = -INFINITY;
+    for (int32_t c = 0; c < P.n_chunks; ++c) M = fmaxf(M, part[slot0 + c].m);
+    double S = 0.0;
+    for (int32_t c = 0; c < P.n_chunks; ++c) {
+        const LogitPartial pc = part[slot0 + c];
+        if (pc.m > -INFINITY) S += pc.s * exp(static_cast<double>(__fmul_rn(__fsub_rn(pc.m, M), P.inv_tau)));
+    }
+    return make_float2(M, __double2float_rn(1.0 / S));
+}
+
+__global__ void __launch_bounds__(256) verify_logit_scan_kernel(const RaceParams P, const LogitPartial* part,
+                                                                float4* lstats) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t r0 = P.row_offsets[i];
+    const int32_t r1 = P.row_offsets[i + 1];
+    const int32_t k = r1 - r0 - 1;
+    const int32_t qbase = r0 - i;
+    int32_t ok = (k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p) ? 1 : 0;
+    const uint32_t rid = P.rids[i];
+    int32_t x = -1;
+    bool bad = false, acc = false;
+    float2 sp = make_float2(0.f, 0.f), sq = make_float2(0.f, 0.f);
+    if (ok && lane <= k) sp = logit_row_stats(P, part, static_cast<int64_t>(r0 + lane) * P.n_chunks);
+    if (ok && lane < k && P.q) sq = logit_row_stats(P, part, (static_cast<int64_t>(P.rows_p) + qbase + lane) * P.n_chunks);
+    if (ok && lane < k) {
+        x = P.drafts[qbase + lane];
+        bad = x < 0 || x >= P.vocab;
+        if (!bad) {
+            const uint4 rr = philox4x32_10(0u, (kPurposeAccept << 16) | static_cast<uint32_t>(lane), rid, P.step,
+                                           P.k0, P.k1);
+            const float u = u_acc_from_word(rr.x);
+            const float qx = P.q ? to_prob(P.q[static_cast<int64_t>(qbase + lane) * P.ld + x], sq.x, sq.y, P.inv_tau) : 1.0f;
+            const float px = to_prob(P.p[static_cast<int64_t>(r0 + lane) * P.ld + x], sp.x, sp.y, P.inv_tau);
+            acc = __fmul_rn(u, qx) < px;  // strict; NaN rejects
+        }
+    }
+    if (__ballot_sync(0xFFFFFFFFu, bad)) ok = 2;
+    const uint32_t accm = __ballot_sync(0xFFFFFFFFu, acc);
+    const uint32_t kmask = (ok == 1 && k > 0) ? ((1u << k) - 1u) : 0u;
+    const uint32_t rej = ~accm & kmask;
+    const int32_t m = rej ? (__ffs(rej) - 1) : (ok == 1 ? k : -1);
+    const int32_t src = (m >= 0 ? m : 0) & 31;
+    const int32_t xm = __shfl_sync(0xFFFFFFFFu, x, src);
+    const float4 st = make_float4(__shfl_sync(0xFFFFFFFFu, sp.x, src), __shfl_sync(0xFFFFFFFFu, sp.y, src),
+                                  __shfl_sync(0xFFFFFFFFu, sq.x, src), __shfl_sync(0xFFFFFFFFu, sq.y, src));
+    if (lane == 0) {
+        ReqMeta rm;
+        rm.r0 = r0;
+        rm.k = k;
+        rm.qbase = qbase;
+        rm.m = m;
+        rm.xm = (m >= 0 && m < k) ? xm : -1;
+        rm.ok = ok;
+        rm.rid = rid;
+        rm.pad = 0;
+        P.meta[i] = rm;
+        lstats[i] = st;
+        P.rowT[i] = 0u;
+        P.rowkey[i] = 0ull;
+        P.num_accepted[i] = m;
+    }
+    if (ok != 1) {
+        emit(P, i, 0, -1, -1);
+        if (lane == 0) report(P.devstatus, ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
+    }
+}
+
+// Standalone softmax rows (reading R23), one CTA per row: max, binary64 sum of expf, write p.
+__global__ void __launch_bounds__(256) softmax_rows_kernel(const float* z, int64_t ld, int32_t V, float inv_tau,
+                                                           float* out) {
+    __shared__ float s_m[8];
+    __shared__ double s_s[8];
+    pdl_wait();
+    pdl_launch_dependents();
+    const float* zr = z + static_cast<int64_t>(blockIdx.x) * ld;
+    float* pr = out + static_cast<int64_t>(blockIdx.x) * ld;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float m = -INFINITY;
+    for (int32_t v = threadIdx.x; v < V; v += 256) m = fmaxf(m, zr[v]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if (lane == 0) s_m[warp] = m;
+    __syncthreads();
+    float M = s_m[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) M = fmaxf(M, s_m[w]);
+    double s = 0.0;
+    for (int32_t v = threadIdx.x; v < V; v += 256)
+        s += static_cast<double>(expf(__fmul_rn(__fsub_rn(zr[v], M), inv_tau)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (lane == 0) s_s[warp] = s;
+    __syncthreads();
+    double S = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) S += s_s[w];
+    const float inv_S = __double2float_rn(1.0 / S);
+    for (int32_t v = threadIdx.x; v < V; v += 256) pr[v] = to_prob(zr[v], M, inv_S, inv_tau);
+    for (int64_t v = V + threadIdx.x; v < ld; v += 256) pr[v] = 0.0f;
+}
+
 // ------------------------------------------------------------------------ host side
 static int sm_count();
 // Default work-item size: about one item per resident warp of the race kernel
@@ -809,6 +1014,8 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.out_tokens = a->out_tokens;
     P.devstatus = a->device_status;
     P.tuples = nullptr;
+    P.lstats = nullptr;
+    P.inv_tau = 1.0f;
     P.ld = a->ld;
     P.k0 = static_cast<uint32_t>(a->seed & 0xFFFFFFFFull);
     P.k1 = static_cast<uint32_t>(a->seed >> 32);
@@ -847,9 +1054,9 @@ static int sm_count() {
     return n[dev] > 0 ? n[dev] : 148;
 }
 
-template <int MODE, bool DENSE_Q, bool PRUNE>
+template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false>
 static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
-    auto kern = verify_race_kernel<MODE, DENSE_Q, PRUNE>;
+    auto kern = verify_race_kernel<MODE, DENSE_Q, PRUNE, LOGITS>;
     static int occ = 0;  // resident CTAs per SM
     if (!occ) {
         int b = 0;
@@ -1070,5 +1277,75 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
              "verify_greedy_argmax_kernel launch");
     TSV_CUDA(launch_pdl(verify_greedy_emit_kernel, dim3(static_cast<unsigned>((a->B + 7) / 8)), dim3(256), 0, st, P),
              "verify_greedy_emit_kernel launch");
+    return TSV_OK;
+}
+
+// Logits workspace: [verify workspace][partials (rows_p + rows_p) x n_chunks][lstats B]
+static size_t logits_extra_bytes(const tsv_verify_args* a, int32_t n_chunks) {
+    return align256(sizeof(LogitPartial) * 2 * static_cast<size_t>(a->rows_p) * static_cast<size_t>(n_chunks)) +
+           align256(sizeof(float4) * static_cast<size_t>(a->B));
+}
+
+extern "C" tsv_status tsv_verify_logits_workspace_size(const tsv_verify_args* a, size_t* bytes) {
+    TSV_REQUIRE(bytes != nullptr, "tsv_verify_logits_workspace_size: bytes is NULL");
+    TSV_TRY(validate(a));
+    const RaceParams P = make_params(a);
+    *bytes = align256(workspace_bytes(a)) + logits_extra_bytes(a, P.n_chunks);
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float temperature, void* stream) {
+    TSV_TRY(validate(a));
+    TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
+                "tsv_verify_accept_logits: vocab sharding is not supported");
+    TSV_REQUIRE(temperature > 0.0f && temperature < INFINITY, "tsv_verify_accept_logits: temperature %g must be > 0",
+                static_cast<double>(temperature));
+    TSV_TRY(check_device());
+    if (a->B == 0) return TSV_OK;
+    RaceParams P = make_params(a);
+    const size_t need = align256(workspace_bytes(a)) + logits_extra_bytes(a, P.n_chunks);
+    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= need,
+                "tsv_verify_accept_logits: workspace too small (%llu < %llu bytes)",
+                (unsigned long long)a->workspace_bytes, (unsigned long long)need);
+    char* ws = static_cast<char*>(a->workspace) + align256(workspace_bytes(a));
+    LogitPartial* part = reinterpret_cast<LogitPartial*>(ws);
+    ws += align256(sizeof(LogitPartial) * 2 * static_cast<size_t>(a->rows_p) * static_cast<size_t>(P.n_chunks));
+    float4* lstats = reinterpret_cast<float4*>(ws);
+    P.lstats = lstats;
+    P.inv_tau = static_cast<float>(1.0 / static_cast<double>(temperature));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t n_items = 2 * static_cast<int64_t>(a->rows_p) * P.n_chunks;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * 4));
+    TSV_CUDA(launch_pdl(verify_logit_stats_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, P, part,
+                        a->rows_p),
+             "verify_logit_stats_kernel launch");
+    const dim3 req_grid(static_cast<unsigned>((a->B + 7) / 8));
+    TSV_CUDA(launch_pdl(verify_logit_scan_kernel, req_grid, dim3(256), 0, st, P,
+                        static_cast<const LogitPartial*>(part), lstats),
+             "verify_logit_scan_kernel launch");
+    const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
+    tsv_status rs;
+    if (a->q) rs = prune ? launch_race<kLazy, true, true, true>(P, st) : launch_race<kLazy, true, false, true>(P, st);
+    else rs = prune ? launch_race<kLazy, false, true, true>(P, st) : launch_race<kLazy, false, false, true>(P, st);
+    TSV_TRY(rs);
+    const UpdateArgs none = {};
+    TSV_CUDA(prune ? launch_pdl(verify_emit_kernel<kLazy, true, false, true>, req_grid, dim3(256), 0, st, P, none)
+                   : launch_pdl(verify_emit_kernel<kLazy, false, false, true>, req_grid, dim3(256), 0, st, P, none),
+             "verify_emit_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_softmax_rows(const float* z, int64_t ld, int32_t vocab, int32_t rows, float temperature,
+                                       float* p_out, void* stream) {
+    TSV_REQUIRE(rows >= 0, "tsv_softmax_rows: rows < 0");
+    TSV_REQUIRE(vocab >= 1 && vocab <= ld, "tsv_softmax_rows: vocab %d outside [1, ld]", vocab);
+    TSV_REQUIRE(temperature > 0.0f && temperature < INFINITY, "tsv_softmax_rows: temperature must be > 0");
+    if (rows == 0) return TSV_OK;
+    TSV_REQUIRE(z && p_out, "tsv_softmax_rows: NULL argument");
+    TSV_TRY(check_device());
+    const float inv_tau = static_cast<float>(1.0 / static_cast<double>(temperature));
+    TSV_CUDA(launch_pdl(softmax_rows_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0,
+                        static_cast<cudaStream_t>(stream), z, ld, vocab, inv_tau, p_out),
+             "softmax_rows_kernel launch");
     return TSV_OK;
 }

@@ -39,7 +39,8 @@ EXPORTED = [
     "tsv_propose_lookup_choose_k", "tsv_verify_accept_update", "tsv_debug_race_E", "tsv_debug_philox",
     "tsv_goodput_partial", "tsv_goodput_finalize", "tsv_goodput_choose_k_sharded", "tsv_update_partial",
     "tsv_update_finalize", "tsv_update_acceptance_sharded", "tsv_verify_shard_flags", "tsv_verify_shard_race",
-    "tsv_verify_shard_emit", "tsv_verify_greedy",
+    "tsv_verify_shard_emit", "tsv_verify_greedy", "tsv_verify_logits_workspace_size",
+    "tsv_verify_accept_logits", "tsv_softmax_rows",
 ]
 
 
@@ -120,6 +121,9 @@ def _load() -> ctypes.CDLL:
         "tsv_verify_shard_race": ([ctypes.POINTER(VerifyArgs), P, P, P], ctypes.c_int),
         "tsv_verify_shard_emit": ([ctypes.POINTER(VerifyArgs), P, P, P], ctypes.c_int),
         "tsv_verify_greedy": ([ctypes.POINTER(VerifyArgs), P], ctypes.c_int),
+        "tsv_verify_logits_workspace_size": ([ctypes.POINTER(VerifyArgs), ctypes.POINTER(sz)], ctypes.c_int),
+        "tsv_verify_accept_logits": ([ctypes.POINTER(VerifyArgs), ctypes.c_float, P], ctypes.c_int),
+        "tsv_softmax_rows": ([P, i64, i32, i32, ctypes.c_float, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -288,6 +292,44 @@ def tsv_verify_greedy(p, row_offsets, draft_tokens, k_max, num_accepted=None, ou
         a.workspace_bytes = workspace.numel()
     _check(_lib.tsv_verify_greedy(ctypes.byref(a), _stream(stream)))
     return num_accepted, out_tokens
+
+
+def tsv_verify_logits_workspace_size(args: VerifyArgs) -> int:
+    n = ctypes.c_size_t(0)
+    _check(_lib.tsv_verify_logits_workspace_size(ctypes.byref(args), ctypes.byref(n)))
+    return int(n.value)
+
+
+def tsv_verify_accept_logits(zp, zq, row_offsets, draft_tokens, request_ids, seed, step, k_max,
+                             temperature=1.0, num_accepted=None, out_tokens=None, device_status=None,
+                             workspace=None, vocab=None, chunk=0, flags=0, stream=None):
+    """Fused softmax-from-logits verify (reading R23).  Returns (num_accepted, out_tokens)."""
+    B = row_offsets.numel() - 1
+    dev = zp.device
+    if num_accepted is None:
+        num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
+    if out_tokens is None:
+        out_tokens = torch.empty((B, k_max + 1), dtype=torch.int32, device=dev)
+    a = make_verify_args(zp, zq, row_offsets, draft_tokens, request_ids, seed, step, k_max,
+                         num_accepted, out_tokens, device_status, workspace, vocab=vocab, chunk=chunk, flags=flags)
+    if workspace is None and B > 0:
+        workspace = alloc_workspace(tsv_verify_logits_workspace_size(a), dev)
+        a.workspace = workspace.data_ptr()
+        a.workspace_bytes = workspace.numel()
+    _check(_lib.tsv_verify_accept_logits(ctypes.byref(a), float(temperature), _stream(stream)))
+    return num_accepted, out_tokens
+
+
+def tsv_softmax_rows(z, temperature=1.0, vocab=None, out=None, stream=None):
+    """Probabilities from logits rows (reading R23), fp32 [rows, ld]."""
+    _want(z, torch.float32, None, "z")
+    rows, ld = z.shape
+    V = ld if vocab is None else int(vocab)
+    if out is None:
+        out = torch.empty_like(z)
+    _check(_lib.tsv_softmax_rows(_ptr(z, rows_ok=True), int(z.stride(0)), V, rows, float(temperature), _ptr(out),
+                                 _stream(stream)))
+    return out
 
 
 def tsv_verify_shard_partial(args: VerifyArgs, tuples_out: torch.Tensor, stream=None):

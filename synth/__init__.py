@@ -116,6 +116,19 @@ def make_verify_batch(B: int, V: int, k_max: int, lam: float = 0.7, sigma: float
     return VerifyBatch(p_all, q, row_offsets, drafts, rids, k, V, k_max)
 
 
+def make_logits_batch(B: int, V: int, k_max: int, lam: float = 0.7, sigma: float = 3.0,
+                      seed: int = DEFAULT_SEED, device="cpu", dense_q: bool = True, ld: Optional[int] = None,
+                      k_list=None) -> VerifyBatch:
+    """The same batch as make_verify_batch with p and q given as LOGITS (NEXT 1): natural logs
+    of the probability rows (a valid logit vector of each row; padding columns stay 0)."""
+    vb = make_verify_batch(B, V, k_max, lam=lam, sigma=sigma, seed=seed, device=device, dense_q=dense_q, ld=ld,
+                           k_list=k_list)
+    vb.p[:, :V] = torch.log(vb.p[:, :V])
+    if vb.q is not None:
+        vb.q[:, :V] = torch.log(vb.q[:, :V])
+    return vb
+
+
 def make_contexts(B: int, L: int, V: int = 32000, seed: int = DEFAULT_SEED, ragged: bool = False,
                   zipf_a: float = 1.1, copy_prob: float = 0.3, copy_mean: float = 16.0):
     """PLD contexts: returns (ctx int32 [sum L_i], ctx_offsets int32 [B+1]) as numpy arrays."""

@@ -702,3 +702,106 @@ def test_greedy_bad_tokens(tsv):
     if len(d):
         d[0] = 500
     assert_greedy_parity(tsv, p, ro, d, 3)
+
+
+# ------------------------------------------------------- fused softmax from logits (NEXT 1)
+def test_softmax_rows_parity(tsv):
+    rng = np.random.Generator(np.random.PCG64(51))
+    for V, ld, tau, sigma in [(32000, 32000, 1.0, 3.0), (4099, 4100, 0.7, 2.0), (13, 16, 1.5, 8.0), (1, 4, 1.0, 1.0)]:
+        z = (rng.standard_normal((7, ld)) * sigma).astype(np.float32)
+        z[0, : min(V - 1, 5)] = -np.inf  # -inf logits: probability 0 (a row keeps one finite logit)
+        want = oracle.softmax_rows(z, tau, vocab=V)
+        got = _np(tsv.tsv_softmax_rows(torch.tensor(z, device=DEV), tau, vocab=V))
+        torch.cuda.synchronize()
+        big = want > 1e-30
+        rel = np.abs(got[big] - want[big]) / want[big]
+        assert rel.max() <= 1e-6, (V, tau, rel.max())
+        assert (got[~big] <= 1e-30).all() and (got[:, V:] == 0).all()
+
+
+def _race_scores(p_row, q_row, x_m, residual, seed, step, rid, m):
+    """Oracle-side scores RN32(w / E(u)) of one raced row (diagnostics for near-tie listing)."""
+    V = p_row.size
+    if residual:
+        w = (p_row - (q_row if q_row is not None else (np.arange(V) == x_m).astype(np.float32))).astype(np.float32)
+        w = np.where(w > 0, w, 0).astype(np.float32)
+    else:
+        w = np.where(p_row > 0, p_row, 0).astype(np.float32)
+    words = np.zeros(V, np.uint32)
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    for quad in range((V + 3) // 4):
+        out = oracle.philox4x32_10([quad, (1 << 16) | m, rid, step], key)
+        n = min(4, V - 4 * quad)
+        words[4 * quad:4 * quad + n] = out[:n]
+    E = _E_TABLE()[words & 0x7FFFFF]
+    return np.where(w > 0, (w / E).astype(np.float32), -1.0).astype(np.float32)
+
+
+_E_CACHE = []
+
+
+def _E_TABLE():
+    if not _E_CACHE:
+        _E_CACHE.append(oracle.E_table())
+    return _E_CACHE[0]
+
+
+def near_tie_flips(vb, p, q, ona, oout, gna, gout, seed, step, tol=2e-6):
+    """Requests whose GPU and oracle results differ, each classified: a flip is a near tie if
+    the deciding comparison (acceptance u q vs p, or the race's top two scores) is within tol."""
+    ro = _np(vb.row_offsets)
+    dt = _np(vb.draft_tokens)
+    rid = _np(vb.request_ids).view(np.uint32)
+    flips = []
+    for i in np.nonzero((ona != gna) | (oout != gout).any(1))[0]:
+        r0, k = int(ro[i]), int(ro[i + 1] - ro[i] - 1)
+        qb = r0 - int(i)
+        reason = None
+        m = int(min(ona[i], gna[i]))
+        for j in range(m + 1 if m < k else k):  # acceptance decisions up to the first disagreement
+            x = int(dt[qb + j])
+            word = oracle.philox4x32_10([0, j, int(rid[i]), step], [seed & 0xFFFFFFFF, seed >> 32])[0]
+            u = oracle.u_acc(int(word))
+            uq = np.float32(u) * np.float32(q[qb + j, x] if q is not None else 1.0)
+            if abs(float(uq) - float(p[r0 + j, x])) <= tol * max(float(p[r0 + j, x]), 1e-30):
+                reason = f"accept j={j}: u*q={float(uq):.9g} vs p={float(p[r0 + j, x]):.9g}"
+        if reason is None and ona[i] == gna[i]:
+            mm = int(ona[i])
+            sc = _race_scores(p[r0 + mm, :vb.vocab], None if (q is None or mm >= k) else q[qb + mm, :vb.vocab],
+                              int(dt[qb + mm]) if mm < k else -1, mm < k, seed, step, int(rid[i]), mm)
+            a, b = int(oout[i, mm]), int(gout[i, mm])
+            if a >= 0 and b >= 0 and abs(float(sc[a]) - float(sc[b])) <= tol * float(max(sc[a], sc[b])):
+                reason = f"race m={mm}: score[{a}]={float(sc[a]):.9g} vs score[{b}]={float(sc[b]):.9g}"
+        flips.append((int(i), reason))
+    return flips
+
+
+@pytest.mark.parametrize("B,V,k_max,tau,dense_q", [(4, 32000, 4, 1.0, True), (128, 32000, 8, 1.0, True),
+                                                   (64, 4099, 6, 0.8, True), (48, 32000, 5, 1.3, False)])
+def test_verify_logits_parity(tsv, B, V, k_max, tau, dense_q):
+    vb = synth.make_logits_batch(B=B, V=V, k_max=k_max, lam=0.7, seed=60 + B, dense_q=dense_q)
+    seed, step = 240614066, 3
+    zp, zq = _np(vb.p), _np(vb.q)
+    p = oracle.softmax_rows(zp, tau, vocab=V)
+    q = None if zq is None else oracle.softmax_rows(zq, tau, vocab=V)
+    ona, oout, ost = oracle.verify(p, q, _np(vb.row_offsets), _np(vb.draft_tokens),
+                                   _np(vb.request_ids).view(np.uint32), seed, step, k_max, vocab=V)
+    g = vb.to(DEV)
+    gna, gout = tsv.tsv_verify_accept_logits(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, seed, step,
+                                             k_max, temperature=tau, vocab=V)
+    torch.cuda.synchronize()
+    gna, gout = _np(gna), _np(gout)
+    flips = near_tie_flips(vb, p, q, ona, oout, gna, gout, seed, step)
+    for f in flips:  # every flip is listed; each must be a near tie
+        print("near-tie flip:", f)
+    assert all(reason is not None for _, reason in flips), flips
+    assert len(flips) <= max(1, B // 64)
+
+
+def test_verify_logits_prune_off_identical(tsv):
+    vb = synth.make_logits_batch(B=32, V=4096, k_max=5, lam=0.6, seed=70).to(DEV)
+    a = tsv.tsv_verify_accept_logits(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 9, 1, 5)
+    b = tsv.tsv_verify_accept_logits(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 9, 1, 5,
+                                     flags=tsv.VERIFY_NO_PRUNE)
+    torch.cuda.synchronize()
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
