@@ -797,16 +797,24 @@ struct LogitPartial {
     double s;
 };
 
-__device__ __forceinline__ void online_push(float z, float inv_tau, float& m, double& s) {
-    if (z > m) {  // new running max: rescale the sum (also the first finite value: s = 0)
-        s = s * exp(static_cast<double>(__fmul_rn(__fsub_rn(m, z), inv_tau))) + 1.0;
-        m = z;
-    } else {
-        s += static_cast<double>(expf(__fmul_rn(__fsub_rn(z, m), inv_tau)));
-    }
+__device__ __forceinline__ uint32_t ordered_bits(float f) {  // monotone float -> uint (no NaN)
+    const uint32_t u = __float_as_uint(f);
+    return (u >> 31) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float from_ordered_bits(uint32_t k) {
+    return __uint_as_float((k >> 31) ? (k & 0x7FFFFFFFu) : ~k);
+}
+__device__ __forceinline__ float exp_arg(float z, float m, float inv_tau) {
+    return __fmul_rn(__fsub_rn(z, m), inv_tau);
 }
 
-__global__ void __launch_bounds__(256, 4) verify_logit_stats_kernel(const RaceParams P, LogitPartial* part,
+// Pass 1: per (row, chunk) item, a warp-uniform running max m (raised at most once per step
+// for all lanes -- no divergent rescaling) and per-lane sums of expf((z - m) / tau): four
+// exponentials added in fp32, then accumulated in binary64.  Stored as (m, sum).
+#ifndef TSV_STATS_MINB
+#define TSV_STATS_MINB 6
+#endif
+__global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel(const RaceParams P, LogitPartial* part,
                                                                     int32_t rows_q_max) {
     pdl_wait();
     pdl_launch_dependents();
@@ -816,6 +824,7 @@ __global__ void __launch_bounds__(256, 4) verify_logit_stats_kernel(const RacePa
     const int32_t rp = P.row_offsets[P.B];  // p rows in use; q rows: rp - B
     const int32_t rq = (P.q != nullptr) ? rp - P.B : 0;
     const int64_t n_items = static_cast<int64_t>(rp + rq) * P.n_chunks;
+    const float it = P.inv_tau;
     for (int64_t item = warp_id; item < n_items; item += n_warps) {
         const int32_t r = static_cast<int32_t>(item % (rp + rq));
         const int32_t c = static_cast<int32_t>(item / (rp + rq));
@@ -827,26 +836,54 @@ __global__ void __launch_bounds__(256, 4) verify_logit_stats_kernel(const RacePa
         const int32_t nq = (col_end - col_begin + 3) >> 2;
         float m = -INFINITY;
         double s = 0.0;
-        for (int32_t f = lane; f < nq; f += 32) {
-            const float4 z = ldg_stream(z4 + f);
-            const int32_t v = col_begin + 4 * f;
-            const float e[4] = {z.x, z.y, z.z, z.w};
+        auto load2 = [&](int32_t f0, float4 (&z)[2]) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (v + t < col_end && e[t] > -INFINITY) online_push(e[t], P.inv_tau, m, s);
+            for (int h = 0; h < 2; ++h) {
+                const int32_t f = f0 + 32 * h + lane;
+                z[h] = f < nq ? ldg_stream(z4 + f) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            }
+        };
+        float4 cur[2];
+        load2(0, cur);
+        for (int32_t f0 = 0; f0 < nq; f0 += 64) {  // two float4 per lane; the next two in flight
+            float4 nxt[2];
+            if (f0 + 64 < nq) load2(f0 + 64, nxt);
+            float e[8];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int32_t v = col_begin + 4 * (f0 + 32 * h + lane);
+                e[4 * h + 0] = cur[h].x;
+                e[4 * h + 1] = v + 1 < col_end ? cur[h].y : -INFINITY;
+                e[4 * h + 2] = v + 2 < col_end ? cur[h].z : -INFINITY;
+                e[4 * h + 3] = v + 3 < col_end ? cur[h].w : -INFINITY;
+            }
+            float lm = e[0];
+#pragma unroll
+            for (int t = 1; t < 8; ++t) lm = fmaxf(lm, e[t]);
+            const float wm = from_ordered_bits(__reduce_max_sync(0xFFFFFFFFu, ordered_bits(lm)));
+            if (wm > m) {  // warp-uniform
+                if (m > -INFINITY) s *= static_cast<double>(expf(exp_arg(m, wm, it)));
+                m = wm;
+            }
+            float acc = 0.0f;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float x[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) x[t] = e[4 * h + t] > -INFINITY ? expf(exp_arg(e[4 * h + t], m, it)) : 0.0f;
+                acc = __fadd_rn(acc, __fadd_rn(__fadd_rn(x[0], x[1]), __fadd_rn(x[2], x[3])));
+            }
+            s += static_cast<double>(acc);
+            cur[0] = nxt[0];
+            cur[1] = nxt[1];
         }
-        // warp combine: M = max m, S = sum s exp((m - M)/tau)
-        float M = m;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xFFFFFFFFu, M, o));
-        double sc = (m > -INFINITY) ? s * exp(static_cast<double>(__fmul_rn(__fsub_rn(m, M), P.inv_tau))) : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xFFFFFFFFu, sc, o);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
         if (lane == 0) {
             const int64_t slot = (isq ? static_cast<int64_t>(P.rows_p) + (r - rp) : r) * P.n_chunks + c;
-            part[slot].m = M;
+            part[slot].m = m;
             part[slot].pad = 0.f;
-            part[slot].s = sc;
+            part[slot].s = s;
         }
     }
     (void)rows_q_max;
@@ -859,7 +896,7 @@ __device__ __forceinline__ float2 logit_row_stats(const RaceParams& P, const Log
     double S = 0.0;
     for (int32_t c = 0; c < P.n_chunks; ++c) {
         const LogitPartial pc = part[slot0 + c];
-        if (pc.m > -INFINITY) S += pc.s * exp(static_cast<double>(__fmul_rn(__fsub_rn(pc.m, M), P.inv_tau)));
+        if (pc.m > -INFINITY) S += pc.s * static_cast<double>(expf(exp_arg(pc.m, M, P.inv_tau)));
     }
     return make_float2(M, __double2float_rn(1.0 / S));
 }
@@ -1315,7 +1352,7 @@ extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float t
     P.inv_tau = static_cast<float>(1.0 / static_cast<double>(temperature));
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t n_items = 2 * static_cast<int64_t>(a->rows_p) * P.n_chunks;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * 4));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * TSV_STATS_MINB));
     TSV_CUDA(launch_pdl(verify_logit_stats_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, P, part,
                         a->rows_p),
              "verify_logit_stats_kernel launch");
