@@ -74,6 +74,8 @@ def _load():
         lib.oracle_verify_greedy.restype = i32
         lib.oracle_softmax_rows.argtypes = [P, i64, i32, i32, ctypes.c_float, P]
         lib.oracle_softmax_rows.restype = None
+        lib.oracle_fit_latency.argtypes = [P, P, P, i32, P, P]
+        lib.oracle_fit_latency.restype = i32
         lib.oracle_lookup.argtypes = [P, P, i32, i32, i32, i32, P, P]
         lib.oracle_lookup.restype = None
         lib.oracle_expected_len.argtypes = [f64, i32]
@@ -188,6 +190,23 @@ def verify_logits(zp, zq, row_offsets, draft_tokens, request_ids, seed, step, k_
     p = softmax_rows(zp, temperature, vocab)
     q = None if zq is None else softmax_rows(zq, temperature, vocab)
     return verify(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max, vocab=vocab)
+
+
+def fit_latency(ctx_tokens, batched_tokens, ms):
+    """Reading R25: OLS of ms on (ctx, batched, 1) with clamp-and-refit of negative coefficients.
+    Returns ((ctx_ms_per_tok, batched_ms_per_tok, fixed_ms), r2); raises ValueError on error."""
+    lib = _load()
+    c = _c(ctx_tokens, np.float64)
+    b = _c(batched_tokens, np.float64)
+    t = _c(ms, np.float64)
+    out = np.zeros(3, np.float64)
+    r2 = np.zeros(1, np.float64)
+    st = lib.oracle_fit_latency(_ptr(c), _ptr(b), _ptr(t), int(t.size), _ptr(out), _ptr(r2))
+    if st == 1:
+        raise ValueError("TooFewSamples")
+    if st == 2:
+        raise ValueError("DegenerateDesign")
+    return tuple(float(x) for x in out), float(r2[0])
 
 
 def lookup(ctx, ctx_offsets, n_min, n_max, K):

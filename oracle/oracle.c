@@ -328,6 +328,106 @@ void oracle_softmax_rows(const float* z, int64_t ld, int32_t V, int32_t rows, fl
     }
 }
 
+/* Latency-model fit ("fits a linear regression model", Eq. forward-time
+ * T = a N_context + gamma N_batched + delta; reading R25 = SPEC.md:44-52): ordinary least
+ * squares on the columns (context, batched, 1); while a free coefficient is negative, clamp
+ * every negative one to 0 and refit the remaining free ones.  R^2 = 1 - SS_res / SS_tot of the
+ * final fit (1 when SS_tot = 0 and the fit is exact).  Returns 0, 1 (n < 3) or 2 (the full
+ * design is rank-deficient).  Written out: normal equations, Gaussian elimination with
+ * partial pivoting, in double. */
+static int solve_normal(const double* X[3], const double* y, int32_t n, const int free_[3], double beta[3])
+{
+    double A[3][4];
+    int idx[3], m = 0, i, j, c, r;
+    for (i = 0; i < 3; ++i)
+        if (free_[i]) idx[m++] = i;
+    for (i = 0; i < m; ++i) {
+        for (j = 0; j < m; ++j) {
+            double s = 0.0;
+            for (r = 0; r < n; ++r) s += X[idx[i]][r] * X[idx[j]][r];
+            A[i][j] = s;
+        }
+        {
+            double s = 0.0;
+            for (r = 0; r < n; ++r) s += X[idx[i]][r] * y[r];
+            A[i][m] = s;
+        }
+    }
+    for (c = 0; c < m; ++c) {
+        int piv = c;
+        double scale = 0.0;
+        for (r = 0; r < m; ++r)
+            for (j = 0; j < m; ++j) scale = fabs(A[r][j]) > scale ? fabs(A[r][j]) : scale;
+        for (r = c + 1; r < m; ++r)
+            if (fabs(A[r][c]) > fabs(A[piv][c])) piv = r;
+        if (!(fabs(A[piv][c]) > 1e-12 * scale)) return 2;
+        if (piv != c)
+            for (j = 0; j <= m; ++j) {
+                double t = A[c][j];
+                A[c][j] = A[piv][j];
+                A[piv][j] = t;
+            }
+        for (r = c + 1; r < m; ++r) {
+            double f = A[r][c] / A[c][c];
+            for (j = c; j <= m; ++j) A[r][j] -= f * A[c][j];
+        }
+    }
+    for (i = 0; i < 3; ++i) beta[i] = 0.0;
+    for (c = m - 1; c >= 0; --c) {
+        double s = A[c][m];
+        for (j = c + 1; j < m; ++j) s -= A[c][j] * beta[idx[j]];
+        beta[idx[c]] = s / A[c][c];
+    }
+    return 0;
+}
+
+int32_t oracle_fit_latency(const double* ctx_tokens, const double* batched_tokens, const double* ms, int32_t n,
+                           double out[3], double* r2)
+{
+    double* ones;
+    const double* X[3];
+    int free_[3] = {1, 1, 1}, i, any_neg, st;
+    double beta[3], mean = 0.0, ss_tot = 0.0, ss_res = 0.0;
+    int32_t r;
+    if (n < 3) return 1;
+    ones = (double*)malloc(sizeof(double) * (size_t)n);
+    for (r = 0; r < n; ++r) ones[r] = 1.0;
+    X[0] = ctx_tokens;
+    X[1] = batched_tokens;
+    X[2] = ones;
+    st = solve_normal(X, ms, n, free_, beta);
+    if (st) {
+        free(ones);
+        return 2;
+    }
+    do {
+        any_neg = 0;
+        for (i = 0; i < 3; ++i)
+            if (free_[i] && beta[i] < 0.0) {
+                free_[i] = 0;
+                any_neg = 1;
+            }
+        if (any_neg) {
+            if (!free_[0] && !free_[1] && !free_[2]) {
+                beta[0] = beta[1] = beta[2] = 0.0;
+                break;
+            }
+            solve_normal(X, ms, n, free_, beta);
+        }
+    } while (any_neg);
+    for (r = 0; r < n; ++r) mean += ms[r];
+    mean /= (double)n;
+    for (r = 0; r < n; ++r) {
+        double pred = beta[0] * ctx_tokens[r] + beta[1] * batched_tokens[r] + beta[2];
+        ss_res += (ms[r] - pred) * (ms[r] - pred);
+        ss_tot += (ms[r] - mean) * (ms[r] - mean);
+    }
+    *r2 = ss_tot > 0.0 ? 1.0 - ss_res / ss_tot : (ss_res == 0.0 ? 1.0 : 0.0);
+    for (i = 0; i < 3; ++i) out[i] = beta[i];
+    free(ones);
+    return 0;
+}
+
 /* ------------------------------------------------------------------------ */
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,

@@ -35,6 +35,9 @@ int32_t oracle_verify_greedy(const float* p, int64_t ld, int32_t V, const int32_
 void oracle_softmax_rows(const float* z, int64_t ld, int32_t V, int32_t rows, float temperature,
                          float* p_out);
 
+int32_t oracle_fit_latency(const double* ctx_tokens, const double* batched_tokens, const double* ms, int32_t n,
+                           double out[3], double* r2);
+
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,
                    int32_t* proposals, int32_t* proposal_len);
