@@ -306,6 +306,16 @@ TSV_API tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, con
 TSV_API tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                     double decay, int32_t estimator, void* stream);
 
+/* Latency-model fit (reading R25; "fits a linear regression
+ * model"): ordinary least squares of ms[i] on (ctx_tokens[i],
+ * batched_tokens[i], 1) over n >= 3 HOST samples; while a coefficient is negative,
+ * clamp every negative one to 0 and refit the remaining ones.  Writes the model
+ * and (nullable) R^2 of the final fit.  Host-only (no device work).  Errors:
+ * TSV_ERR_INVALID_ARG for n < 3 (TooFewSamples) or collinear regressors
+ * (DegenerateDesign). */
+TSV_API tsv_status tsv_fit_latency_model(const double* ctx_tokens, const double* batched_tokens, const double* ms,
+                                         int32_t n, tsv_latency_model* out, double* r2_out);
+
 /* --------------------------------------------------------------------------
  * Communicator for the multi-GPU modes (NCCL over NVLink 5 / NVSwitch,
  * resolved at run time from the process's libnccl.so.2).

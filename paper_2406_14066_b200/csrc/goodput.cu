@@ -11,6 +11,10 @@
 // request's l is quantised once to 2^-32 fixed point (rint) and summed in int64,
 // so the batch sums are exact and independent of reduction order, block shape or
 // the number of ranks that contribute partial sums.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "goodput.cuh"
 
 namespace tsv {
@@ -225,5 +229,104 @@ extern "C" tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, 
     A.estimator = estimator;
     TSV_CUDA(launch_pdl(update_acceptance_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream), A),
              "update_acceptance_kernel launch");
+    return TSV_OK;
+}
+
+// ---------------------------------------------------------------- latency-model fit (host)
+// Reading R25: OLS of the measured forward time on
+// (N_context, N_batched, 1), clamp-and-refit of negative coefficients, R^2.  Host code (a
+// profiling-time fit of a handful of samples); least squares by Householder QR of the
+// column-scaled design, so no normal equations are formed.
+namespace {
+// min ||X b - y|| over the columns in `cols` (X column-major n x 3); false if rank-deficient.
+bool qr_lstsq(const std::vector<double>& X, const std::vector<double>& y, int n, const int* cols, int m,
+              double beta[3]) {
+    std::vector<double> A(static_cast<size_t>(n) * m), r(y);
+    double scale[3];
+    for (int j = 0; j < m; ++j) {
+        double nrm = 0.0;
+        for (int i = 0; i < n; ++i) nrm = std::max(nrm, std::fabs(X[static_cast<size_t>(cols[j]) * n + i]));
+        scale[j] = nrm > 0.0 ? nrm : 1.0;
+        for (int i = 0; i < n; ++i) A[static_cast<size_t>(j) * n + i] = X[static_cast<size_t>(cols[j]) * n + i] / scale[j];
+    }
+    double R[3][3] = {};
+    for (int j = 0; j < m; ++j) {
+        double* a = &A[static_cast<size_t>(j) * n];
+        double nrm = 0.0;
+        for (int i = j; i < n; ++i) nrm += a[i] * a[i];
+        nrm = std::sqrt(nrm);
+        if (!(nrm > 1e-10 * std::sqrt(static_cast<double>(n)))) return false;  // dependent column
+        const double alpha = a[j] > 0 ? -nrm : nrm;
+        std::vector<double> v(a + j, a + n);
+        v[0] -= alpha;
+        double vv = 0.0;
+        for (double t : v) vv += t * t;
+        auto reflect = [&](double* col) {
+            double d = 0.0;
+            for (int i = j; i < n; ++i) d += v[i - j] * col[i];
+            const double f = 2.0 * d / vv;
+            for (int i = j; i < n; ++i) col[i] -= f * v[i - j];
+        };
+        if (vv > 0.0) {
+            for (int k = j; k < m; ++k) reflect(&A[static_cast<size_t>(k) * n]);
+            reflect(r.data());
+        }
+        for (int k = j; k < m; ++k) R[j][k] = A[static_cast<size_t>(k) * n + j];
+    }
+    double z[3] = {};
+    for (int j = m - 1; j >= 0; --j) {
+        double t = r[j];
+        for (int k = j + 1; k < m; ++k) t -= R[j][k] * z[k];
+        z[j] = t / R[j][j];
+    }
+    for (int i = 0; i < 3; ++i) beta[i] = 0.0;
+    for (int j = 0; j < m; ++j) beta[cols[j]] = z[j] / scale[j];
+    return true;
+}
+}  // namespace
+
+extern "C" tsv_status tsv_fit_latency_model(const double* ctx_tokens, const double* batched_tokens,
+                                            const double* ms, int32_t n, tsv_latency_model* out, double* r2_out) {
+    TSV_REQUIRE(n >= 3, "tsv_fit_latency_model: TooFewSamples (n = %d < 3)", n);
+    TSV_REQUIRE(ctx_tokens && batched_tokens && ms && out, "tsv_fit_latency_model: NULL argument");
+    std::vector<double> X(3 * static_cast<size_t>(n)), y(ms, ms + n);
+    for (int32_t i = 0; i < n; ++i) {
+        X[i] = ctx_tokens[i];
+        X[static_cast<size_t>(n) + i] = batched_tokens[i];
+        X[2 * static_cast<size_t>(n) + i] = 1.0;
+    }
+    double beta[3];
+    int cols[3] = {0, 1, 2};
+    TSV_REQUIRE(qr_lstsq(X, y, n, cols, 3, beta), "tsv_fit_latency_model: DegenerateDesign (collinear regressors)");
+    bool free_[3] = {true, true, true};
+    for (;;) {  // clamp every negative free coefficient, refit the rest
+        bool neg = false;
+        for (int i = 0; i < 3; ++i)
+            if (free_[i] && beta[i] < 0.0) {
+                free_[i] = false;
+                neg = true;
+            }
+        if (!neg) break;
+        int m = 0;
+        for (int i = 0; i < 3; ++i)
+            if (free_[i]) cols[m++] = i;
+        if (m == 0) {
+            beta[0] = beta[1] = beta[2] = 0.0;
+            break;
+        }
+        if (!qr_lstsq(X, y, n, cols, m, beta)) break;
+    }
+    double mean = 0.0, ss_res = 0.0, ss_tot = 0.0;
+    for (int32_t i = 0; i < n; ++i) mean += ms[i];
+    mean /= n;
+    for (int32_t i = 0; i < n; ++i) {
+        const double pred = beta[0] * ctx_tokens[i] + beta[1] * batched_tokens[i] + beta[2];
+        ss_res += (ms[i] - pred) * (ms[i] - pred);
+        ss_tot += (ms[i] - mean) * (ms[i] - mean);
+    }
+    out->ctx_ms_per_tok = beta[0];
+    out->batched_ms_per_tok = beta[1];
+    out->fixed_ms = beta[2];
+    if (r2_out) *r2_out = ss_tot > 0.0 ? 1.0 - ss_res / ss_tot : (ss_res == 0.0 ? 1.0 : 0.0);
     return TSV_OK;
 }

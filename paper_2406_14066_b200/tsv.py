@@ -11,6 +11,7 @@ import ctypes
 import os
 from typing import Optional
 
+import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -40,7 +41,7 @@ EXPORTED = [
     "tsv_goodput_partial", "tsv_goodput_finalize", "tsv_goodput_choose_k_sharded", "tsv_update_partial",
     "tsv_update_finalize", "tsv_update_acceptance_sharded", "tsv_verify_shard_flags", "tsv_verify_shard_race",
     "tsv_verify_shard_emit", "tsv_verify_greedy", "tsv_verify_logits_workspace_size",
-    "tsv_verify_accept_logits", "tsv_softmax_rows",
+    "tsv_verify_accept_logits", "tsv_softmax_rows", "tsv_fit_latency_model",
 ]
 
 
@@ -124,6 +125,7 @@ def _load() -> ctypes.CDLL:
         "tsv_verify_logits_workspace_size": ([ctypes.POINTER(VerifyArgs), ctypes.POINTER(sz)], ctypes.c_int),
         "tsv_verify_accept_logits": ([ctypes.POINTER(VerifyArgs), ctypes.c_float, P], ctypes.c_int),
         "tsv_softmax_rows": ([P, i64, i32, i32, ctypes.c_float, P, P], ctypes.c_int),
+        "tsv_fit_latency_model": ([P, P, P, i32, ctypes.POINTER(LatencyModel), P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -478,6 +480,18 @@ def tsv_update_finalize(alpha, sums, decay=0.9, stream=None):
     _want(sums, torch.int64, 2, "sums")
     _check(_lib.tsv_update_finalize(_ptr(alpha), _ptr(sums), float(decay), _stream(stream)))
     return alpha
+
+
+def tsv_fit_latency_model(ctx_tokens, batched_tokens, ms):
+    """Host-side OLS latency fit (reading R25).  Returns ((ctx, batched, fixed) ms coefficients, R^2)."""
+    c = np.ascontiguousarray(ctx_tokens, np.float64)
+    b = np.ascontiguousarray(batched_tokens, np.float64)
+    t = np.ascontiguousarray(ms, np.float64)
+    out = LatencyModel()
+    r2 = ctypes.c_double(0.0)
+    _check(_lib.tsv_fit_latency_model(c.ctypes.data, b.ctypes.data, t.ctypes.data, int(t.size), ctypes.byref(out),
+                                      ctypes.byref(r2)))
+    return (out.ctx_ms_per_tok, out.batched_ms_per_tok, out.fixed_ms), float(r2.value)
 
 
 # ----------------------------------------------------------------------------- comm
