@@ -76,6 +76,10 @@ def _load():
         lib.oracle_softmax_rows.restype = None
         lib.oracle_fit_latency.argtypes = [P, P, P, i32, P, P]
         lib.oracle_fit_latency.restype = i32
+        lib.oracle_sim_target.argtypes = [P, i32, P, i32, ctypes.c_float, i32, i64, P, P, P]
+        lib.oracle_sim_target.restype = None
+        lib.oracle_context_append.argtypes = [P, i32, i32, P, P, i32, P, P]
+        lib.oracle_context_append.restype = None
         lib.oracle_lookup.argtypes = [P, P, i32, i32, i32, i32, P, P]
         lib.oracle_lookup.restype = None
         lib.oracle_expected_len.argtypes = [f64, i32]
@@ -207,6 +211,34 @@ def fit_latency(ctx_tokens, batched_tokens, ms):
     if st == 2:
         raise ValueError("DegenerateDesign")
     return tuple(float(x) for x in out), float(r2[0])
+
+
+def sim_target(proposals, k_req, alpha_true, V, ld=None):
+    """Closed-loop synthetic target (reading R26): returns (p [R, ld], row_offsets [B+1], drafts [R-B])."""
+    lib = _load()
+    pr = _c(proposals, np.int32)
+    B, K = pr.shape
+    kr = _c(k_req, np.int32)
+    ld = V if ld is None else ld
+    R = int((kr + 1).sum())
+    p = np.zeros((max(R, 1), ld), np.float32)
+    ro = np.zeros(B + 1, np.int32)
+    d = np.zeros(max(R - B, 1), np.int32)
+    lib.oracle_sim_target(_ptr(pr), K, _ptr(kr), B, float(alpha_true), int(V), ld, _ptr(p), _ptr(ro), _ptr(d))
+    return p[:R], ro, d[:R - B]
+
+
+def context_append(ctx, L, out_tokens, num_accepted, ctx_len):
+    """Window append (reading R26): returns (new ctx [B*L], new ctx_len [B])."""
+    lib = _load()
+    c = _c(ctx, np.int32)
+    ot = _c(out_tokens, np.int32)
+    na = _c(num_accepted, np.int32)
+    B = na.size
+    out = np.zeros_like(c)
+    cl = np.array(ctx_len, np.int32).copy()
+    lib.oracle_context_append(_ptr(c), int(L), B, _ptr(ot), _ptr(na), int(ot.shape[1] - 1), _ptr(out), _ptr(cl))
+    return out, cl
 
 
 def lookup(ctx, ctx_offsets, n_min, n_max, K):

@@ -428,6 +428,57 @@ int32_t oracle_fit_latency(const double* ctx_tokens, const double* batched_token
     return 0;
 }
 
+/* Closed-loop harness (reading R26): the synthetic target model that
+ * stands in for the LLM forward in a multi-step on-device loop, and the context append.
+ * Not from the paper (which runs real models); a world in which every draft token is kept by
+ * rejection sampling with probability exactly alpha_true:
+ *   request i verifies k_i = k_req[i] drafts x_j = proposals[i][j] (j < k_i);
+ *   row_offsets = exclusive scan of (k_i + 1); drafts packed at row_offsets[i] - i;
+ *   row j < k_i:  p[x_j] = alpha_true, every other token (1 - alpha_true) / (V - 1) (V > 1);
+ *   row k_i (bonus): uniform 1 / V.
+ * With one-hot drafts (q = NULL) the acceptance test is u < p[x_j] = alpha_true. */
+void oracle_sim_target(const int32_t* proposals, int32_t K, const int32_t* k_req, int32_t B, float alpha_true,
+                       int32_t V, int64_t ld, float* p_out, int32_t* row_offsets, int32_t* drafts)
+{
+    int32_t i, j, v, r = 0;
+    const float rest = V > 1 ? (float)((1.0 - (double)alpha_true) / (double)(V - 1)) : 0.0f;
+    const float unif = (float)(1.0 / (double)V);
+    for (i = 0; i < B; ++i) {
+        int32_t k = k_req[i];
+        row_offsets[i] = r;
+        for (j = 0; j <= k; ++j, ++r) {
+            float* row = p_out + (int64_t)r * ld;
+            if (j < k) {
+                int32_t x = proposals[(int64_t)i * K + j];
+                drafts[r - i] = x;
+                for (v = 0; v < V; ++v) row[v] = rest;
+                row[x] = alpha_true;
+            } else {
+                for (v = 0; v < V; ++v) row[v] = unif;
+            }
+        }
+    }
+    row_offsets[B] = r;
+}
+
+/* Context window of L tokens per request (request i at [i L, (i+1) L)): the m_i + 1 emitted
+ * tokens are appended and as many of the oldest dropped; ctx_len[i] (the context length the
+ * latency model sees) grows by m_i + 1.  A request with m_i < 0 (flagged) is unchanged. */
+void oracle_context_append(const int32_t* ctx_in, int32_t L, int32_t B, const int32_t* out_tokens,
+                           const int32_t* num_accepted, int32_t k_max, int32_t* ctx_out, int32_t* ctx_len)
+{
+    int32_t i, t;
+    for (i = 0; i < B; ++i) {
+        int32_t e = num_accepted[i] >= 0 ? num_accepted[i] + 1 : 0;
+        const int32_t* in = ctx_in + (int64_t)i * L;
+        int32_t* out = ctx_out + (int64_t)i * L;
+        if (e > L) e = L;
+        for (t = 0; t < L - e; ++t) out[t] = in[t + e];
+        for (t = 0; t < e; ++t) out[L - e + t] = out_tokens[(int64_t)i * (k_max + 1) + (num_accepted[i] + 1 - e) + t];
+        ctx_len[i] += num_accepted[i] >= 0 ? num_accepted[i] + 1 : 0;
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,

@@ -38,6 +38,11 @@ void oracle_softmax_rows(const float* z, int64_t ld, int32_t V, int32_t rows, fl
 int32_t oracle_fit_latency(const double* ctx_tokens, const double* batched_tokens, const double* ms, int32_t n,
                            double out[3], double* r2);
 
+void oracle_sim_target(const int32_t* proposals, int32_t K, const int32_t* k_req, int32_t B, float alpha_true,
+                       int32_t V, int64_t ld, float* p_out, int32_t* row_offsets, int32_t* drafts);
+void oracle_context_append(const int32_t* ctx_in, int32_t L, int32_t B, const int32_t* out_tokens,
+                           const int32_t* num_accepted, int32_t k_max, int32_t* ctx_out, int32_t* ctx_len);
+
 void oracle_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                    int32_t n_min, int32_t n_max, int32_t K,
                    int32_t* proposals, int32_t* proposal_len);
