@@ -317,6 +317,30 @@ TSV_API tsv_status tsv_fit_latency_model(const double* ctx_tokens, const double*
                                          int32_t n, tsv_latency_model* out, double* r2_out);
 
 /* --------------------------------------------------------------------------
+ * Closed-loop harness (reading R26): a synthetic target
+ * and the context append close the decode loop on the device -- lookup ->
+ * choose-k -> tsv_sim_target -> verify (+ alpha update) -> tsv_context_append --
+ * so the controller's adaptation can be replayed for many steps
+ * as one CUDA graph without model weights.  All pointers are device pointers.
+ * tsv_sim_target: request i verifies k_req[i] drafts proposals[i*K + j]; writes
+ *   row_offsets [B+1] (exclusive scan of k_req + 1), drafts (packed at
+ *   row_offsets[i] - i), row_info [rows_cap] scratch, and p_out rows [rows_cap, ld]:
+ *   draft row j puts *alpha_true on x_j and (1 - *alpha_true)/(V - 1) elsewhere,
+ *   the bonus row is uniform 1/V; columns >= V are 0.  rows_cap >= B (K + 1).
+ *   With q = NULL in the verify, each draft is kept with probability *alpha_true.
+ * tsv_context_append: windows of L tokens (request i at [iL, (i+1)L)); appends the
+ *   num_accepted[i] + 1 emitted tokens (out_tokens [B, k_max+1]) and drops the
+ *   oldest, writing ctx_out (must not alias ctx_in); ctx_len[i] += num_accepted[i]+1
+ *   (unchanged for flagged requests, num_accepted < 0).
+ * ------------------------------------------------------------------------ */
+TSV_API tsv_status tsv_sim_target(const int32_t* proposals, int32_t K, const int32_t* k_req, int32_t B,
+                                  const float* alpha_true, int32_t V, int64_t ld, int32_t rows_cap, float* p_out,
+                                  int32_t* row_offsets, int32_t* drafts, int32_t* row_info, void* stream);
+TSV_API tsv_status tsv_context_append(const int32_t* ctx_in, int32_t L, int32_t B, const int32_t* out_tokens,
+                                      const int32_t* num_accepted, int32_t k_max, int32_t* ctx_out, int32_t* ctx_len,
+                                      void* stream);
+
+/* --------------------------------------------------------------------------
  * Communicator for the multi-GPU modes (NCCL over NVLink 5 / NVSwitch,
  * resolved at run time from the process's libnccl.so.2).
  * tsv_comm_get_unique_id: rank 0 only; the 128 bytes are broadcast by the

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(OUT_DIR, "libtsv.so")
-SOURCES = ["api.cu", "verify.cu", "lookup.cu", "goodput.cu"]
+SOURCES = ["api.cu", "verify.cu", "lookup.cu", "goodput.cu", "loop.cu"]
 HEADERS = ["common.cuh", "goodput.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -41,7 +41,8 @@ EXPORTED = [
     "tsv_goodput_partial", "tsv_goodput_finalize", "tsv_goodput_choose_k_sharded", "tsv_update_partial",
     "tsv_update_finalize", "tsv_update_acceptance_sharded", "tsv_verify_shard_flags", "tsv_verify_shard_race",
     "tsv_verify_shard_emit", "tsv_verify_greedy", "tsv_verify_logits_workspace_size",
-    "tsv_verify_accept_logits", "tsv_softmax_rows", "tsv_fit_latency_model",
+    "tsv_verify_accept_logits", "tsv_softmax_rows", "tsv_fit_latency_model", "tsv_sim_target",
+    "tsv_context_append",
 ]
 
 
@@ -126,6 +127,8 @@ def _load() -> ctypes.CDLL:
         "tsv_verify_accept_logits": ([ctypes.POINTER(VerifyArgs), ctypes.c_float, P], ctypes.c_int),
         "tsv_softmax_rows": ([P, i64, i32, i32, ctypes.c_float, P, P], ctypes.c_int),
         "tsv_fit_latency_model": ([P, P, P, i32, ctypes.POINTER(LatencyModel), P], ctypes.c_int),
+        "tsv_sim_target": ([P, i32, P, i32, P, i32, i64, i32, P, P, P, P, P], ctypes.c_int),
+        "tsv_context_append": ([P, i32, i32, P, P, i32, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
