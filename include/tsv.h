@@ -267,11 +267,15 @@ TSV_API tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_per_r
  * Fused Propose + GetVerificationLen for the PLD method (Listing 1 lines 15-16 +
  * 22-23): tsv_propose_lookup followed by tsv_goodput_choose_k
  * with policy TSV_POLICY_PLD, cap = the proposal lengths just found and
- * k_max = k_fixed, in ONE kernel (the CTA that finishes its lookup last runs
- * the selection).  Outputs are identical to the two separate calls.
- *   counter  uint32 [1] device scratch, zero-filled once after allocation
- *            (tsv_workspace_clear); every call leaves it zero.  One per stream.
+ * k_max = k_fixed, in ONE kernel: every CTA adds its request's terms of the
+ * batch sums (exact int64 atomics) after its lookup, and the CTA that arrives
+ * last evaluates the goodput of each k and writes k*, the goodput values and k_i.
+ * Outputs are identical to the two separate calls.
+ *   counter  device scratch of TSV_LOOKUP_CHOOSE_SCRATCH bytes (8-byte aligned),
+ *            zero-filled once after allocation (tsv_workspace_clear); every call
+ *            leaves it zero.  One per stream.
  * ------------------------------------------------------------------------ */
+#define TSV_LOOKUP_CHOOSE_SCRATCH 512
 TSV_API tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                                        int32_t n_min, int32_t n_max, int32_t k_fixed,
                                        int32_t* proposals, int32_t* proposal_len,

@@ -22,7 +22,18 @@
 
 namespace tsv {
 
-constexpr int kLookupThreads = 256;  // == kGpThreads: the fused variant runs choose_k_block
+constexpr int kLookupThreads = 256;  // == kGpThreads: the fused variant finishes with CTA-wide code
+
+// Fused lookup + choose-k scratch (TSV_LOOKUP_CHOOSE_SCRATCH bytes, zero when idle): the batch sums
+// of ArgMaxGoodput accumulated by every CTA with integer atomics, and the arrival counter.
+struct FusedScratch {
+    unsigned int counter;
+    unsigned int pad;
+    unsigned long long L[kGpMaxK];  // sum_i rint(2^32 l(alpha_i, min(k, cap_i)))  (two's complement add)
+    unsigned long long N[kGpMaxK];  // sum_i min(k, cap_i)
+    unsigned long long C[3];        // sum ctx_len, sum ctx_len over cap > 0, #{cap > 0}
+};
+static_assert(sizeof(FusedScratch) <= TSV_LOOKUP_CHOOSE_SCRATCH, "scratch size");
 constexpr int kLookupUnroll = 4;     // groups in flight per thread
 
 struct Group {
@@ -85,6 +96,65 @@ __device__ __forceinline__ uint32_t scan_group(const int32_t* __restrict__ ctx, 
     return best;
 }
 
+// Fused ArgMaxGoodput (CTA-wide, after request i's proposal length is written): warp 0 adds
+// request i's terms of the batch sums with integer atomics (exact, any order: the same sums
+// as choose_k_block), then the CTA that arrives last evaluates G(k) from the sums, writes k*,
+// the goodput values and k_i for every request, and re-zeroes the scratch.
+__device__ __forceinline__ void fused_choose_k(const ChooseArgs& A, FusedScratch* S, int32_t i, int32_t ci) {
+    __shared__ int s_last, s_best;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {  // ci: request i's proposal length (valid in warp 0)
+        const double a = __ldcg(A.alpha + (A.alpha_per_request ? i : 0));
+        const int32_t k = lane;
+        if (k <= A.k_max) {
+            int32_t ki = k < ci ? k : ci;
+            if (ki < 0) ki = 0;
+            double l = 1.0;  // l(a, ki) by Horner, op-for-op choose_k_block
+            for (int32_t j = 0; j < ki; ++j) l = __fma_rn(a, l, 1.0);
+            atomicAdd(&S->L[k], static_cast<unsigned long long>(__double2ll_rn(l * 0x1p32)));
+            atomicAdd(&S->N[k], static_cast<unsigned long long>(ki));
+        }
+        if (lane == 0) {
+            const int32_t cl = __ldcg(A.ctx_len + i);
+            atomicAdd(&S->C[0], static_cast<unsigned long long>(static_cast<long long>(cl)));
+            if (ci > 0) {
+                atomicAdd(&S->C[1], static_cast<unsigned long long>(static_cast<long long>(cl)));
+                atomicAdd(&S->C[2], 1ull);
+            }
+        }
+        __threadfence();  // this request's terms (and proposal row) before the arrival
+        __syncwarp();
+        if (lane == 0) {
+            const unsigned int prev = atomicAdd(&S->counter, 1u);
+            s_last = prev == static_cast<unsigned int>(A.B) - 1u;
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x < 32) {
+        GpTotals t;
+        t.L = lane <= A.k_max ? static_cast<long long>(atomicAdd(&S->L[lane], 0ull)) : 0;
+        t.N = lane <= A.k_max ? static_cast<long long>(atomicAdd(&S->N[lane], 0ull)) : 0;
+        t.c0 = static_cast<long long>(atomicAdd(&S->C[0], 0ull));
+        t.c1 = static_cast<long long>(atomicAdd(&S->C[1], 0ull));
+        t.c2 = static_cast<long long>(atomicAdd(&S->C[2], 0ull));
+        t.c3 = A.B;
+        const int kb = gp_argmax_warp(A, t);
+        if (lane == 0) s_best = kb;
+        if (lane < kGpMaxK) {  // idle again for the next call
+            S->L[lane] = 0ull;
+            S->N[lane] = 0ull;
+        }
+        if (lane < 3) S->C[lane] = 0ull;
+        if (lane == 0) S->counter = 0u;
+    }
+    if (A.k_per_request) {
+        __syncthreads();
+        gp_write_k_per_request(A, s_best);
+    }
+}
+
 // FUSED: the CTA that finishes last also runs ArgMaxGoodput (PLD policy, cap_i = the
 // proposal lengths just written) -- GetVerificationLen right after Propose (Listing 1).
 template <bool FUSED>
@@ -100,6 +170,7 @@ __global__ void __launch_bounds__(kLookupThreads)
     const int32_t off = __ldg(ctx_offsets + i);
     const int32_t L = __ldg(ctx_offsets + i + 1) - off;
     const int32_t* c = ctx + off;
+    int32_t my_len = 0;  // this request's proposal length (warp 0)
     uint32_t best = 0;
     if (L >= 2) {
         const int64_t last = static_cast<int64_t>(off) + L - 1;
@@ -140,11 +211,12 @@ __global__ void __launch_bounds__(kLookupThreads)
         const int32_t e_star = static_cast<int32_t>(v & 0xFFFFFu);
         int32_t len = 0;
         if (L >= 2 && n_star >= n_min) len = min(K, L - 1 - e_star);
+        my_len = len;
         int32_t* out = proposals + static_cast<int64_t>(i) * K;
         for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? __ldg(c + e_star + 1 + t) : -1;
         if (tid == 0) proposal_len[i] = len;
     }
-    if (FUSED && last_cta_done(counter, static_cast<uint32_t>(B))) choose_k_block(ca);
+    if (FUSED) fused_choose_k(ca, reinterpret_cast<FusedScratch*>(counter), i, my_len);
 }
 
 }  // namespace tsv
@@ -183,6 +255,7 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
     TSV_REQUIRE(k_fixed >= 1 && k_fixed <= TSV_MAX_K, "tsv_propose_lookup_choose_k: k_fixed %d outside [1, %d]", k_fixed, TSV_MAX_K);
     TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len && alpha && ctx_len && k_out && counter,
                 "tsv_propose_lookup_choose_k: a required array is NULL");
+    TSV_REQUIRE((reinterpret_cast<uintptr_t>(counter) & 7u) == 0, "tsv_propose_lookup_choose_k: scratch must be 8-byte aligned");
     TSV_TRY(check_device());
     ChooseArgs A = {};
     A.alpha = alpha;

@@ -91,7 +91,7 @@ class SpecStep:
         self.num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
         self.out_tokens = torch.empty((B, K + 1), dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)  # fused lookup + choose-k
+        self.counter = tsv.lookup_choose_scratch(dev)  # fused lookup + choose-k
         self.fused = fused
         self.args = []
         for vb in inp.verify:

@@ -25,6 +25,7 @@ DEVSTATUS_BAD_K = 2
 DEVSTATUS_NO_WEIGHT = 4
 VERIFY_NO_PRUNE = 1
 VERIFY_SHARD_DENSE = 2
+LOOKUP_CHOOSE_SCRATCH = 512  # TSV_LOOKUP_CHOOSE_SCRATCH
 POLICY_DRAFT = 0
 POLICY_PLD = 1
 EST_TESTED = 0
@@ -362,15 +363,22 @@ def tsv_verify_shard_emit(args: VerifyArgs, masks: torch.Tensor, keys: torch.Ten
     _check(_lib.tsv_verify_shard_emit(ctypes.byref(args), _ptr(masks), _ptr(keys), _stream(stream)))
 
 
+def lookup_choose_scratch(device) -> torch.Tensor:
+    """Zero-filled scratch for tsv_propose_lookup_choose_k."""
+    return torch.zeros(LOOKUP_CHOOSE_SCRATCH // 8, dtype=torch.int64, device=device)
+
+
 def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, ctx_len, target,
                                 pld_cost_ms, counter, kv_free_slots=-1, alpha_per_request=None,
                                 proposals=None, proposal_len=None, k_out=None, goodput_out=None,
                                 k_per_request=None, stream=None):
-    """Fused prompt lookup + PLD goodput selection.  ``counter``: uint32 [1], zeroed once.
+    """Fused prompt lookup + PLD goodput selection.  ``counter``: device scratch of
+    LOOKUP_CHOOSE_SCRATCH bytes (e.g. lookup_choose_scratch()), zeroed once.
     Returns (proposals, proposal_len, k_out, goodput_out)."""
     B = ctx_offsets.numel() - 1
     dev = ctx_offsets.device
-    _want(counter, torch.int32, 1, "counter")
+    if counter.numel() * counter.element_size() < LOOKUP_CHOOSE_SCRATCH:
+        raise ValueError(f"counter scratch must hold {LOOKUP_CHOOSE_SCRATCH} bytes")
     if proposals is None:
         proposals = torch.empty((B, k_fixed), dtype=torch.int32, device=dev)
     if proposal_len is None:
