@@ -755,6 +755,8 @@ def run_reference(args, rank, world):
 
 
 def main():
+    # NCCL's own messages (e.g. its version banner) go to stderr: stdout carries only the JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
