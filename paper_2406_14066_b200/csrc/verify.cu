@@ -306,7 +306,13 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
 // float4, the 3-instruction prune test, deferred exact evaluation of survivors.  Warps
 // racing chunks of the same row share their threshold (red.max on rowT, read back before
 // the final flush) and their best key (red.max on rowkey).  No barriers, no shared memory.
-constexpr int kRaceThreads = 256;
+#ifndef TSV_RACE_THREADS
+#define TSV_RACE_THREADS 512
+#endif
+#ifndef TSV_RACE_MINB
+#define TSV_RACE_MINB (1024 / TSV_RACE_THREADS)
+#endif
+constexpr int kRaceThreads = TSV_RACE_THREADS;
 constexpr int kRaceWarps = kRaceThreads / 32;
 constexpr int kUnroll = 2;
 
@@ -331,7 +337,7 @@ __device__ __forceinline__ uint32_t smid() {
 #endif
 
 template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false>
-__global__ void __launch_bounds__(kRaceThreads, 4) verify_race_kernel(const RaceParams P) {
+__global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kernel(const RaceParams P) {
     pdl_wait();  // the scan kernel's ReqMeta / rowT / rowkey are complete and visible
     pdl_launch_dependents();
     const int lane = threadIdx.x & 31;
@@ -1002,7 +1008,7 @@ static int sm_count();
 // (148 SMs x 4 CTAs x 8 warps), in whole 128-column iterations.  Never changes results.
 static int32_t auto_chunk(const tsv_verify_args* a) {
     if (a->chunk > 0) return a->chunk;
-    const int64_t warps = static_cast<int64_t>(sm_count()) * 4 * 8;
+    const int64_t warps = static_cast<int64_t>(sm_count()) * 32;  // resident warps of the race kernel
     const int64_t rows_x_cols = static_cast<int64_t>(a->B) * a->vocab;
     int64_t c = (rows_x_cols + warps - 1) / warps;
     c = (c + 127) / 128 * 128;

@@ -58,6 +58,7 @@ for trial in range(3):
 
 for us, buf in res:
     used = buf[:, 2] > 0
+    item_idx = np.nonzero(used)[0]
     t = buf[used].astype(np.int64)
     t0 = t[:, 0].min()
     start, sdone, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3
@@ -78,12 +79,19 @@ for us, buf in res:
     print(f"  per-SM last end: p10 {np.percentile(sm_max, 10):5.2f} p50 {np.median(sm_max):5.2f} "
           f"p90 {np.percentile(sm_max, 90):5.2f} max {sm_max.max():5.2f} | within-SM spread p50 "
           f"{np.median(sm_spread):5.2f} | within-CTA spread p50 {np.median(cta_spread):5.2f} us")
-    slot = cta // 148
+    slot = cta // int(os.environ.get("SLOT_CTAS", "148"))
     for sl in np.unique(slot):  # CTAs by launch slot (blockIdx // SMs)
         msk = slot == sl
         print(f"  CTA slot {sl}: items {msk.sum()} end p50 {np.median(end[msk]):5.2f} "
               f"p90 {np.percentile(end[msk], 90):5.2f} max {end[msk].max():5.2f} | stream p50 "
               f"{np.median((sdone - start)[msk]):5.2f}")
+    wpc = int(os.environ.get("WARPS_PER_CTA", "16"))
+    wic = item_idx % wpc  # first round: item = global warp id
+    line = []
+    for w in range(wpc):
+        msk = wic == w
+        line.append(f"{w}:{np.median(end[msk]):.1f}")
+    print("  end p50 by warp-in-CTA:", " ".join(line))
     bins = np.arange(0, end.max() + 0.5, 0.5)
     inflight = [int(((start <= b) & (end > b)).sum()) for b in bins]
     print("  items in flight every 0.5 us:", inflight)
