@@ -10,12 +10,18 @@
  *   tsv_verify_accept      rejection-sampling acceptance + bonus
  *   tsv_update_acceptance  moving-average acceptance update
  * The target model's Score step is not here: its output (probability rows p)
- * is an input.  Readings of silent or garbled passages are numbered R1..R23
- * in DESIGN.md section 3 and cited below.
+ * is an input.  Readings of silent or garbled passages are numbered R1..R26
+ * in DESIGN.md section 3 and cited below.  Beyond the four calls: vocab-
+ * sharded and request-sharded variants (NCCL), greedy and softmax-from-logits
+ * verify, a fused verify + update, and a closed-loop harness.
  *
  * Conventions (all entry points):
- *  - Array arguments are DEVICE pointers (cudaMalloc / torch CUDA memory) owned
- *    by the caller; the library never allocates, frees or retains them.
+ *  - Array arguments are DEVICE-ACCESSIBLE pointers owned by the caller; the
+ *    library never allocates, frees or retains them.  Read-only inputs may also
+ *    live in pinned host memory (cudaHostAlloc / torch pin_memory(), mapped
+ *    into the device address space by UVA): the kernels then read exactly the
+ *    bytes they need over PCIe (zero-copy; e.g. only row m of p and q in the
+ *    lazy verify).  Outputs and workspaces must be device memory.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Every call is asynchronous on `stream`, never synchronises, never
  *    allocates device memory, and is CUDA-graph capturable.

@@ -152,15 +152,21 @@ def _check(status: int):
 
 
 def _ptr(t: Optional[torch.Tensor], rows_ok: bool = False) -> Optional[int]:
-    """Device pointer of a contiguous CUDA tensor (rows_ok: a 2-D row-strided view is fine)."""
+    """Device-accessible pointer of a contiguous tensor (rows_ok: a 2-D row-strided view is fine):
+    a CUDA tensor, or a pinned host tensor, which the kernels read over PCIe (UVA zero-copy)."""
     if t is None:
         return None
-    if not t.is_cuda:
-        raise ValueError("libtsv takes CUDA tensors (device pointers); got a CPU tensor")
+    if not t.is_cuda and not t.is_pinned():
+        raise ValueError("libtsv takes CUDA tensors or pinned host tensors; got pageable host memory")
     ok = t.is_contiguous() or (rows_ok and t.dim() == 2 and t.stride(1) == 1)
     if not ok:
         raise ValueError("libtsv takes contiguous tensors")
     return t.data_ptr()
+
+
+def _dev(t: torch.Tensor) -> torch.device:
+    """Where to allocate outputs / workspaces for an input tensor (pinned host inputs -> current GPU)."""
+    return t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
 
 
 def _stream(stream) -> Optional[int]:
@@ -190,7 +196,7 @@ def tsv_propose_lookup(ctx: torch.Tensor, ctx_offsets: torch.Tensor, n_min: int,
     B = ctx_offsets.numel() - 1
     _want(ctx, torch.int32, None, "ctx")
     _want(ctx_offsets, torch.int32, None, "ctx_offsets")
-    dev = ctx_offsets.device
+    dev = _dev(ctx_offsets)
     if proposals is None:
         proposals = torch.empty((B, k_fixed), dtype=torch.int32, device=dev)
     if proposal_len is None:
@@ -264,7 +270,7 @@ def tsv_verify_accept(p, q, row_offsets, draft_tokens, request_ids, seed, step, 
                       chunk=0, flags=0, vocab=None, stream=None):
     """Rejection-sampling verify/accept.  Returns (num_accepted, out_tokens)."""
     B = row_offsets.numel() - 1
-    dev = row_offsets.device
+    dev = _dev(row_offsets)
     if num_accepted is None:
         num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
     if out_tokens is None:
@@ -284,7 +290,7 @@ def tsv_verify_greedy(p, row_offsets, draft_tokens, k_max, num_accepted=None, ou
                       device_status=None, workspace=None, vocab=None, chunk=0, stream=None):
     """Greedy (temperature-0) verify (reading R24).  Returns (num_accepted, out_tokens)."""
     B = row_offsets.numel() - 1
-    dev = p.device
+    dev = _dev(p)
     if num_accepted is None:
         num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
     if out_tokens is None:
@@ -311,7 +317,7 @@ def tsv_verify_accept_logits(zp, zq, row_offsets, draft_tokens, request_ids, see
                              workspace=None, vocab=None, chunk=0, flags=0, stream=None):
     """Fused softmax-from-logits verify (reading R23).  Returns (num_accepted, out_tokens)."""
     B = row_offsets.numel() - 1
-    dev = zp.device
+    dev = _dev(zp)
     if num_accepted is None:
         num_accepted = torch.empty(B, dtype=torch.int32, device=dev)
     if out_tokens is None:
@@ -376,7 +382,7 @@ def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, 
     LOOKUP_CHOOSE_SCRATCH bytes (e.g. lookup_choose_scratch()), zeroed once.
     Returns (proposals, proposal_len, k_out, goodput_out)."""
     B = ctx_offsets.numel() - 1
-    dev = ctx_offsets.device
+    dev = _dev(ctx_offsets)
     if counter.numel() * counter.element_size() < LOOKUP_CHOOSE_SCRATCH:
         raise ValueError(f"counter scratch must hold {LOOKUP_CHOOSE_SCRATCH} bytes")
     if proposals is None:
@@ -412,7 +418,7 @@ def tsv_goodput_choose_k(alpha, ctx_len, cap, k_max, policy, target, draft=(0.0,
                          goodput_out=None, k_per_request=None, stream=None):
     """ArgMaxGoodput (Listing 2).  Returns (k_out[1], goodput[k_max+1], k_per_request)."""
     B = ctx_len.numel()
-    dev = ctx_len.device
+    dev = _dev(ctx_len)
     _want(alpha, torch.float64, 1, "alpha")
     _want(ctx_len, torch.int32, None, "ctx_len")
     _want(cap, torch.int32, B, "cap")
@@ -446,7 +452,7 @@ def tsv_update_acceptance(alpha, num_accepted, row_offsets, decay=0.9, estimator
 def tsv_goodput_partial(alpha, ctx_len, cap, k_max, alpha_per_request=None, sums=None, stream=None):
     """This rank's exact int64 batch sums for ArgMaxGoodput (TSV_GP_SUMS(k_max) words)."""
     B = ctx_len.numel()
-    dev = ctx_len.device
+    dev = _dev(ctx_len)
     _want(ctx_len, torch.int32, None, "ctx_len")
     _want(cap, torch.int32, B, "cap")
     per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
@@ -461,7 +467,7 @@ def tsv_goodput_finalize(sums, k_max, policy, target, draft=(0.0, 0.0, 0.0), pld
                          kv_free_slots=-1, cap=None, k_out=None, goodput_out=None, k_per_request=None,
                          stream=None):
     """ArgMaxGoodput on (rank-summed) sums; k_per_request = min(k*, cap) for the local requests."""
-    dev = sums.device
+    dev = _dev(sums)
     _want(sums, torch.int64, gp_sums_len(k_max), "sums")
     if k_out is None:
         k_out = torch.empty(1, dtype=torch.int32, device=dev)
@@ -480,7 +486,7 @@ def tsv_update_partial(num_accepted, row_offsets, estimator=EST_TESTED, sums=Non
     B = num_accepted.numel()
     _want(row_offsets, torch.int32, B + 1, "row_offsets")
     if sums is None:
-        sums = torch.empty(2, dtype=torch.int64, device=num_accepted.device)
+        sums = torch.empty(2, dtype=torch.int64, device=_dev(num_accepted))
     _check(_lib.tsv_update_partial(_ptr(num_accepted), _ptr(row_offsets), B, int(estimator), _ptr(sums),
                                    _stream(stream)))
     return sums
@@ -545,7 +551,7 @@ def tsv_goodput_choose_k_sharded(alpha, ctx_len, cap, k_max, policy, target, com
                                  sums_ws=None, stream=None):
     """Request-sharded ArgMaxGoodput: partial -> ncclAllReduce(sum, int64) -> finalize."""
     B = ctx_len.numel()
-    dev = ctx_len.device
+    dev = _dev(ctx_len)
     per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
     if k_out is None:
         k_out = torch.empty(1, dtype=torch.int32, device=dev)
@@ -566,7 +572,7 @@ def tsv_update_acceptance_sharded(alpha, num_accepted, row_offsets, comm: "Comm"
     """Request-sharded global alpha update: partial -> ncclAllReduce(sum, int64) -> finalize."""
     B = num_accepted.numel()
     if sums_ws is None:
-        sums_ws = torch.empty(2, dtype=torch.int64, device=num_accepted.device)
+        sums_ws = torch.empty(2, dtype=torch.int64, device=_dev(num_accepted))
     _check(_lib.tsv_update_acceptance_sharded(_ptr(alpha), _ptr(num_accepted), _ptr(row_offsets), B,
                                               float(decay), int(estimator), _ptr(sums_ws), comm.handle,
                                               _stream(stream)))

@@ -805,3 +805,21 @@ def test_verify_logits_prune_off_identical(tsv):
                                      flags=tsv.VERIFY_NO_PRUNE)
     torch.cuda.synchronize()
     assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+
+
+# ------------------------------------------------------------------- zero-copy host inputs
+def test_pinned_host_inputs_zero_copy(tsv):
+    # p, q and the metadata left in pinned host memory: the kernels read them over PCIe (UVA)
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=26)
+    ona, oout, _ = oracle_verify(vb, 7, 2)
+    pin = lambda t: t.contiguous().pin_memory()
+    na, out = tsv.tsv_verify_accept(pin(vb.p), pin(vb.q), pin(vb.row_offsets), pin(vb.draft_tokens),
+                                    pin(vb.request_ids), 7, 2, 8,
+                                    num_accepted=torch.empty(64, dtype=torch.int32, device=DEV),
+                                    out_tokens=torch.empty((64, 9), dtype=torch.int32, device=DEV))
+    torch.cuda.synchronize()
+    assert (_np(na) == ona).all() and (_np(out) == oout).all()
+    ctx, offs = synth.make_contexts(B=16, L=1024, seed=27)
+    pr, pl = tsv.tsv_propose_lookup(pin(torch.tensor(ctx)), pin(torch.tensor(offs)), 1, 4, 5)
+    opr, opl = oracle.lookup(ctx, offs, 1, 4, 5)
+    assert (_np(pr) == opr).all() and (_np(pl) == opl).all()
