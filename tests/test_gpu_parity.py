@@ -823,3 +823,20 @@ def test_pinned_host_inputs_zero_copy(tsv):
     pr, pl = tsv.tsv_propose_lookup(pin(torch.tensor(ctx)), pin(torch.tensor(offs)), 1, 4, 5)
     opr, opl = oracle.lookup(ctx, offs, 1, 4, 5)
     assert (_np(pr) == opr).all() and (_np(pl) == opl).all()
+
+
+# ------------------------------------------------------------------- randomised shape sweep
+def test_random_shape_sweep(tsv):
+    # 40 random (B, V, ld, k_max, lambda, dense/one-hot, chunk, seed, step) draws, bit-exact
+    rng = np.random.Generator(np.random.PCG64(99))
+    for trial in range(40):
+        B = int(rng.integers(1, 80))
+        V = int(rng.integers(1, 9000))
+        ld = (V + 3) // 4 * 4 + 4 * int(rng.integers(0, 3))
+        k_max = int(rng.integers(0, 16))
+        dense = bool(rng.random() < 0.7)
+        lam = float(rng.uniform(0.05, 0.99))
+        chunk = int(rng.choice([0, 128, 512, 1536]))
+        vb = synth.make_verify_batch(B=B, V=V, k_max=k_max, lam=lam, seed=1000 + trial, dense_q=dense, ld=ld)
+        seed, step = int(rng.integers(0, 2 ** 63)), int(rng.integers(0, 2 ** 32))
+        assert_verify_parity(tsv, vb, seed=seed, step=step, chunk=chunk)
