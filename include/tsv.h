@@ -269,6 +269,18 @@ TSV_API tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_per_r
                                 int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
                                 int32_t* k_per_request, void* stream);
 
+/* Batched ArgMaxGoodput for sweeps (BASELINE config 5): n_inst independent
+ * batches; instance n owns requests [inst_offsets[n], inst_offsets[n+1]) of the
+ * concatenated ctx_len / cap arrays and the global alpha[n].  Outputs k_out[n],
+ * goodput_out[n*(k_max+1) + k] (nullable), k_per_request (nullable, same layout
+ * as ctx_len).  Bit-identical to one tsv_goodput_choose_k per instance; one CTA
+ * per instance. */
+TSV_API tsv_status tsv_goodput_choose_k_batched(const double* alpha, const int32_t* ctx_len, const int32_t* cap,
+                                                const int32_t* inst_offsets, int32_t n_inst, int32_t k_max,
+                                                int32_t policy, tsv_latency_model target, tsv_latency_model draft,
+                                                double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
+                                                double* goodput_out, int32_t* k_per_request, void* stream);
+
 /* --------------------------------------------------------------------------
  * Fused Propose + GetVerificationLen for the PLD method (Listing 1 lines 15-16 +
  * 22-23): tsv_propose_lookup followed by tsv_goodput_choose_k

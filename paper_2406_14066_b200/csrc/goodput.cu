@@ -88,9 +88,61 @@ __global__ void update_finalize_kernel(double* alpha, const long long* sums, dou
     if (threadIdx.x == 0) ewma_apply(alpha, sums[0], sums[1], decay);
 }
 
+// Batched ArgMaxGoodput (config 5 sweeps): one CTA per independent instance n, which owns
+// requests [inst_offsets[n], inst_offsets[n+1]) of the concatenated ctx_len / cap arrays and
+// the global alpha[n]; identical arithmetic to tsv_goodput_choose_k per instance.
+__global__ void __launch_bounds__(kGpThreads) goodput_choose_k_batched_kernel(ChooseArgs A, const int32_t* inst_offsets,
+                                                                            int32_t n_inst) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t n = blockIdx.x;
+    if (n >= n_inst) return;
+    const int32_t lo = inst_offsets[n], hi = inst_offsets[n + 1];
+    ChooseArgs B = A;
+    B.alpha = A.alpha + n;
+    B.alpha_per_request = 0;
+    B.ctx_len = A.ctx_len + lo;
+    B.cap = A.cap + lo;
+    B.B = hi - lo;
+    B.k_out = A.k_out + n;
+    B.goodput_out = A.goodput_out ? A.goodput_out + static_cast<int64_t>(n) * (A.k_max + 1) : nullptr;
+    B.k_per_request = A.k_per_request ? A.k_per_request + lo : nullptr;
+    choose_k_block(B);
+}
+
 }  // namespace tsv
 
 using namespace tsv;
+
+extern "C" tsv_status tsv_goodput_choose_k_batched(const double* alpha, const int32_t* ctx_len, const int32_t* cap,
+                                                   const int32_t* inst_offsets, int32_t n_inst, int32_t k_max,
+                                                   int32_t policy, tsv_latency_model target, tsv_latency_model draft,
+                                                   double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
+                                                   double* goodput_out, int32_t* k_per_request, void* stream) {
+    TSV_REQUIRE(n_inst >= 0, "tsv_goodput_choose_k_batched: n_inst < 0");
+    TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_choose_k_batched: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
+    TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_choose_k_batched: unknown policy");
+    if (n_inst == 0) return TSV_OK;
+    TSV_REQUIRE(alpha && ctx_len && cap && inst_offsets && k_out, "tsv_goodput_choose_k_batched: a required array is NULL");
+    TSV_TRY(check_device());
+    ChooseArgs A = {};
+    A.alpha = alpha;
+    A.ctx_len = ctx_len;
+    A.cap = cap;
+    A.k_out = k_out;
+    A.goodput_out = goodput_out;
+    A.k_per_request = k_per_request;
+    A.target = target;
+    A.draft = draft;
+    A.pld_cost_ms = pld_cost_ms;
+    A.kv_free = static_cast<long long>(kv_free_slots);
+    A.k_max = k_max;
+    A.policy = policy;
+    TSV_CUDA(launch_pdl(goodput_choose_k_batched_kernel, dim3(static_cast<unsigned>(n_inst)), dim3(kGpThreads), 0,
+                        static_cast<cudaStream_t>(stream), A, inst_offsets, n_inst),
+             "goodput_choose_k_batched_kernel launch");
+    return TSV_OK;
+}
 
 extern "C" tsv_status tsv_goodput_partial(const double* alpha, int32_t alpha_per_request, const int32_t* ctx_len,
                                           const int32_t* cap, int32_t B, int32_t k_max, int64_t* sums,

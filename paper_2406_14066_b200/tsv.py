@@ -43,7 +43,7 @@ EXPORTED = [
     "tsv_update_finalize", "tsv_update_acceptance_sharded", "tsv_verify_shard_flags", "tsv_verify_shard_race",
     "tsv_verify_shard_emit", "tsv_verify_greedy", "tsv_verify_logits_workspace_size",
     "tsv_verify_accept_logits", "tsv_softmax_rows", "tsv_fit_latency_model", "tsv_sim_target",
-    "tsv_context_append",
+    "tsv_context_append", "tsv_goodput_choose_k_batched",
 ]
 
 
@@ -130,6 +130,8 @@ def _load() -> ctypes.CDLL:
         "tsv_fit_latency_model": ([P, P, P, i32, ctypes.POINTER(LatencyModel), P], ctypes.c_int),
         "tsv_sim_target": ([P, i32, P, i32, P, i32, i64, i32, P, P, P, P, P], ctypes.c_int),
         "tsv_context_append": ([P, i32, i32, P, P, i32, P, P, P], ctypes.c_int),
+        "tsv_goodput_choose_k_batched": ([P, P, P, P, i32, i32, i32, LatencyModel, LatencyModel, f64, i64,
+                                          P, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -433,6 +435,24 @@ def tsv_goodput_choose_k(alpha, ctx_len, cap, k_max, policy, target, draft=(0.0,
                                      _ptr(k_out), _ptr(goodput_out), _ptr(k_per_request),
                                      _stream(stream)))
     return k_out, goodput_out, k_per_request
+
+
+def tsv_goodput_choose_k_batched(alpha, ctx_len, cap, inst_offsets, k_max, policy, target, draft=(0.0, 0.0, 0.0),
+                                 pld_cost_ms=0.0, kv_free_slots=-1, k_out=None, goodput_out=None,
+                                 k_per_request=None, stream=None):
+    """n_inst independent ArgMaxGoodput problems in one launch.  Returns (k_out[n], goodput[n, k_max+1])."""
+    n = inst_offsets.numel() - 1
+    dev = _dev(ctx_len)
+    _want(alpha, torch.float64, n, "alpha")
+    if k_out is None:
+        k_out = torch.empty(n, dtype=torch.int32, device=dev)
+    if goodput_out is None:
+        goodput_out = torch.empty((n, k_max + 1), dtype=torch.float64, device=dev)
+    _check(_lib.tsv_goodput_choose_k_batched(_ptr(alpha), _ptr(ctx_len), _ptr(cap), _ptr(inst_offsets), n,
+                                             int(k_max), int(policy), LatencyModel(*target), LatencyModel(*draft),
+                                             float(pld_cost_ms), int(kv_free_slots), _ptr(k_out),
+                                             _ptr(goodput_out), _ptr(k_per_request), _stream(stream)))
+    return k_out, goodput_out
 
 
 def tsv_update_acceptance(alpha, num_accepted, row_offsets, decay=0.9, estimator=EST_TESTED,

@@ -840,3 +840,31 @@ def test_random_shape_sweep(tsv):
         vb = synth.make_verify_batch(B=B, V=V, k_max=k_max, lam=lam, seed=1000 + trial, dense_q=dense, ld=ld)
         seed, step = int(rng.integers(0, 2 ** 63)), int(rng.integers(0, 2 ** 32))
         assert_verify_parity(tsv, vb, seed=seed, step=step, chunk=chunk)
+
+
+def test_choose_k_batched_config5_sweep(tsv):
+    # BASELINE config 5: batch 1-512 x alpha 0.3-0.9, K = 8, both policies, one launch per sweep
+    for target, draft in PROFILES:
+        for pol in (0, 1):
+            Bs = list(range(1, 65)) + [96, 128, 200, 256, 300, 384, 511, 512]
+            alphas = (0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9)
+            ctxs, caps, offs, al, want_k, want_g = [], [], [0], [], [], []
+            for B in Bs:
+                ctx, cap = synth.make_goodput_instance(B, 8, seed=B)
+                if pol == 1:
+                    cap = np.random.Generator(np.random.PCG64(B)).integers(0, 9, B).astype(np.int32)
+                for a in alphas:
+                    ok, og = oracle.choose_k(a, ctx, cap, 8, pol, target, draft, pld_cost_ms=0.05)
+                    ctxs.append(ctx)
+                    caps.append(cap)
+                    offs.append(offs[-1] + B)
+                    al.append(a)
+                    want_k.append(ok)
+                    want_g.append(og)
+            k, g = tsv.tsv_goodput_choose_k_batched(
+                torch.tensor(al, dtype=torch.float64, device=DEV), torch.tensor(np.concatenate(ctxs), device=DEV),
+                torch.tensor(np.concatenate(caps), device=DEV), torch.tensor(np.array(offs, np.int32), device=DEV),
+                8, pol, target, draft, 0.05)
+            torch.cuda.synchronize()
+            assert (_np(k) == np.array(want_k)).all()
+            assert (_np(g).view(np.uint64) == np.stack(want_g).view(np.uint64)).all()
