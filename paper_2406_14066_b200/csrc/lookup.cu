@@ -22,7 +22,13 @@
 
 namespace tsv {
 
-constexpr int kLookupThreads = 256;  // == kGpThreads: the fused variant finishes with CTA-wide code
+#ifndef TSV_LOOKUP_THREADS
+#define TSV_LOOKUP_THREADS 1024
+#endif
+#ifndef TSV_LOOKUP_UNROLL
+#define TSV_LOOKUP_UNROLL 1
+#endif
+constexpr int kLookupThreads = TSV_LOOKUP_THREADS;  // the fused variant's tail is written for any multiple of 32
 
 // Fused lookup + choose-k scratch (TSV_LOOKUP_CHOOSE_SCRATCH bytes, zero when idle): the batch sums
 // of ArgMaxGoodput accumulated by every CTA with integer atomics, and the arrival counter.
@@ -34,7 +40,7 @@ struct FusedScratch {
     unsigned long long C[3];        // sum ctx_len, sum ctx_len over cap > 0, #{cap > 0}
 };
 static_assert(sizeof(FusedScratch) <= TSV_LOOKUP_CHOOSE_SCRATCH, "scratch size");
-constexpr int kLookupUnroll = 4;     // groups in flight per thread
+constexpr int kLookupUnroll = TSV_LOOKUP_UNROLL;  // groups in flight per thread
 
 struct Group {
     int4 cur;   // ctx[4g .. 4g+3]
