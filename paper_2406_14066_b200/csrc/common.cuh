@@ -74,12 +74,8 @@ __device__ __forceinline__ float u_acc_from_word(uint32_t x) {
     return __uint2float_rn(x >> 8) * 0x1p-24f;
 }
 
-// u_race = (2 (x & 0x7FFFFF) + 1) 2^-24 in (0, 1): exact in binary32 (R7).
-__device__ __forceinline__ float u_race_from_word(uint32_t x) {
-    return __uint2float_rn(2u * (x & 0x7FFFFFu) + 1u) * 0x1p-24f;
-}
-
-// 1 - u_race, exactly, with one LOP3 and one FADD:
+// The race uniform is u_race = (2 (x & 0x7FFFFF) + 1) 2^-24 in (0, 1), exact in binary32 (R7);
+// the kernels only ever need 1 - u_race, exactly, with one LOP3 and one FADD:
 // as_float((x & 0x7FFFFF) ^ 0x3FFFFFFF) = 2 - (m+1) 2^-23 with m = x & 0x7FFFFF, and
 // subtracting (1 - 2^-24) leaves 1 - (2m+1) 2^-24 (24 significant bits: exact).
 __device__ __forceinline__ float one_minus_u_race(uint32_t x) {
@@ -224,38 +220,6 @@ __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
-}
-
-// ---------------------------------------------------------------- TMA bulk copy + mbarrier
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {  // spin on try_wait.parity
-    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(a), "r"(phase)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
-        "l"(gmem_src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- programmatic dependent launch

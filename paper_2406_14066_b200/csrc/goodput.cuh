@@ -256,24 +256,4 @@ __device__ __forceinline__ void update_block(const UpdateArgs& A, long long* sum
     }
 }
 
-// "Last CTA done": every CTA calls this after its own results are written; returns true
-// (to every thread) in the one CTA that arrives last, which then sees all other CTAs'
-// writes.  The counter is left at zero again (self-cleaning).
-__device__ __forceinline__ bool last_cta_done(uint32_t* counter, uint32_t n_ctas) {
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t prev = atomicAdd(counter, 1u);
-        const int last = prev == n_ctas - 1;
-        if (last) {
-            atomicExch(counter, 0u);
-            __threadfence();
-        }
-        s_last = last;
-    }
-    __syncthreads();
-    return s_last != 0;
-}
-
 }  // namespace tsv
