@@ -1161,8 +1161,8 @@ extern "C" tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream) 
     TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
                 "tsv_verify_accept: unsharded call needs vocab_offset == 0 and vocab == vocab_global "
                 "(use tsv_verify_shard_partial/combine for vocab shards)");
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_accept: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
@@ -1177,8 +1177,8 @@ extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double*
     TSV_REQUIRE(alpha != nullptr, "tsv_verify_accept_update: alpha is NULL");
     TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_verify_accept_update: decay %g outside [0, 1]", decay);
     TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED, "tsv_verify_accept_update: unknown estimator");
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_accept_update: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
@@ -1196,8 +1196,8 @@ extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double*
 extern "C" tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_shard_tuple* tuples_out,
                                                void* stream) {
     TSV_TRY(validate(a));
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     TSV_REQUIRE(tuples_out != nullptr, "tsv_verify_shard_partial: tuples_out is NULL");
     TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_shard_partial: workspace too small (%llu < %llu bytes)",
@@ -1210,8 +1210,8 @@ extern "C" tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_sha
 extern "C" tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const tsv_shard_tuple* gathered,
                                                int32_t num_shards, void* stream) {
     TSV_TRY(validate(a));
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     TSV_REQUIRE(gathered != nullptr, "tsv_verify_shard_combine: gathered is NULL");
     TSV_REQUIRE(num_shards >= 1, "tsv_verify_shard_combine: num_shards < 1");
     RaceParams P = make_params(a);
@@ -1225,8 +1225,8 @@ extern "C" tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const t
 
 extern "C" tsv_status tsv_verify_shard_flags(const tsv_verify_args* a, uint64_t* masks_out, void* stream) {
     TSV_TRY(validate(a));
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     TSV_REQUIRE(masks_out != nullptr, "tsv_verify_shard_flags: masks_out is NULL");
     RaceParams P = make_params(a);
     TSV_CUDA(launch_pdl(verify_shard_flags_kernel, dim3(static_cast<unsigned>((a->B + 7) / 8)), dim3(256), 0,
@@ -1238,8 +1238,8 @@ extern "C" tsv_status tsv_verify_shard_flags(const tsv_verify_args* a, uint64_t*
 extern "C" tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint64_t* masks, uint64_t* keys_out,
                                             void* stream) {
     TSV_TRY(validate(a));
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     TSV_REQUIRE(masks && keys_out, "tsv_verify_shard_race: NULL argument");
     TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_shard_race: workspace too small (%llu < %llu bytes)",
@@ -1265,8 +1265,8 @@ extern "C" tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint
 extern "C" tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_t* masks, const uint64_t* keys,
                                             void* stream) {
     TSV_TRY(validate(a));
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     TSV_REQUIRE(masks && keys, "tsv_verify_shard_emit: NULL argument");
     RaceParams P = make_params(a);
     TSV_CUDA(launch_pdl(verify_shard_emit_kernel, dim3(static_cast<unsigned>((a->B + 7) / 8)), dim3(256), 0,
@@ -1346,8 +1346,8 @@ extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float t
                 "tsv_verify_accept_logits: vocab sharding is not supported");
     TSV_REQUIRE(temperature > 0.0f && temperature < INFINITY, "tsv_verify_accept_logits: temperature %g must be > 0",
                 static_cast<double>(temperature));
-    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;
+    TSV_TRY(check_device());
     RaceParams P = make_params(a);
     const size_t need = align256(workspace_bytes(a)) + logits_extra_bytes(a, P.n_chunks);
     TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= need,

@@ -109,3 +109,26 @@ def test_binding_rejects_cpu_tensors(tsv):
     import torch
     with pytest.raises(ValueError):
         tsv._ptr(torch.zeros(4))
+
+
+def test_empty_batch_is_a_noop_without_device_work(tsv):
+    # B = 0: every entry point returns TSV_OK before touching the device (no GPU needed)
+    L = tsv.lib()
+    a = tsv.VerifyArgs()
+    a.B, a.k_max, a.vocab, a.vocab_global, a.ld = 0, 4, 8, 8, 8
+    dummy = ctypes.c_void_p(16)
+    assert L.tsv_verify_accept(ctypes.byref(a), None) == 0
+    assert L.tsv_verify_greedy(ctypes.byref(a), None) == 0
+    assert L.tsv_verify_accept_logits(ctypes.byref(a), 1.0, None) == 0
+    assert L.tsv_verify_accept_update(ctypes.byref(a), dummy, 0, 0.9, 0, None) == 0
+    assert L.tsv_verify_shard_partial(ctypes.byref(a), None, None) == 0
+    assert L.tsv_verify_shard_combine(ctypes.byref(a), None, 1, None) == 0
+    assert L.tsv_verify_shard_flags(ctypes.byref(a), None, None) == 0
+    assert L.tsv_verify_shard_race(ctypes.byref(a), None, None, None) == 0
+    assert L.tsv_verify_shard_emit(ctypes.byref(a), None, None, None) == 0
+    assert L.tsv_update_acceptance(None, 0, None, None, 0, 0.9, 0, None) == 0
+    assert L.tsv_sim_target(None, 5, None, 0, None, 16, 16, 0, None, None, None, None, None) == 0
+    assert L.tsv_context_append(None, 16, 0, None, None, 5, None, None, None) == 0
+    assert L.tsv_softmax_rows(None, 16, 16, 0, 1.0, None, None) == 0
+    m = tsv.LatencyModel(0.001, 0.05, 2.0)
+    assert L.tsv_goodput_choose_k_batched(None, None, None, None, 0, 8, 0, m, m, 0.0, -1, None, None, None, None) == 0
