@@ -435,7 +435,14 @@ TSV_API tsv_status tsv_update_acceptance_sharded(double* alpha, const int32_t* n
  * tsv_debug_philox: out[4t..4t+3] = Philox4x32-10(ctr[4t..4t+3], key[0..1]) on the
  *   device; race_variant != 0 uses the row-specialised evaluation of the race
  *   kernels (philox_race).  ctr: uint32 [4n], key: uint32 [2], out: uint32 [4n].
+ * tsv_debug_race_row: one warp races the weights w[V] with the given Philox words
+ *   (one per element, instead of generated ones) through the race kernels' logic
+ *   (prune != 0: the prune test and deferred exact evaluation; 0: every element
+ *   exact) and writes the packed key (bits(score) << 32 | ~v, 0 = no positive
+ *   weight) to *key_out (device uint64).
  * ------------------------------------------------------------------------ */
+TSV_API tsv_status tsv_debug_race_row(const float* w, const uint32_t* words, int32_t V, int32_t prune,
+                                      uint64_t* key_out, void* stream);
 TSV_API tsv_status tsv_debug_race_E(uint32_t m_begin, uint32_t n, float* out, void* stream);
 TSV_API tsv_status tsv_debug_philox(const uint32_t* ctr, const uint32_t* key, uint32_t n, uint32_t* out,
                                     int32_t race_variant, void* stream);

@@ -1395,3 +1395,49 @@ extern "C" tsv_status tsv_softmax_rows(const float* z, int64_t ld, int32_t vocab
              "softmax_rows_kernel launch");
     return TSV_OK;
 }
+
+// ------------------------------------------------------------------ diagnostics (tests)
+namespace tsv {
+// One warp races one row of weights with INJECTED Philox words (instead of generated ones),
+// through exactly the race kernel's Race logic: prune test, deferred exact evaluation, packed
+// keys.  Lets the GPU tests drive adversarial words (identical words -> exact score ties).
+template <bool PRUNE>
+__global__ void debug_race_row_kernel(const float* __restrict__ w, const uint32_t* __restrict__ words, int32_t V,
+                                      unsigned long long* key_out) {
+    const int lane = threadIdx.x & 31;
+    const int32_t nq = (V + 3) >> 2;
+    Race R;
+    R.init();
+    for (int32_t f0 = 0; f0 < nq; f0 += 32) {
+        const int32_t f = f0 + lane;
+        float wv[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t x[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int32_t v = 4 * f + t;
+            if (f < nq && v < V) {
+                wv[t] = w[v];
+                x[t] = words[v];
+            }
+        }
+        const uint4 r = make_uint4(x[0], x[1], x[2], x[3]);
+        if (PRUNE && R.T == 0.0f) R.warm(wv, r);
+        R.quad<PRUNE>(wv, r, static_cast<uint32_t>(4 * f));
+        if (PRUNE) R.sync_T();
+    }
+    R.finish<PRUNE>(R.T);
+    const uint64_t key = warp_max_u64(R.best);
+    if (lane == 0) *key_out = key;
+}
+}  // namespace tsv
+
+extern "C" tsv_status tsv_debug_race_row(const float* w, const uint32_t* words, int32_t V, int32_t prune,
+                                         uint64_t* key_out, void* stream) {
+    TSV_REQUIRE(w && words && key_out && V >= 1, "tsv_debug_race_row: bad arguments");
+    TSV_TRY(check_device());
+    auto* k = reinterpret_cast<unsigned long long*>(key_out);
+    if (prune) debug_race_row_kernel<true><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(w, words, V, k);
+    else debug_race_row_kernel<false><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(w, words, V, k);
+    TSV_CUDA(cudaGetLastError(), "debug_race_row_kernel launch");
+    return TSV_OK;
+}

@@ -43,7 +43,7 @@ EXPORTED = [
     "tsv_update_finalize", "tsv_update_acceptance_sharded", "tsv_verify_shard_flags", "tsv_verify_shard_race",
     "tsv_verify_shard_emit", "tsv_verify_greedy", "tsv_verify_logits_workspace_size",
     "tsv_verify_accept_logits", "tsv_softmax_rows", "tsv_fit_latency_model", "tsv_sim_target",
-    "tsv_context_append", "tsv_goodput_choose_k_batched",
+    "tsv_context_append", "tsv_goodput_choose_k_batched", "tsv_debug_race_row",
 ]
 
 
@@ -132,6 +132,7 @@ def _load() -> ctypes.CDLL:
         "tsv_context_append": ([P, i32, i32, P, P, i32, P, P, P], ctypes.c_int),
         "tsv_goodput_choose_k_batched": ([P, P, P, P, i32, i32, i32, LatencyModel, LatencyModel, f64, i64,
                                           P, P, P, P], ctypes.c_int),
+        "tsv_debug_race_row": ([P, P, i32, i32, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -611,6 +612,14 @@ def tsv_debug_race_E(m_begin: int, n: int, out=None, device="cuda"):
         out = torch.empty(n, dtype=torch.float32, device=device)
     _check(_lib.tsv_debug_race_E(int(m_begin), int(n), _ptr(out), _stream(None)))
     return out
+
+
+def tsv_debug_race_row(w: torch.Tensor, words: torch.Tensor, prune: bool = True) -> int:
+    """Packed race key of one row with injected Philox words (diagnostics)."""
+    out = torch.zeros(1, dtype=torch.int64, device=w.device)
+    _check(_lib.tsv_debug_race_row(_ptr(w), _ptr(words), int(w.numel()), 1 if prune else 0, _ptr(out),
+                                   _stream(None)))
+    return int(out.item()) & 0xFFFFFFFFFFFFFFFF
 
 
 def tsv_debug_philox(ctr: torch.Tensor, key: torch.Tensor, race_variant: bool = False):

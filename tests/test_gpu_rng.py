@@ -13,6 +13,8 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
+DEV = "cuda"
+
 
 @pytest.fixture(scope="module")
 def tsv():
@@ -49,3 +51,67 @@ def test_device_philox_kats_and_random(tsv, race_variant):
     got = got.cpu().numpy().view(np.uint32).reshape(-1, 4)
     for t in range(0, 4096, 97):
         assert (got[t] == oracle.philox4x32_10(ctrs[t], key)).all()
+
+
+# ------------------------------------------------------------------ race logic with injected words
+def _race_oracle(w, words):
+    """Oracle token (k = 0 bonus row = w, injected E from the words) and its exact score bits."""
+    E = _E_TABLE()[words & 0x7FFFFF]
+    na, out, st = oracle.verify(w[None, :].astype(np.float32), None, np.array([0, 1], np.int32),
+                                np.zeros(0, np.int32), np.zeros(1, np.uint32), 0, 0, 0,
+                                inj_E=E[None, :].astype(np.float32))
+    t = int(out[0, 0])
+    score = np.float32(np.float32(w[t]) / E[t]).view(np.uint32) if t >= 0 else None
+    return t, score
+
+
+_EC = []
+
+
+def _E_TABLE():
+    if not _EC:
+        _EC.append(oracle.E_table())
+    return _EC[0]
+
+
+def _gpu_race(tsv, w, words, prune=True):
+    key = tsv.tsv_debug_race_row(torch.tensor(w, dtype=torch.float32, device=DEV),
+                                 torch.tensor(words.view(np.int32), device=DEV), prune)
+    if key == 0:
+        return -1, None
+    return 0xFFFFFFFF - (key & 0xFFFFFFFF), np.uint32(key >> 32)
+
+
+def test_race_logic_with_adversarial_words(tsv):
+    rng = np.random.Generator(np.random.PCG64(123))
+    cases = []
+    V = 1000
+    cases.append((np.full(V, 0.001, np.float32), np.full(V, 0x12345678, np.uint32)))      # all tied -> index 0
+    w = rng.random(V).astype(np.float32)
+    x = rng.integers(0, 2 ** 32, V, dtype=np.uint64).astype(np.uint32)
+    s = w / _E_TABLE()[x & 0x7FFFFF]
+    top = int(np.argmax(s))
+    w2, x2 = w.copy(), x.copy()
+    w2[3], x2[3] = w[top], x[top]                                                         # exact tie at a lower index
+    cases.append((w2, x2))
+    cases.append((w, x))
+    xe = x.copy()
+    xe[::7] = 0x007FFFFF                                                                   # u -> 1: E tiny, scores huge
+    xe[1::7] = 0                                                                           # u -> 2^-24: E large
+    cases.append((w, xe))
+    wz = w.copy()
+    wz[rng.random(V) < 0.5] = 0.0
+    wz[rng.random(V) < 0.2] = -1.0                                                         # non-positive: never win
+    wz[rng.random(V) < 0.05] = np.nan
+    cases.append((wz, x))
+    cases.append((np.full(V, 1e-40, np.float32), x))                                      # denormal weights
+    cases.append((np.zeros(V, np.float32), x))                                            # nothing positive
+    big = (rng.zipf(1.2, 100003) * 1e-6).astype(np.float32)
+    cases.append((big, rng.integers(0, 2 ** 32, 100003, dtype=np.uint64).astype(np.uint32)))
+    for n, (w, x) in enumerate(cases):
+        want_t, want_s = _race_oracle(w, x)
+        for prune in (True, False):
+            got_t, got_s = _gpu_race(tsv, w, x, prune)
+            assert got_t == want_t, (n, prune, got_t, want_t)
+            if want_t >= 0:
+                assert got_s == want_s, (n, prune)
