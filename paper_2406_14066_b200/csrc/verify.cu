@@ -6,19 +6,24 @@
 //
 //  1. verify_scan_kernel: one warp per request.  Acceptance test with first-rejection
 //     scan (lane j < k_i gathers p_j[x_j], q_j[x_j], draws u_acc, one ballot) -> m_i.
-//     Writes a 32-byte ReqMeta per request; bad requests are emitted (-1) right here.
-//  2. verify_race_kernel: warp-independent.  Work item = (request, 2048-column chunk) of
-//     the selected row [lazy] or (request, position, chunk) of every row [vocab-shard
-//     partial], interleaved over all warps of the grid.  Each warp streams its chunk of p
-//     -- and of q on a rejection -- with 128-bit loads into registers (2-deep prefetch),
-//     one specialised Philox4x32-10 call per float4, the provably conservative prune test
-//      that skips the exact double-log + IEEE-division score of elements
-//     that cannot reach the best score seen, deferred exact evaluation of survivors, and
-//     a packed (score, ~index) u64 key per item, stored without atomics.  No shared
-//     memory, no barriers, no inter-warp synchronisation.
-//  3. verify_emit_kernel: one warp per request (or p row in shard mode) reduces the
-//     chunk keys (max), falls back to the p_m race when the residual was identically zero
-//     (R5), and emits out_tokens / num_accepted (or the shard tuple).
+//     Writes a 32-byte ReqMeta per request and m_i; bad requests are emitted (-1) here.
+//  2. verify_race_kernel: warp-independent.  Work item = (request, column chunk; the
+//     default chunk gives about one item per resident warp) of the selected row [lazy] or
+//     (request, position, chunk) of every row [vocab-shard partial], request-minor over
+//     all warps of the grid.  Each warp streams its chunk of p -- and of q on a rejection --
+//     two 128-bit loads per lane per step, one specialised Philox4x32-10 call per float4,
+//     the provably conservative prune test that skips the exact
+//     double-log + IEEE-division score of elements that cannot reach the best score seen,
+//     deferred exact evaluation of survivors, and a packed (score, ~index) u64 key per
+//     row combined with red.max.  No shared memory, no barriers.
+//  3. verify_emit_kernel: one warp per request (or p row in shard mode) reads the row key,
+//     falls back to the p_m race when the residual was identically zero (R5), and emits
+//     out_tokens / num_accepted (or the shard tuple); optionally one extra CTA runs the
+//     alpha update.
+// Also here: the lazy two-round vocab sharding kernels (flags / meta / keys / emit), the
+// greedy verify (dense row argmax + first-mismatch emit), the fused softmax-from-logits
+// verify (online-softmax partials + logits scan; the race and emit take a LOGITS flag),
+// the standalone softmax rows, and the injected-word race diagnostic.
 #include <stdio.h>
 
 #include <algorithm>
