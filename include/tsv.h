@@ -153,6 +153,12 @@ typedef struct tsv_verify_args {
 
 #define TSV_VERIFY_NO_PRUNE 1     /* evaluate every race element exactly (test)     */
 #define TSV_VERIFY_SHARD_DENSE 2  /* tsv_verify_accept_sharded: one-round dense mode  */
+#define TSV_VERIFY_RACE_ONLY 4    /* measurement only (tsv_verify_accept): launch the */
+                                  /* race kernel alone over the workspace left by a  */
+                                  /* previous call with identical arguments; the race */
+                                  /* max-combines into the same row keys, so outputs  */
+                                  /* are unchanged.  bench.py times the dominant     */
+                                  /* kernel with it.                                  */
 
 /* Workspace: device scratch for per-request scan results and per-chunk race
  * keys (size from tsv_verify_workspace_size; no initialisation needed).  One

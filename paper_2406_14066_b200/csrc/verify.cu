@@ -228,6 +228,16 @@ __device__ __forceinline__ void emit(const RaceParams& P, int32_t i, int32_t qba
     if (lane == 0) P.num_accepted[i] = m;
 }
 
+// The scan's share of the emit (lazy modes): lanes j < m write the accepted drafts x_j
+// (already in the lane's register), lanes m < j <= k_max the -1 padding.  Slot m (the
+// correction / bonus token t) is left to the emit kernel, which then needs one load round
+// trip (meta + row key) and one store.
+__device__ __forceinline__ void emit_prefix(const RaceParams& P, int32_t i, int32_t m, int32_t x) {
+    const int lane = threadIdx.x & 31;
+    if (lane <= P.k_max && lane != m)
+        P.out_tokens[static_cast<int64_t>(i) * (P.k_max + 1) + lane] = lane < m ? x : -1;
+}
+
 // ------------------------------------------------------------------ 1. acceptance scan
 // One warp per request (R1-R4).  Lane j < k tests draft j if this shard owns x_j (the
 // lazy mode's shard is the whole vocabulary).  Lazy: invalid requests are emitted here.
@@ -292,7 +302,8 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     }
     if (MODE == kLazy) {
         if (lane == 0) P.num_accepted[i] = m;  // final here (-1: bad request); the update may read it
-        if (ok != 1) {
+        if (ok == 1) emit_prefix(P, i, m, x);
+        else {
             emit(P, i, 0, -1, -1);
             if (lane == 0) report(P.devstatus, ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
         }
@@ -485,17 +496,21 @@ template <int MODE, bool PRUNE, bool LOGITS = false>
 __device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
     const int lane = threadIdx.x & 31;
     if (unit >= P.B) return;
+    // lazy: the row key is loaded next to the meta (one round trip)
+    uint64_t key = (MODE == kLazy) ? P.rowkey[unit] : 0ull;
     const ReqMeta rm = P.meta[unit];
     if (rm.ok != 1) return;  // lazy: emitted by the scan kernel; shard: flagged by the combine
     if (MODE == kLazy) {
-        uint64_t key = P.rowkey[unit];
         if (key == 0 && rm.m < rm.k) {  // R5: residual identically zero -> race over p_m
             const float4 ls = LOGITS ? P.lstats[unit] : make_float4(0.f, 0.f, 0.f, 0.f);
             key = warp_race_row<PRUNE, LOGITS>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid,
                                                ls.x, ls.y);
         }
-        emit(P, unit, rm.qbase, rm.m, key ? key_index(key) : -1);
-        if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+        // drafts x_0..x_{m-1}, the padding and num_accepted were written by the scan kernel
+        if (lane == 0) {
+            P.out_tokens[static_cast<int64_t>(unit) * (P.k_max + 1) + rm.m] = key ? key_index(key) : -1;
+            if (!key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+        }
     } else {
         for (int32_t j = 0; j <= rm.k; ++j) {
             const int32_t row = rm.r0 + j;
@@ -970,7 +985,8 @@ __global__ void __launch_bounds__(256) verify_logit_scan_kernel(const RaceParams
         P.rowkey[i] = 0ull;
         P.num_accepted[i] = m;
     }
-    if (ok != 1) {
+    if (ok == 1) emit_prefix(P, i, m, x);
+    else {
         emit(P, i, 0, -1, -1);
         if (lane == 0) report(P.devstatus, ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
     }
@@ -1125,13 +1141,16 @@ static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
 
 template <int MODE>
 static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_t st, const UpdateArgs* ua = nullptr) {
+    const bool race_only = (a->flags & TSV_VERIFY_RACE_ONLY) != 0;  // measurement of the dominant kernel
     const unsigned scan_blocks = static_cast<unsigned>((a->B + 7) / 8);
-    TSV_CUDA(launch_pdl(verify_scan_kernel<MODE>, dim3(scan_blocks), dim3(256), 0, st, P), "verify_scan_kernel launch");
+    if (!race_only)
+        TSV_CUDA(launch_pdl(verify_scan_kernel<MODE>, dim3(scan_blocks), dim3(256), 0, st, P), "verify_scan_kernel launch");
     const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
     tsv_status rs;
     if (a->q) rs = prune ? launch_race<MODE, true, true>(P, st) : launch_race<MODE, true, false>(P, st);
     else rs = prune ? launch_race<MODE, false, true>(P, st) : launch_race<MODE, false, false>(P, st);
     TSV_TRY(rs);
+    if (race_only) return TSV_OK;
     const unsigned emit_blocks = static_cast<unsigned>((a->B + 7) / 8) + (ua ? 1u : 0u);
     const UpdateArgs none = {};
     cudaError_t e;
