@@ -59,6 +59,22 @@ def parse():
     return ap.parse_args()
 
 
+# Test mode for the N > 1 host path on a one-GPU box: TSV_BENCH_SHARED_GPU=1 puts every rank on
+# cuda:0 and uses the gloo backend (NCCL refuses two ranks on one device).  Not a measurement.
+SHARED_GPU = os.environ.get("TSV_BENCH_SHARED_GPU") == "1"
+
+
+def _dev_index(local_rank):
+    return 0 if SHARED_GPU else local_rank
+
+
+def _barrier(dist, local_rank):
+    if SHARED_GPU:
+        dist.barrier()
+    else:
+        dist.barrier(device_ids=[local_rank])
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -161,7 +177,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2406_14066_b200 import tsv
     from paper_2406_14066_b200.step import SpecStep, StepInputs
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", _dev_index(local_rank))
     torch.cuda.set_device(dev)
     R = max(1, args.sets)
     seed = synth.DEFAULT_SEED
@@ -182,7 +198,7 @@ def run_ours(args, rank, world, local_rank):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            _barrier(dist, local_rank)
 
     # ---- graphs: warm-up and timed steps with distinct Philox step counters
     W, K = max(3, args.warmup), args.steps
@@ -436,7 +452,7 @@ def run_config4(args, rank, world, local_rank):
     from paper_2406_14066_b200 import dist as pdist
     from paper_2406_14066_b200 import tsv
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", _dev_index(local_rank))
     torch.cuda.set_device(dev)
     R = max(2, args.sets)
     seed = synth.DEFAULT_SEED
@@ -488,7 +504,7 @@ def run_config4(args, rank, world, local_rank):
     def barrier():
         if world > 1:
             import torch.distributed as dist
-            dist.barrier(device_ids=[local_rank])
+            _barrier(dist, local_rank)
 
     barrier()
     torch.cuda.synchronize()
@@ -550,7 +566,7 @@ def run_greedy(args, rank, world, local_rank):
     from paper_2406_14066_b200 import dist as pdist
     from paper_2406_14066_b200 import tsv
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", _dev_index(local_rank))
     torch.cuda.set_device(dev)
     R = max(2, args.sets)
     sets, footprint = [], 0
@@ -598,7 +614,7 @@ def run_greedy(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.barrier(device_ids=[local_rank])
+        _barrier(dist, local_rank)
     torch.cuda.synchronize()
     with sampler:
         e0.record(stream)
@@ -651,7 +667,7 @@ def run_logits(args, rank, world, local_rank):
     from paper_2406_14066_b200 import dist as pdist
     from paper_2406_14066_b200 import tsv
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", _dev_index(local_rank))
     torch.cuda.set_device(dev)
     R = max(2, args.sets)
     seed = synth.DEFAULT_SEED
@@ -692,7 +708,7 @@ def run_logits(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.barrier(device_ids=[local_rank])
+        _barrier(dist, local_rank)
     torch.cuda.synchronize()
     with sampler:
         e0.record(stream)
@@ -749,7 +765,7 @@ def run_config5(args, rank, world, local_rank):
     from paper_2406_14066_b200 import dist as pdist
     from paper_2406_14066_b200 import tsv
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", _dev_index(local_rank))
     torch.cuda.set_device(dev)
     alphas = (0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9)
     ctxs, caps, offs, al = [], [], [0], []
@@ -795,7 +811,7 @@ def run_config5(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.barrier(device_ids=[local_rank])
+        _barrier(dist, local_rank)
     torch.cuda.synchronize()
     with sampler:
         e0.record(stream)
@@ -921,8 +937,11 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(_dev_index(local_rank))
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.workload in ("config4", "greedy", "logits", "config5"):
         fn = {"config4": run_config4, "greedy": run_greedy, "logits": run_logits, "config5": run_config5}[args.workload]
         line = fn(args, rank, world, local_rank)

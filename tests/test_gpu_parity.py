@@ -842,6 +842,19 @@ def test_random_shape_sweep(tsv):
         assert_verify_parity(tsv, vb, seed=seed, step=step, chunk=chunk)
 
 
+# Shapes around the work-item and grid boundaries of the lazy race at the default chunk:
+# one request, V at and around powers of two, V not a multiple of 4, more requests than SMs,
+# Llama-3 vocabulary, thousands of short rows; pruned and unpruned.
+@pytest.mark.parametrize("B,V,k_max,dense", [
+    (1, 5, 3, True), (1, 8192, 8, True), (2, 8193, 8, False), (3, 16385, 4, True), (147, 100, 2, True),
+    (149, 24577, 8, True), (300, 8191, 6, False), (257, 128256, 3, True), (4096, 64, 2, True),
+    (4097, 64, 2, True)])
+def test_race_shapes(tsv, B, V, k_max, dense):
+    vb = synth.make_verify_batch(B=B, V=V, k_max=k_max, lam=0.7, seed=B * 131 + V, dense_q=dense)
+    assert_verify_parity(tsv, vb, seed=B + V, step=B)
+    assert_verify_parity(tsv, vb, seed=B + V, step=B, flags=tsv.VERIFY_NO_PRUNE)
+
+
 def test_choose_k_batched_config5_sweep(tsv):
     # BASELINE config 5: batch 1-512 x alpha 0.3-0.9, K = 8, both policies, one launch per sweep
     for target, draft in PROFILES:
