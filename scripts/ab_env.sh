@@ -8,6 +8,6 @@ for e in "$@"; do
   n=$((n+1))
   for rep in 1 2; do
     env $e timeout 300 python bench.py --steps 256 --warmup 16 --no-cpu-baseline --e2e-steps 0 ${AB_BENCH:-} > gpurun_out/abe_$n.json 2>gpurun_out/abe_$n.err || tail -3 gpurun_out/abe_$n.err
-    python -c "import json;d=json.load(open('gpurun_out/abe_$n.json'));print('[$e]', round(d['ms_per_step']*1e3,2),'us/step; verify', round(d['roofline']['launch_us'],2),'us frac',round(d['roofline']['frac'],3))"
+    python -c "import json;d=json.load(open('gpurun_out/abe_$n.json'));print('[$e]', round(d['ms_per_step']*1e3,2),'us/step; verify', round(d['roofline']['launch_us'],2),'us frac',round(d['roofline']['frac'],3), 'call', round(d['roofline'].get('verify_call',{}).get('launch_us',0),2))"
   done
 done
