@@ -836,6 +836,24 @@ __device__ __forceinline__ float from_ordered_bits(uint32_t k) {
 __device__ __forceinline__ float exp_arg(float z, float m, float inv_tau) {
     return __fmul_rn(__fsub_rn(z, m), inv_tau);
 }
+// Terms of the row sums only (never a probability): 2^(RN32(z - m) * RN32(log2(e) / tau)) by one
+// MUFU.EX2 (ex2.approx, relative error ~2^-22, the same order as expf's 2 ulp; results below
+// 2^-126 flush to 0, which a sum >= 1 in binary64 cannot see).  The probabilities themselves
+// (to_prob: scan gathers, the race, softmax rows) keep the accurate expf.
+#ifndef TSV_STATS_FAST_EXP
+#define TSV_STATS_FAST_EXP 1
+#endif
+__device__ __forceinline__ float sum_term(float z, float m, float inv_tau, float l2e_tau) {
+#if TSV_STATS_FAST_EXP
+    (void)inv_tau;
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fmul_rn(__fsub_rn(z, m), l2e_tau)));
+    return r;
+#else
+    (void)l2e_tau;
+    return expf(exp_arg(z, m, inv_tau));
+#endif
+}
 
 // Pass 1: per (row, chunk) item, a warp-uniform running max m (raised at most once per step
 // for all lanes -- no divergent rescaling) and per-lane sums of expf((z - m) / tau): four
@@ -854,6 +872,7 @@ __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel
     const int32_t rq = (P.q != nullptr) ? rp - P.B : 0;
     const int64_t n_items = static_cast<int64_t>(rp + rq) * P.n_chunks;
     const float it = P.inv_tau;
+    const float l2e = __fmul_rn(1.4426950408889634f, it);  // RN32(log2(e) / tau)
     for (int64_t item = warp_id; item < n_items; item += n_warps) {
         const int32_t r = static_cast<int32_t>(item % (rp + rq));
         const int32_t c = static_cast<int32_t>(item / (rp + rq));
@@ -899,7 +918,7 @@ __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel
             for (int h = 0; h < 2; ++h) {
                 float x[4];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) x[t] = e[4 * h + t] > -INFINITY ? expf(exp_arg(e[4 * h + t], m, it)) : 0.0f;
+                for (int t = 0; t < 4; ++t) x[t] = e[4 * h + t] > -INFINITY ? sum_term(e[4 * h + t], m, it, l2e) : 0.0f;
                 acc = __fadd_rn(acc, __fadd_rn(__fadd_rn(x[0], x[1]), __fadd_rn(x[2], x[3])));
             }
             s += static_cast<double>(acc);
@@ -1011,9 +1030,10 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* z, int64
     float M = s_m[0];
 #pragma unroll
     for (int w = 1; w < 8; ++w) M = fmaxf(M, s_m[w]);
-    double s = 0.0;
+    double s = 0.0;  // the row sum with the terms of the verify's statistics pass (sum_term)
+    const float l2e = __fmul_rn(1.4426950408889634f, inv_tau);
     for (int32_t v = threadIdx.x; v < V; v += 256)
-        s += static_cast<double>(expf(__fmul_rn(__fsub_rn(zr[v], M), inv_tau)));
+        if (zr[v] > -INFINITY) s += static_cast<double>(sum_term(zr[v], M, inv_tau, l2e));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
     if (lane == 0) s_s[warp] = s;
