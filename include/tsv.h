@@ -69,6 +69,8 @@ typedef enum {
 #define TSV_DEVSTATUS_BAD_TOKEN 1u  /* draft token outside [0, vocab_global)      */
 #define TSV_DEVSTATUS_BAD_K 2u      /* k_i < 0 or k_i > k_max (ragged offsets)    */
 #define TSV_DEVSTATUS_NO_WEIGHT 4u  /* selected p row has no positive entry        */
+#define TSV_DEVSTATUS_P2P_TIMEOUT 8u /* a peer-memory exchange wait gave up (a peer
+                                        never arrived); outputs are not valid      */
 
 TSV_API const char* tsv_last_error(void);
 TSV_API int tsv_abi_version(void);
@@ -240,6 +242,40 @@ TSV_API tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint64_
                                          void* stream);
 TSV_API tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_t* masks, const uint64_t* keys,
                                          void* stream);
+
+/* Lazy two-round vocab sharding over NVLink peer memory:
+ * the same computation as tsv_verify_accept_sharded's lazy mode, with both exchanges
+ * done by the producing kernels themselves instead of NCCL all-reduces.  Every rank
+ * owns one symmetric buffer (tsv_p2p_alloc, zero-filled; B_max requests), mapped
+ * into every peer (tsv_p2p_open of the 64-byte CUDA IPC handle; the caller exchanges
+ * handles, e.g. torch.distributed all_gather_object).  Round 1: the flags kernel
+ * stores this rank's mask words into slot [rank] of every peer's buffer and its last
+ * CTA publishes the call's epoch in every peer's flag [0][rank] (release, system
+ * scope); the meta kernel of each rank waits for all G flags (acquire) and sums the G
+ * slots (disjoint owners: the sum is the OR).  Round 2 the same for the (key,
+ * fallback key) pairs after the race, combined by max in the emit kernel.  Slots
+ * alternate by epoch parity.  A wait that never completes (a peer died) gives up
+ * after seconds and sets TSV_DEVSTATUS_P2P_TIMEOUT instead of hanging.
+ *  tsv_p2p_init: bufs[g] = rank g's buffer as mapped in this process (bufs[rank]
+ *    local), world <= TSV_P2P_MAX_WORLD, B <= B_max in every call; the handle keeps
+ *    the call epoch (all ranks must make the same sequence of calls).
+ *  tsv_verify_accept_sharded_p2p: the whole step on `stream` (flags -> meta -> race
+ *    -> keys -> emit, five kernels, no host synchronisation); needs the verify
+ *    workspace (tsv_verify_workspace_size).
+ *  tsv_verify_shard_p2p_phase: phase 0 (new epoch, flags + push), 1 (wait, meta,
+ *    race, keys + push), 2 (wait, emit) separately: lets one process drive G
+ *    loopback ranks on one device (all phase 0, then all 1, then all 2). */
+#define TSV_P2P_MAX_WORLD 8
+typedef struct tsv_p2p tsv_p2p;
+TSV_API tsv_status tsv_p2p_buffer_size(int32_t B_max, size_t* bytes);
+TSV_API tsv_status tsv_p2p_alloc(int32_t B_max, void** buf_out, void* ipc_handle_out /* 64 B, nullable */);
+TSV_API tsv_status tsv_p2p_free(void* buf);
+TSV_API tsv_status tsv_p2p_open(const void* ipc_handle /* 64 B */, void** buf_out);
+TSV_API tsv_status tsv_p2p_close(void* buf);
+TSV_API tsv_status tsv_p2p_init(tsv_p2p** out, int32_t rank, int32_t world, int32_t B_max, void* const* bufs);
+TSV_API tsv_status tsv_p2p_destroy(tsv_p2p* p);
+TSV_API tsv_status tsv_verify_accept_sharded_p2p(const tsv_verify_args* a, tsv_p2p* p, void* stream);
+TSV_API tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p2p* p, int32_t phase, void* stream);
 
 /* --------------------------------------------------------------------------
  * Goodput k selection: ArgMaxGoodput (Listing 2) over

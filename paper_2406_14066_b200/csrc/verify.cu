@@ -25,6 +25,7 @@
 // verify (online-softmax partials + logits scan; the race and emit take a LOGITS flag),
 // the standalone softmax rows, and the injected-word race diagnostic.
 #include <stdio.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -594,11 +595,8 @@ __global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_
 // Round 2 (race): from the summed masks every shard forms the same m_i, races row m_i over
 // its columns and publishes (local key, local fallback key); the element-wise max over
 // shards is the unsharded row key.  Emit: from summed masks + maxed keys.
-__global__ void __launch_bounds__(256) verify_shard_flags_kernel(const RaceParams P, unsigned long long* masks) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= P.B) return;
+// Warp-collective: the request's mask word (owner bits << 32 | accept bits) on this shard.
+__device__ __forceinline__ unsigned long long shard_flags_mask(const RaceParams& P, int32_t i) {
     const int lane = threadIdx.x & 31;
     const int32_t r0 = P.row_offsets[i];
     const int32_t r1 = P.row_offsets[i + 1];
@@ -622,7 +620,16 @@ __global__ void __launch_bounds__(256) verify_shard_flags_kernel(const RaceParam
     }
     const uint32_t accm = __ballot_sync(0xFFFFFFFFu, acc);
     const uint32_t ownm = __ballot_sync(0xFFFFFFFFu, own);
-    if (lane == 0) masks[i] = (static_cast<unsigned long long>(ownm) << 32) | accm;
+    return (static_cast<unsigned long long>(ownm) << 32) | accm;
+}
+
+__global__ void __launch_bounds__(256) verify_shard_flags_kernel(const RaceParams P, unsigned long long* masks) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const unsigned long long mask = shard_flags_mask(P, i);
+    if ((threadIdx.x & 31) == 0) masks[i] = mask;
 }
 
 // The request's ReqMeta from the summed mask word (every lane; identical on every shard).
@@ -707,6 +714,163 @@ __global__ void __launch_bounds__(256) verify_shard_emit_kernel(const RaceParams
     }
     uint64_t key = keys[2 * i];
     if (key == 0 && rm.m < rm.k) key = keys[2 * i + 1];
+    emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
+    if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+}
+
+// ------------------------------------------------ vocab sharding over peer memory (NEXT 3)
+// The lazy two rounds with the two exchanges done by the producing kernels themselves over
+// NVLink peer memory instead of NCCL all-reduces.  Every rank owns
+// one symmetric buffer (P2PLayout), mapped into every peer (CUDA IPC).  Round r: the
+// producing kernel (flags, keys) stores this rank's words into slot [rank] of every peer's
+// buffer, fences at system scope, and its last CTA publishes the call's epoch in flag
+// [r][rank] of every peer (st.release.sys); the consuming kernel (meta, emit) waits until
+// its own buffer's flags [r][0..G) all hold the epoch (ld.acquire.sys) and combines the G
+// slots locally -- sum of the disjoint mask words, max of the packed keys.  Slots alternate
+// by epoch parity, so a rank one call ahead never overwrites words a peer still reads.
+// A wait gives up after 2^24 sleeps of >= 256 ns (seconds) and sets TSV_DEVSTATUS_P2P_TIMEOUT.
+struct P2PView {
+    unsigned char* buf[TSV_P2P_MAX_WORLD];  // rank g's symmetric buffer as mapped in this process
+    int32_t rank, G, B_max;
+    uint32_t epoch;
+};
+constexpr size_t kP2PHdr = 256;  // u32 flags [2][MAX_WORLD] at 0, u32 counters [2] at 128
+__host__ __device__ constexpr size_t p2p_masks_bytes(int32_t B_max) {
+    return 2ull * TSV_P2P_MAX_WORLD * static_cast<size_t>(B_max) * 8ull;
+}
+__host__ __device__ constexpr size_t p2p_buffer_bytes(int32_t B_max) {
+    return kP2PHdr + 3ull * p2p_masks_bytes(B_max);  // masks [2][W][B] + keys [2][W][2B]
+}
+__device__ __forceinline__ uint32_t* p2p_flag(const P2PView& V, int32_t owner, int32_t round, int32_t from) {
+    return reinterpret_cast<uint32_t*>(V.buf[owner]) + round * TSV_P2P_MAX_WORLD + from;
+}
+__device__ __forceinline__ uint32_t* p2p_counter(const P2PView& V, int32_t round) {
+    return reinterpret_cast<uint32_t*>(V.buf[V.rank] + 128) + round;
+}
+__device__ __forceinline__ unsigned long long* p2p_masks(const P2PView& V, int32_t owner, int32_t slot) {
+    const int32_t par = static_cast<int32_t>(V.epoch & 1u);
+    return reinterpret_cast<unsigned long long*>(V.buf[owner] + kP2PHdr) +
+           (static_cast<size_t>(par) * TSV_P2P_MAX_WORLD + slot) * V.B_max;
+}
+__device__ __forceinline__ unsigned long long* p2p_keys(const P2PView& V, int32_t owner, int32_t slot) {
+    const int32_t par = static_cast<int32_t>(V.epoch & 1u);
+    return reinterpret_cast<unsigned long long*>(V.buf[owner] + kP2PHdr + p2p_masks_bytes(V.B_max)) +
+           (static_cast<size_t>(par) * TSV_P2P_MAX_WORLD + slot) * 2 * V.B_max;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// After this CTA's pushes (each pushing thread fenced at system scope): the last CTA of the
+// grid publishes the epoch to every peer.
+__device__ __forceinline__ void p2p_signal(const P2PView& V, int32_t round) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const uint32_t prev = atomicAdd(p2p_counter(V, round), 1u);
+        if (prev == gridDim.x - 1) {
+            atomicExch(p2p_counter(V, round), 0u);  // the next call's kernels run after this one
+            __threadfence_system();
+            for (int32_t g = 0; g < V.G; ++g) st_release_sys(p2p_flag(V, g, round, V.rank), V.epoch);
+        }
+    }
+}
+
+// Every CTA: wait until all G ranks published this epoch for `round` in our own buffer.
+__device__ __forceinline__ void p2p_wait(const P2PView& V, int32_t round, int32_t* devstatus) {
+    if (threadIdx.x < static_cast<unsigned>(V.G)) {
+        const uint32_t* f = p2p_flag(V, V.rank, round, threadIdx.x);
+        uint32_t n = 0;
+        while (ld_acquire_sys(f) != V.epoch) {
+            __nanosleep(256);
+            if (++n == (1u << 24)) {  // ~4+ s: a peer never arrived
+                report(devstatus, TSV_DEVSTATUS_P2P_TIMEOUT);
+                break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams P, const P2PView V) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i < P.B) {
+        const unsigned long long mask = shard_flags_mask(P, i);
+        const int lane = threadIdx.x & 31;
+        if (lane < V.G) p2p_masks(V, lane, V.rank)[i] = mask;  // lane g stores into rank g's buffer
+        if (lane < V.G) __threadfence_system();
+    }
+    p2p_signal(V, 0);
+}
+
+__global__ void __launch_bounds__(256) verify_p2p_meta_kernel(const RaceParams P, const P2PView V) {
+    pdl_wait();
+    pdl_launch_dependents();
+    p2p_wait(V, 0, P.devstatus);
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    unsigned long long mask = 0;
+    for (int32_t g = 0; g < V.G; ++g) mask += p2p_masks(V, V.rank, g)[i];  // disjoint owners: sum = OR
+    const ReqMeta rm = shard_meta_from_masks(P, i, mask);
+    if ((threadIdx.x & 31) == 0) {
+        P.meta[i] = rm;
+        P.rowT[i] = 0u;
+        P.rowkey[i] = 0ull;
+    }
+}
+
+template <bool PRUNE>
+__global__ void __launch_bounds__(256) verify_p2p_keys_kernel(const RaceParams P, const P2PView V) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i < P.B) {
+        const int lane = threadIdx.x & 31;
+        const ReqMeta rm = P.meta[i];
+        uint64_t key = 0, fb = 0;
+        if (rm.ok == 1) {
+            key = P.rowkey[i];
+            if (key == 0 && rm.m < rm.k)  // this shard's residual is zero: its share of the R5 fallback
+                fb = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
+        }
+        if (lane < V.G) {
+            unsigned long long* d = p2p_keys(V, lane, V.rank);
+            d[2 * i] = key;
+            d[2 * i + 1] = fb;
+            __threadfence_system();
+        }
+    }
+    p2p_signal(V, 1);
+}
+
+__global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P, const P2PView V) {
+    pdl_wait();
+    pdl_launch_dependents();
+    p2p_wait(V, 1, P.devstatus);
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (i >= P.B) return;
+    const int lane = threadIdx.x & 31;
+    const ReqMeta rm = P.meta[i];  // written by this rank's meta kernel (same m_i on every rank)
+    if (rm.ok != 1) {
+        emit(P, i, 0, -1, -1);
+        if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
+        return;
+    }
+    uint64_t key = 0, fb = 0;
+    for (int32_t g = 0; g < V.G; ++g) {
+        const unsigned long long* s = p2p_keys(V, V.rank, g);
+        key = s[2 * i] > key ? s[2 * i] : key;
+        fb = s[2 * i + 1] > fb ? s[2 * i + 1] : fb;
+    }
+    if (key == 0 && rm.m < rm.k) key = fb;
     emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
     if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
 }
@@ -1483,5 +1647,112 @@ extern "C" tsv_status tsv_debug_race_row(const float* w, const uint32_t* words, 
     if (prune) debug_race_row_kernel<true><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(w, words, V, k);
     else debug_race_row_kernel<false><<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(w, words, V, k);
     TSV_CUDA(cudaGetLastError(), "debug_race_row_kernel launch");
+    return TSV_OK;
+}
+
+// ------------------------------------------------------------ peer-memory vocab sharding (host)
+struct tsv_p2p {
+    tsv::P2PView view;
+};
+
+extern "C" tsv_status tsv_p2p_buffer_size(int32_t B_max, size_t* bytes) {
+    TSV_REQUIRE(bytes != nullptr && B_max >= 1, "tsv_p2p_buffer_size: bad arguments");
+    *bytes = tsv::p2p_buffer_bytes(B_max);
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_p2p_alloc(int32_t B_max, void** buf_out, void* ipc_handle_out) {
+    TSV_REQUIRE(buf_out != nullptr && B_max >= 1, "tsv_p2p_alloc: bad arguments");
+    TSV_TRY(check_device());
+    void* p = nullptr;
+    const size_t n = tsv::p2p_buffer_bytes(B_max);
+    TSV_CUDA(cudaMalloc(&p, n), "cudaMalloc (p2p buffer)");
+    TSV_CUDA(cudaMemset(p, 0, n), "cudaMemset (p2p buffer)");
+    if (ipc_handle_out) {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        TSV_CUDA(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
+        memcpy(ipc_handle_out, &h, sizeof(h));
+    }
+    *buf_out = p;
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_p2p_free(void* buf) {
+    if (buf) TSV_CUDA(cudaFree(buf), "cudaFree (p2p buffer)");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_p2p_open(const void* ipc_handle, void** buf_out) {
+    TSV_REQUIRE(ipc_handle && buf_out, "tsv_p2p_open: NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    TSV_CUDA(cudaIpcOpenMemHandle(buf_out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_p2p_close(void* buf) {
+    if (buf) TSV_CUDA(cudaIpcCloseMemHandle(buf), "cudaIpcCloseMemHandle");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_p2p_init(tsv_p2p** out, int32_t rank, int32_t world, int32_t B_max, void* const* bufs) {
+    TSV_REQUIRE(out && bufs, "tsv_p2p_init: NULL argument");
+    TSV_REQUIRE(world >= 1 && world <= TSV_P2P_MAX_WORLD && rank >= 0 && rank < world && B_max >= 1,
+                "tsv_p2p_init: rank %d / world %d / B_max %d invalid", rank, world, B_max);
+    auto* p = new tsv_p2p;
+    memset(&p->view, 0, sizeof(p->view));
+    for (int32_t g = 0; g < world; ++g) {
+        TSV_REQUIRE(bufs[g] != nullptr, "tsv_p2p_init: buffer of rank %d is NULL", g);
+        p->view.buf[g] = static_cast<unsigned char*>(bufs[g]);
+    }
+    p->view.rank = rank;
+    p->view.G = world;
+    p->view.B_max = B_max;
+    p->view.epoch = 0;
+    *out = p;
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_p2p_destroy(tsv_p2p* p) {
+    delete p;
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p2p* p, int32_t phase, void* stream) {
+    TSV_TRY(validate(a));
+    TSV_REQUIRE(p != nullptr, "tsv_verify_shard_p2p_phase: p2p handle is NULL");
+    TSV_REQUIRE(phase >= 0 && phase <= 2, "tsv_verify_shard_p2p_phase: phase %d", phase);
+    TSV_REQUIRE(a->B <= p->view.B_max, "tsv_verify_shard_p2p_phase: B %d > B_max %d", a->B, p->view.B_max);
+    TSV_TRY(check_device());
+    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+                "tsv_verify_shard_p2p_phase: workspace too small (%llu < %llu bytes)",
+                (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    if (phase == 0) ++p->view.epoch;  // every call goes through phase 0 first, on every rank
+    if (a->B == 0) return TSV_OK;     // (all ranks skip the exchange together)
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    RaceParams P = make_params(a);
+    const dim3 grid(static_cast<unsigned>((a->B + 7) / 8));
+    const P2PView V = p->view;
+    const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
+    if (phase == 0) {
+        TSV_CUDA(launch_pdl(verify_p2p_flags_kernel, grid, dim3(256), 0, st, P, V), "verify_p2p_flags_kernel launch");
+    } else if (phase == 1) {
+        TSV_CUDA(launch_pdl(verify_p2p_meta_kernel, grid, dim3(256), 0, st, P, V), "verify_p2p_meta_kernel launch");
+        tsv_status rs;
+        if (a->q) rs = prune ? launch_race<kLazy, true, true>(P, st) : launch_race<kLazy, true, false>(P, st);
+        else rs = prune ? launch_race<kLazy, false, true>(P, st) : launch_race<kLazy, false, false>(P, st);
+        TSV_TRY(rs);
+        TSV_CUDA(prune ? launch_pdl(verify_p2p_keys_kernel<true>, grid, dim3(256), 0, st, P, V)
+                       : launch_pdl(verify_p2p_keys_kernel<false>, grid, dim3(256), 0, st, P, V),
+                 "verify_p2p_keys_kernel launch");
+    } else {
+        TSV_CUDA(launch_pdl(verify_p2p_emit_kernel, grid, dim3(256), 0, st, P, V), "verify_p2p_emit_kernel launch");
+    }
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_verify_accept_sharded_p2p(const tsv_verify_args* a, tsv_p2p* p, void* stream) {
+    for (int32_t ph = 0; ph < 3; ++ph) TSV_TRY(tsv_verify_shard_p2p_phase(a, p, ph, stream));
     return TSV_OK;
 }

@@ -78,3 +78,16 @@ def broadcast_bytes(blob: bytes, src: int = 0) -> bytes:
     obj = [blob]
     dist.broadcast_object_list(obj, src=src)
     return obj[0]
+
+
+def exchange_handles(local: bytes, rank: int, world: int, group=None) -> list:
+    """Every rank's blob (e.g. the 64-byte CUDA IPC handle of its peer-memory buffer) in rank
+    order, via all_gather_object (any backend).  One rank: [local]."""
+    import torch.distributed as dist
+    if world <= 1 or not (dist.is_available() and dist.is_initialized()):
+        return [local]
+    out = [None] * world
+    dist.all_gather_object(out, local, group=group)
+    assert all(isinstance(b, bytes) and len(b) == len(local) for b in out), "handle exchange failed"
+    assert out[rank] == local
+    return out

@@ -45,6 +45,8 @@ EXPORTED = [
     "tsv_verify_shard_emit", "tsv_verify_greedy", "tsv_verify_logits_workspace_size",
     "tsv_verify_accept_logits", "tsv_softmax_rows", "tsv_fit_latency_model", "tsv_sim_target",
     "tsv_context_append", "tsv_goodput_choose_k_batched", "tsv_debug_race_row",
+    "tsv_p2p_buffer_size", "tsv_p2p_alloc", "tsv_p2p_free", "tsv_p2p_open", "tsv_p2p_close", "tsv_p2p_init",
+    "tsv_p2p_destroy", "tsv_verify_accept_sharded_p2p", "tsv_verify_shard_p2p_phase",
 ]
 
 
@@ -134,6 +136,15 @@ def _load() -> ctypes.CDLL:
         "tsv_goodput_choose_k_batched": ([P, P, P, P, i32, i32, i32, LatencyModel, LatencyModel, f64, i64,
                                           P, P, P, P], ctypes.c_int),
         "tsv_debug_race_row": ([P, P, i32, i32, P, P], ctypes.c_int),
+        "tsv_p2p_buffer_size": ([i32, ctypes.POINTER(sz)], ctypes.c_int),
+        "tsv_p2p_alloc": ([i32, ctypes.POINTER(P), P], ctypes.c_int),
+        "tsv_p2p_free": ([P], ctypes.c_int),
+        "tsv_p2p_open": ([P, ctypes.POINTER(P)], ctypes.c_int),
+        "tsv_p2p_close": ([P], ctypes.c_int),
+        "tsv_p2p_init": ([ctypes.POINTER(P), i32, i32, i32, P], ctypes.c_int),
+        "tsv_p2p_destroy": ([P], ctypes.c_int),
+        "tsv_verify_accept_sharded_p2p": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
+        "tsv_verify_shard_p2p_phase": ([ctypes.POINTER(VerifyArgs), P, i32, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -555,6 +566,88 @@ class Comm:
         if self.handle:
             _check(_lib.tsv_comm_destroy(self.handle))
             self.handle = None
+
+
+class P2PComm:
+    """Peer-memory exchange for the lazy vocab-sharded verify (tsv_verify_accept_sharded_p2p).
+
+    Every rank allocates its symmetric buffer in libtsv (cudaMalloc, zero-filled) and
+    exports its 64-byte CUDA IPC handle; the handles travel over torch.distributed
+    (all_gather_object) and each rank maps its peers' buffers (cudaIpcOpenMemHandle).
+    Host-side plumbing only: the exchange itself runs in the kernels."""
+
+    def __init__(self, rank: int, world: int, B_max: int, group=None):
+        import torch.distributed as dist
+        self.rank, self.world, self.B_max = int(rank), int(world), int(B_max)
+        own = ctypes.c_void_p()
+        hnd = (ctypes.c_uint8 * 64)()
+        _check(_lib.tsv_p2p_alloc(self.B_max, ctypes.byref(own), ctypes.cast(hnd, ctypes.c_void_p)))
+        self.own = own
+        from . import dist as pdist
+        handles = pdist.exchange_handles(bytes(hnd), self.rank, self.world, group)
+        self.opened = []
+        bufs = (ctypes.c_void_p * self.world)()
+        for g, h in enumerate(handles):
+            if g == self.rank:
+                bufs[g] = own.value
+                continue
+            raw = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+            ptr = ctypes.c_void_p()
+            _check(_lib.tsv_p2p_open(ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(ptr)))
+            self.opened.append(ptr)
+            bufs[g] = ptr.value
+        h = ctypes.c_void_p()
+        _check(_lib.tsv_p2p_init(ctypes.byref(h), self.rank, self.world, self.B_max,
+                                 ctypes.cast(bufs, ctypes.c_void_p)))
+        self.handle = h
+        if dist.is_initialized() and self.world > 1:
+            dist.barrier(group=group)  # every peer mapped before anyone's first store
+
+    def close(self):
+        if self.handle:
+            _check(_lib.tsv_p2p_destroy(self.handle))
+            self.handle = None
+        for p in self.opened:
+            _check(_lib.tsv_p2p_close(p))
+        self.opened = []
+        if self.own:
+            _check(_lib.tsv_p2p_free(self.own))
+            self.own = None
+
+
+class P2PLoopback:
+    """G virtual ranks on one device (tests): one local buffer per rank, every rank's peer table
+    holds all of them.  Drive with tsv_verify_shard_p2p_phase: all ranks phase 0, then 1, then 2."""
+
+    def __init__(self, world: int, B_max: int):
+        self.world, self.B_max = int(world), int(B_max)
+        self.bufs = []
+        for _ in range(self.world):
+            b = ctypes.c_void_p()
+            _check(_lib.tsv_p2p_alloc(self.B_max, ctypes.byref(b), None))
+            self.bufs.append(b)
+        table = (ctypes.c_void_p * self.world)(*[b.value for b in self.bufs])
+        self.handles = []
+        for g in range(self.world):
+            h = ctypes.c_void_p()
+            _check(_lib.tsv_p2p_init(ctypes.byref(h), g, self.world, self.B_max, ctypes.cast(table, ctypes.c_void_p)))
+            self.handles.append(h)
+
+    def close(self):
+        for h in self.handles:
+            _check(_lib.tsv_p2p_destroy(h))
+        for b in self.bufs:
+            _check(_lib.tsv_p2p_free(b))
+        self.handles, self.bufs = [], []
+
+
+def tsv_verify_accept_sharded_p2p(args: VerifyArgs, p2p, stream=None):
+    h = p2p.handle if hasattr(p2p, "handle") else p2p
+    _check(_lib.tsv_verify_accept_sharded_p2p(ctypes.byref(args), h, _stream(stream)))
+
+
+def tsv_verify_shard_p2p_phase(args: VerifyArgs, handle, phase: int, stream=None):
+    _check(_lib.tsv_verify_shard_p2p_phase(ctypes.byref(args), handle, int(phase), _stream(stream)))
 
 
 def tsv_verify_sharded_workspace_size(args: VerifyArgs, world: int) -> int:

@@ -1,7 +1,8 @@
 """Multi-rank host logic on CPU with the gloo backend (world_size 2).
 
 Covers what the N > 1 bench path does around the kernels: max-over-ranks timing,
-sum-over-ranks token counts, broadcast of the 128-byte NCCL unique id, and the
+sum-over-ranks token counts, broadcast of the 128-byte NCCL unique id, the all-gather of the 64-byte
+CUDA IPC handles of the peer-memory buffers, and the
 request / vocab partitions (global request ids => identical Philox streams)."""
 import os
 import socket
@@ -34,7 +35,8 @@ def _worker(rank, world, port, q):
         got = pdist.broadcast_bytes(blob)
         k = np.random.Generator(np.random.PCG64(3)).integers(0, 9, 256)
         parts = pdist.partition_requests(k, world)
-        q.put((rank, t, s, got, parts))
+        handles = pdist.exchange_handles(bytes([rank]) * 64, rank, world)  # peer-memory handle exchange
+        q.put((rank, t, s, got, parts, handles))
     finally:
         dist.destroy_process_group()
 
@@ -51,7 +53,8 @@ def test_two_rank_reductions_and_broadcast():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, t, s, got, parts in res:
+    for rank, t, s, got, parts, handles in res:
+        assert handles == [bytes([r]) * 64 for r in range(world)]
         assert t == 2.5
         assert s == 30.0
         assert got == bytes(range(128))

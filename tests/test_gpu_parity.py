@@ -295,6 +295,88 @@ def test_lazy_vocab_shard_one_hot_and_adversarial(tsv):
         assert (na == ona).all() and (out == oout).all()
 
 
+def p2p_shard_loopback(tsv, vb, G, seed, steps, chunk=0, B_max=None):
+    """Lazy two rounds over peer memory (tsv_verify_shard_p2p_phase), G virtual ranks on one device:
+    all ranks phase 0, then phase 1, then phase 2, for each step; every rank's outputs are returned."""
+    g = vb.to(DEV)
+    B, V = vb.B, vb.vocab
+    assert V % (4 * G) == 0
+    Vs = V // G
+    lb = tsv.P2PLoopback(G, B_max or max(B, 1))
+    res = []
+    try:
+        for step in steps:
+            outs, args = [], []
+            for s in range(G):
+                lo = s * Vs
+                na = torch.full((B,), -7, dtype=torch.int32, device=DEV)
+                out = torch.full((B, vb.k_max + 1), -7, dtype=torch.int32, device=DEV)
+                st = torch.zeros(1, dtype=torch.int32, device=DEV)
+                a = tsv.make_verify_args(g.p[:, lo:lo + Vs], None if g.q is None else g.q[:, lo:lo + Vs],
+                                         g.row_offsets, g.draft_tokens, g.request_ids, seed, step, vb.k_max,
+                                         na, out, device_status=st, vocab=Vs, vocab_offset=lo, vocab_global=V,
+                                         chunk=chunk)
+                ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+                a.workspace = ws.data_ptr()
+                a.workspace_bytes = ws.numel()
+                args.append((a, ws))
+                outs.append((na, out, st))
+            for phase in range(3):
+                for s in range(G):
+                    tsv.tsv_verify_shard_p2p_phase(args[s][0], lb.handles[s], phase)
+            torch.cuda.synchronize()
+            res.append([(_np(na), _np(out), int(st.item())) for na, out, st in outs])
+    finally:
+        lb.close()
+    return res
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_p2p_vocab_shard_loopback_equals_oracle(tsv, G):
+    # three consecutive calls: both slot parities and advancing epochs
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=26)
+    res = p2p_shard_loopback(tsv, vb, G, 21, [3, 4, 5], B_max=80)
+    for step, ranks in zip([3, 4, 5], res):
+        ona, oout, ost = oracle_verify(vb, 21, step)
+        for na, out, st in ranks:
+            assert (na == ona).all() and (out == oout).all() and st == ost
+
+
+def test_p2p_vocab_shard_one_hot_adversarial_llama3(tsv):
+    vb = synth.make_verify_batch(B=40, V=4096, k_max=6, lam=0.7, seed=27, dense_q=False)
+    ona, oout, _ = oracle_verify(vb, 2, 2)
+    for G in (2, 4):
+        for na, out, st in p2p_shard_loopback(tsv, vb, G, 2, [2], chunk=1024)[0]:
+            assert (na == ona).all() and (out == oout).all()
+    adv = _adversarial_batch()
+    adv.vocab = 256
+    adv.p = adv.p[:, :256].contiguous(); adv.q = adv.q[:, :256].contiguous()
+    adv.draft_tokens = adv.draft_tokens.clamp(max=255)
+    res = p2p_shard_loopback(tsv, adv, 4, 4, [0, 1, 2, 3])
+    for step, ranks in enumerate(res):
+        ona, oout, ost = oracle_verify(adv, 4, step)
+        for na, out, st in ranks:
+            assert (na == ona).all() and (out == oout).all() and st == ost
+    vb3 = synth.make_verify_batch(B=24, V=128256, k_max=8, lam=0.7, seed=28)  # Llama-3 vocabulary, G = 8
+    ona, oout, _ = oracle_verify(vb3, 9, 1)
+    for na, out, st in p2p_shard_loopback(tsv, vb3, 8, 9, [1])[0]:
+        assert (na == ona).all() and (out == oout).all()
+
+
+def test_p2p_vocab_shard_two_processes_ipc(tmp_path):
+    # the real multi-process path (CUDA IPC buffers, system-scope flags, epochs) with two ranks on the one
+    # GPU of this box (time-sliced contexts), over gloo for the handle exchange; each rank checks the oracle
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "tests", "p2p_worker.py")]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("P2P-OK") == 2, r.stdout[-3000:]
+
+
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_vocab_shard_loopback_equals_oracle(tsv, G):
     vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=17)
