@@ -55,13 +55,18 @@ def parse():
                          "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling); logits: the fused "
                          "softmax-from-logits verify (NEXT 1) on the config-2 batch given as logits; config5: the "
                          "goodput sweep (B 1-512 x alpha 0.3-0.9, K = 8) as one batched choose-k launch")
-    ap.add_argument("--shard-mode", default="lazy", choices=["lazy", "dense"], help="config4 sharding mode")
+    ap.add_argument("--shard-mode", default="lazy", choices=["lazy", "dense", "p2p"],
+                    help="config4 sharding mode: lazy two rounds over NCCL all-reduces, one-round dense over an "
+                         "NCCL all-gather, or the lazy two rounds over NVLink peer memory (no NCCL)")
     return ap.parse_args()
 
 
 # Test mode for the N > 1 host path on a one-GPU box: TSV_BENCH_SHARED_GPU=1 puts every rank on
 # cuda:0 and uses the gloo backend (NCCL refuses two ranks on one device).  Not a measurement.
 SHARED_GPU = os.environ.get("TSV_BENCH_SHARED_GPU") == "1"
+
+
+_JSON_OUT = sys.stdout
 
 
 def _dev_index(local_rank):
@@ -458,8 +463,13 @@ def run_config4(args, rank, world, local_rank):
     seed = synth.DEFAULT_SEED
     lo, Vs = pdist.vocab_shards(V4, world)[rank]
     hi = lo + Vs
-    comm = tsv.Comm(rank, world)
+    p2p = args.shard_mode == "p2p"
+    comm = tsv.P2PComm(rank, world, B_max=B) if p2p else tsv.Comm(rank, world)
     flags = tsv.VERIFY_SHARD_DENSE if args.shard_mode == "dense" else 0
+    entry = tsv.lib().tsv_verify_accept_sharded_p2p if p2p else tsv.lib().tsv_verify_accept_sharded
+
+    def run_sharded(a, stream=None):
+        tsv._check(entry(tsv.ctypes.byref(a), comm.handle, tsv._stream(stream)))
     na = torch.empty(B, dtype=torch.int32, device=dev)
     outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
     sets, footprint = [], 0
@@ -487,12 +497,12 @@ def run_config4(args, rank, world, local_rank):
     side = torch.cuda.Stream()
     side.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(side):
-        tsv.tsv_verify_accept_sharded(args_list[0], comm, stream=side)  # warm-up outside capture
+        run_sharded(args_list[0], stream=side)  # warm-up outside capture
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=side):
         for a in args_list:
-            tsv._check(tsv.lib().tsv_verify_accept_sharded(tsv.ctypes.byref(a), comm.handle, side.cuda_stream))
+            tsv._check(entry(tsv.ctypes.byref(a), comm.handle, side.cuda_stream))
     torch.cuda.synchronize()
     for _ in range((W + gl - 1) // gl):
         g.replay()
@@ -521,7 +531,7 @@ def run_config4(args, rank, world, local_rank):
     tok, vbytes = 0, 0.0
     for t in range(gl):
         a = args_list[t]
-        tsv.tsv_verify_accept_sharded(a, comm)
+        run_sharded(a)
         torch.cuda.synchronize()
         m = na.cpu().numpy()
         k = sets[t % R][0].k.cpu().numpy()
@@ -545,7 +555,8 @@ def run_config4(args, rank, world, local_rank):
                    "global_batch": B, "vocab": V4, "k_max": K_MAX, "parallelism": f"vocab-sharded x{world}",
                    "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank",
                    "graph_steps": gl},
-        "roofline": {"kernel": "tsv_verify_accept_sharded (per rank)", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": f"tsv_verify_accept_sharded{'_p2p' if p2p else ''} (per rank)", "bound": "hbm",
+                     "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),
@@ -923,7 +934,12 @@ def run_reference(args, rank, world):
 
 
 def main():
-    # NCCL's own messages (e.g. its version banner) go to stderr: stdout carries only the JSON line
+    # stdout carries only the JSON line: anything native code writes to fd 1 (e.g. NCCL's version
+    # banner) is sent to stderr, and the line goes to a private duplicate of the original stdout
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -932,7 +948,7 @@ def main():
     if args.impl == "reference":
         line = run_reference(args, rank, world)
         if line is not None:
-            print(json.dumps(line), flush=True)
+            print(json.dumps(line), file=_JSON_OUT, flush=True)
         return
     if world > 1:
         import torch
@@ -946,7 +962,7 @@ def main():
         fn = {"config4": run_config4, "greedy": run_greedy, "logits": run_logits, "config5": run_config5}[args.workload]
         line = fn(args, rank, world, local_rank)
         if line is not None:
-            print(json.dumps(line), flush=True)
+            print(json.dumps(line), file=_JSON_OUT, flush=True)
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
@@ -956,7 +972,7 @@ def main():
     if line is not None:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_JSON_OUT, flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

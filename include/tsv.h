@@ -248,23 +248,25 @@ TSV_API tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_
  * done by the producing kernels themselves instead of NCCL all-reduces.  Every rank
  * owns one symmetric buffer (tsv_p2p_alloc, zero-filled; B_max requests), mapped
  * into every peer (tsv_p2p_open of the 64-byte CUDA IPC handle; the caller exchanges
- * handles, e.g. torch.distributed all_gather_object).  Round 1: the flags kernel
- * stores this rank's mask words into slot [rank] of every peer's buffer and its last
- * CTA publishes the call's epoch in every peer's flag [0][rank] (release, system
- * scope); the meta kernel of each rank waits for all G flags (acquire) and sums the G
- * slots (disjoint owners: the sum is the OR).  Round 2 the same for the (key,
- * fallback key) pairs after the race, combined by max in the emit kernel.  Slots
- * alternate by epoch parity.  A wait that never completes (a peer died) gives up
- * after seconds and sets TSV_DEVSTATUS_P2P_TIMEOUT instead of hanging.
+ * handles, e.g. torch.distributed all_gather_object).  Every exchanged 32-bit word
+ * travels with the call's epoch in one aligned 8-byte word {data, epoch}, stored
+ * with 16-byte vector stores into slot [rank] of every peer's buffer; the consumer
+ * polls its own buffer until each word carries the epoch (no fences, no grid
+ * barrier).  Round 1: the flags kernel pushes the mask words, the meta kernel sums
+ * the G slots (disjoint owners: the sum is the OR).  Round 2: the keys kernel pushes
+ * the (key, fallback key) pairs after the race, the emit kernel takes their max.
+ * Slots alternate by epoch parity.  A wait that never completes (a peer died) gives
+ * up after seconds and sets TSV_DEVSTATUS_P2P_TIMEOUT instead of hanging.
  *  tsv_p2p_init: bufs[g] = rank g's buffer as mapped in this process (bufs[rank]
- *    local), world <= TSV_P2P_MAX_WORLD, B <= B_max in every call; the handle keeps
- *    the call epoch (all ranks must make the same sequence of calls).
+ *    local), world <= TSV_P2P_MAX_WORLD, B <= B_max in every call.  The call epoch
+ *    is kept on the device (advanced by the emit kernel), so the calls can be
+ *    captured in CUDA graphs; all ranks must make the same sequence of calls.
  *  tsv_verify_accept_sharded_p2p: the whole step on `stream` (flags -> meta -> race
  *    -> keys -> emit, five kernels, no host synchronisation); needs the verify
  *    workspace (tsv_verify_workspace_size).
- *  tsv_verify_shard_p2p_phase: phase 0 (new epoch, flags + push), 1 (wait, meta,
- *    race, keys + push), 2 (wait, emit) separately: lets one process drive G
- *    loopback ranks on one device (all phase 0, then all 1, then all 2). */
+ *  tsv_verify_shard_p2p_phase: phase 0 (flags + push), 1 (wait, meta, race, keys +
+ *    push), 2 (wait, emit) separately: lets one process drive G loopback ranks on
+ *    one device (all phase 0, then all 1, then all 2). */
 #define TSV_P2P_MAX_WORLD 8
 typedef struct tsv_p2p tsv_p2p;
 TSV_API tsv_status tsv_p2p_buffer_size(int32_t B_max, size_t* bytes);

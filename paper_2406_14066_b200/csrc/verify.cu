@@ -721,106 +721,100 @@ __global__ void __launch_bounds__(256) verify_shard_emit_kernel(const RaceParams
 // ------------------------------------------------ vocab sharding over peer memory (NEXT 3)
 // The lazy two rounds with the two exchanges done by the producing kernels themselves over
 // NVLink peer memory instead of NCCL all-reduces.  Every rank owns
-// one symmetric buffer (P2PLayout), mapped into every peer (CUDA IPC).  Round r: the
-// producing kernel (flags, keys) stores this rank's words into slot [rank] of every peer's
-// buffer, fences at system scope, and its last CTA publishes the call's epoch in flag
-// [r][rank] of every peer (st.release.sys); the consuming kernel (meta, emit) waits until
-// its own buffer's flags [r][0..G) all hold the epoch (ld.acquire.sys) and combines the G
-// slots locally -- sum of the disjoint mask words, max of the packed keys.  Slots alternate
-// by epoch parity, so a rank one call ahead never overwrites words a peer still reads.
-// A wait gives up after 2^24 sleeps of >= 256 ns (seconds) and sets TSV_DEVSTATUS_P2P_TIMEOUT.
+// one symmetric buffer, mapped into every peer (CUDA IPC).  Each exchanged 32-bit word
+// travels with the call's epoch in one 8-byte word {data, epoch} (the "LL" idea: an
+// aligned 8-byte store arrives whole), written with 16-byte vector stores into slot
+// [rank][i] of every peer's buffer.  The consumer of request i polls its own buffer's G
+// slots until every word carries the epoch -- no fences, no grid barrier, no flag round
+// trip -- and combines: the sum of the disjoint mask words (round 1, flags -> meta), the max
+// of the packed keys (round 2, keys -> emit).  Slots alternate by epoch parity.  The epoch
+// lives on the device (own buffer), read by every kernel of a call and advanced by the
+// emit kernel's last CTA, so captured CUDA graphs replay with advancing epochs.  A wait
+// gives up after seconds and sets TSV_DEVSTATUS_P2P_TIMEOUT instead of hanging.
 struct P2PView {
     unsigned char* buf[TSV_P2P_MAX_WORLD];  // rank g's symmetric buffer as mapped in this process
     int32_t rank, G, B_max;
-    uint32_t epoch;
 };
-constexpr size_t kP2PHdr = 256;  // u32 flags [2][MAX_WORLD] at 0, u32 counters [2] at 128
+constexpr size_t kP2PHdr = 256;  // u32 epoch at 0, u32 emit-arrival counter at 4
+// round 1 slot: 16 B per request {acc, e, own, e}; round 2 slot: 32 B {key lo/hi, fb lo/hi, each with e}
 __host__ __device__ constexpr size_t p2p_masks_bytes(int32_t B_max) {
-    return 2ull * TSV_P2P_MAX_WORLD * static_cast<size_t>(B_max) * 8ull;
+    return 2ull * TSV_P2P_MAX_WORLD * static_cast<size_t>(B_max) * 16ull;
 }
 __host__ __device__ constexpr size_t p2p_buffer_bytes(int32_t B_max) {
-    return kP2PHdr + 3ull * p2p_masks_bytes(B_max);  // masks [2][W][B] + keys [2][W][2B]
+    return kP2PHdr + 3ull * p2p_masks_bytes(B_max);
 }
-__device__ __forceinline__ uint32_t* p2p_flag(const P2PView& V, int32_t owner, int32_t round, int32_t from) {
-    return reinterpret_cast<uint32_t*>(V.buf[owner]) + round * TSV_P2P_MAX_WORLD + from;
+__device__ __forceinline__ uint32_t* p2p_epoch(const P2PView& V) {
+    return reinterpret_cast<uint32_t*>(V.buf[V.rank]);
 }
-__device__ __forceinline__ uint32_t* p2p_counter(const P2PView& V, int32_t round) {
-    return reinterpret_cast<uint32_t*>(V.buf[V.rank] + 128) + round;
+__device__ __forceinline__ uint32_t* p2p_counter(const P2PView& V) {
+    return reinterpret_cast<uint32_t*>(V.buf[V.rank]) + 1;
 }
-__device__ __forceinline__ unsigned long long* p2p_masks(const P2PView& V, int32_t owner, int32_t slot) {
-    const int32_t par = static_cast<int32_t>(V.epoch & 1u);
-    return reinterpret_cast<unsigned long long*>(V.buf[owner] + kP2PHdr) +
-           (static_cast<size_t>(par) * TSV_P2P_MAX_WORLD + slot) * V.B_max;
+__device__ __forceinline__ uint32_t p2p_load_epoch(const P2PView& V) {
+    return *reinterpret_cast<volatile uint32_t*>(p2p_epoch(V)) + 1u;  // this call's epoch (E + 1)
 }
-__device__ __forceinline__ unsigned long long* p2p_keys(const P2PView& V, int32_t owner, int32_t slot) {
-    const int32_t par = static_cast<int32_t>(V.epoch & 1u);
-    return reinterpret_cast<unsigned long long*>(V.buf[owner] + kP2PHdr + p2p_masks_bytes(V.B_max)) +
-           (static_cast<size_t>(par) * TSV_P2P_MAX_WORLD + slot) * 2 * V.B_max;
+__device__ __forceinline__ uint4* p2p_masks(const P2PView& V, uint32_t e, int32_t owner, int32_t slot) {
+    return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr) +
+           (static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + slot) * V.B_max;
 }
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ uint4* p2p_keys(const P2PView& V, uint32_t e, int32_t owner, int32_t slot) {
+    return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr + p2p_masks_bytes(V.B_max)) +
+           (static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + slot) * 2 * V.B_max;
 }
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ void st_ll(uint4* p, uint4 v) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p) : "memory");
     return v;
 }
-
-// After this CTA's pushes (each pushing thread fenced at system scope): the last CTA of the
-// grid publishes the epoch to every peer.
-__device__ __forceinline__ void p2p_signal(const P2PView& V, int32_t round) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        const uint32_t prev = atomicAdd(p2p_counter(V, round), 1u);
-        if (prev == gridDim.x - 1) {
-            atomicExch(p2p_counter(V, round), 0u);  // the next call's kernels run after this one
-            __threadfence_system();
-            for (int32_t g = 0; g < V.G; ++g) st_release_sys(p2p_flag(V, g, round, V.rank), V.epoch);
+// Poll one 16-byte LL line until both 8-byte halves carry epoch e (bounded).
+__device__ __forceinline__ uint4 ld_ll_wait(const uint4* p, uint32_t e, int32_t* devstatus) {
+    uint4 v = ld_ll(p);
+    uint32_t n = 0;
+    while (v.y != e || v.w != e) {
+        __nanosleep(32);
+        if (++n == (1u << 26)) {  // seconds: a peer never arrived
+            report(devstatus, TSV_DEVSTATUS_P2P_TIMEOUT);
+            break;
         }
+        v = ld_ll(p);
     }
-}
-
-// Every CTA: wait until all G ranks published this epoch for `round` in our own buffer.
-__device__ __forceinline__ void p2p_wait(const P2PView& V, int32_t round, int32_t* devstatus) {
-    if (threadIdx.x < static_cast<unsigned>(V.G)) {
-        const uint32_t* f = p2p_flag(V, V.rank, round, threadIdx.x);
-        uint32_t n = 0;
-        while (ld_acquire_sys(f) != V.epoch) {
-            __nanosleep(256);
-            if (++n == (1u << 24)) {  // ~4+ s: a peer never arrived
-                report(devstatus, TSV_DEVSTATUS_P2P_TIMEOUT);
-                break;
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
+    return v;
 }
 
 __global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams P, const P2PView V) {
     pdl_wait();
     pdl_launch_dependents();
+    const uint32_t e = p2p_load_epoch(V);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i < P.B) {
-        const unsigned long long mask = shard_flags_mask(P, i);
-        const int lane = threadIdx.x & 31;
-        if (lane < V.G) p2p_masks(V, lane, V.rank)[i] = mask;  // lane g stores into rank g's buffer
-        if (lane < V.G) __threadfence_system();
-    }
-    p2p_signal(V, 0);
+    if (i >= P.B) return;
+    const unsigned long long mask = shard_flags_mask(P, i);
+    const int lane = threadIdx.x & 31;
+    if (lane < V.G)  // lane g stores into rank g's buffer
+        st_ll(p2p_masks(V, e, lane, V.rank) + i,
+              make_uint4(static_cast<uint32_t>(mask), e, static_cast<uint32_t>(mask >> 32), e));
 }
 
 __global__ void __launch_bounds__(256) verify_p2p_meta_kernel(const RaceParams P, const P2PView V) {
     pdl_wait();
     pdl_launch_dependents();
-    p2p_wait(V, 0, P.devstatus);
+    const uint32_t e = p2p_load_epoch(V);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= P.B) return;
-    unsigned long long mask = 0;
-    for (int32_t g = 0; g < V.G; ++g) mask += p2p_masks(V, V.rank, g)[i];  // disjoint owners: sum = OR
+    const int lane = threadIdx.x & 31;
+    unsigned long long mask = 0;  // lane g polls rank g's words; disjoint owners: the sum is the OR
+    if (lane < V.G) {
+        const uint4 v = ld_ll_wait(p2p_masks(V, e, V.rank, lane) + i, e, P.devstatus);
+        mask = (static_cast<unsigned long long>(v.z) << 32) | v.x;
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) mask += __shfl_xor_sync(0xFFFFFFFFu, mask, o);  // lanes 0..7
+    mask = __shfl_sync(0xFFFFFFFFu, mask, 0);
     const ReqMeta rm = shard_meta_from_masks(P, i, mask);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         P.meta[i] = rm;
         P.rowT[i] = 0u;
         P.rowkey[i] = 0ull;
@@ -831,48 +825,66 @@ template <bool PRUNE>
 __global__ void __launch_bounds__(256) verify_p2p_keys_kernel(const RaceParams P, const P2PView V) {
     pdl_wait();
     pdl_launch_dependents();
+    const uint32_t e = p2p_load_epoch(V);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i < P.B) {
-        const int lane = threadIdx.x & 31;
-        const ReqMeta rm = P.meta[i];
-        uint64_t key = 0, fb = 0;
-        if (rm.ok == 1) {
-            key = P.rowkey[i];
-            if (key == 0 && rm.m < rm.k)  // this shard's residual is zero: its share of the R5 fallback
-                fb = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
-        }
-        if (lane < V.G) {
-            unsigned long long* d = p2p_keys(V, lane, V.rank);
-            d[2 * i] = key;
-            d[2 * i + 1] = fb;
-            __threadfence_system();
-        }
+    if (i >= P.B) return;
+    const int lane = threadIdx.x & 31;
+    const ReqMeta rm = P.meta[i];
+    uint64_t key = 0, fb = 0;
+    if (rm.ok == 1) {
+        key = P.rowkey[i];
+        if (key == 0 && rm.m < rm.k)  // this shard's residual is zero: its share of the R5 fallback
+            fb = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
     }
-    p2p_signal(V, 1);
+    if (lane < V.G) {
+        uint4* d = p2p_keys(V, e, lane, V.rank) + 2 * i;
+        st_ll(d, make_uint4(static_cast<uint32_t>(key), e, static_cast<uint32_t>(key >> 32), e));
+        st_ll(d + 1, make_uint4(static_cast<uint32_t>(fb), e, static_cast<uint32_t>(fb >> 32), e));
+    }
 }
 
 __global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P, const P2PView V) {
     pdl_wait();
     pdl_launch_dependents();
-    p2p_wait(V, 1, P.devstatus);
+    const uint32_t e = p2p_load_epoch(V);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= P.B) return;
-    const int lane = threadIdx.x & 31;
-    const ReqMeta rm = P.meta[i];  // written by this rank's meta kernel (same m_i on every rank)
-    if (rm.ok != 1) {
-        emit(P, i, 0, -1, -1);
-        if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
-        return;
+    if (i < P.B) {
+        const int lane = threadIdx.x & 31;
+        const ReqMeta rm = P.meta[i];  // written by this rank's meta kernel (same m_i on every rank)
+        uint64_t key = 0, fb = 0;
+        if (lane < V.G) {  // poll every rank's words (also for bad requests: keeps the slots' epochs in step)
+            const uint4* s = p2p_keys(V, e, V.rank, lane) + 2 * i;
+            const uint4 a = ld_ll_wait(s, e, P.devstatus);
+            const uint4 b = ld_ll_wait(s + 1, e, P.devstatus);
+            key = (static_cast<uint64_t>(a.z) << 32) | a.x;
+            fb = (static_cast<uint64_t>(b.z) << 32) | b.x;
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+            const uint64_t k2 = __shfl_xor_sync(0xFFFFFFFFu, key, o), f2 = __shfl_xor_sync(0xFFFFFFFFu, fb, o);
+            key = k2 > key ? k2 : key;
+            fb = f2 > fb ? f2 : fb;
+        }
+        key = __shfl_sync(0xFFFFFFFFu, key, 0);
+        fb = __shfl_sync(0xFFFFFFFFu, fb, 0);
+        if (rm.ok != 1) {
+            emit(P, i, 0, -1, -1);
+            if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
+        } else {
+            if (key == 0 && rm.m < rm.k) key = fb;
+            emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
+            if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+        }
     }
-    uint64_t key = 0, fb = 0;
-    for (int32_t g = 0; g < V.G; ++g) {
-        const unsigned long long* s = p2p_keys(V, V.rank, g);
-        key = s[2 * i] > key ? s[2 * i] : key;
-        fb = s[2 * i + 1] > fb ? s[2 * i + 1] : fb;
+    // advance the device epoch once every CTA of this kernel has read it (last CTA, GPU scope)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p2p_counter(V), 1u) == gridDim.x - 1) {
+            atomicExch(p2p_counter(V), 0u);
+            atomicExch(p2p_epoch(V), e);
+        }
     }
-    if (key == 0 && rm.m < rm.k) key = fb;
-    emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
-    if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
 }
 
 // ------------------------------------------------------------------ greedy verify (NEXT 2)
@@ -1709,7 +1721,6 @@ extern "C" tsv_status tsv_p2p_init(tsv_p2p** out, int32_t rank, int32_t world, i
     p->view.rank = rank;
     p->view.G = world;
     p->view.B_max = B_max;
-    p->view.epoch = 0;
     *out = p;
     return TSV_OK;
 }
@@ -1728,8 +1739,7 @@ extern "C" tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p
     TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_shard_p2p_phase: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
-    if (phase == 0) ++p->view.epoch;  // every call goes through phase 0 first, on every rank
-    if (a->B == 0) return TSV_OK;     // (all ranks skip the exchange together)
+    if (a->B == 0) return TSV_OK;  // (all ranks skip the exchange together; the epoch does not advance)
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     RaceParams P = make_params(a);
     const dim3 grid(static_cast<unsigned>((a->B + 7) / 8));

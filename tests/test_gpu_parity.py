@@ -363,6 +363,43 @@ def test_p2p_vocab_shard_one_hot_adversarial_llama3(tsv):
         assert (na == ona).all() and (out == oout).all()
 
 
+def test_p2p_graph_replay_advances_epochs(tsv):
+    # the call epoch lives on the device: a captured graph of 3 calls replayed twice stays correct
+    vb = synth.make_verify_batch(B=32, V=8192, k_max=8, lam=0.7, seed=30)
+    g = vb.to(DEV)
+    comm = tsv.P2PComm(0, 1, B_max=32)
+    try:
+        outs = []
+        args = []
+        for step in range(3):
+            na = torch.empty(vb.B, dtype=torch.int32, device=DEV)
+            out = torch.full((vb.B, vb.k_max + 1), -7, dtype=torch.int32, device=DEV)
+            a = tsv.make_verify_args(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, 8, step, vb.k_max,
+                                     na, out, vocab=vb.vocab, vocab_global=vb.vocab)
+            ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+            a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+            args.append((a, ws))
+            outs.append((na, out))
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            tsv.tsv_verify_accept_sharded_p2p(args[0][0], comm, stream=side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            for a, _ in args:
+                tsv.tsv_verify_accept_sharded_p2p(a, comm, stream=side)
+        for _ in range(2):
+            for na, out in outs:
+                out.fill_(-7)
+            graph.replay()
+            torch.cuda.synchronize()
+            for step, (na, out) in enumerate(outs):
+                ona, oout, _ = oracle_verify(vb, 8, step)
+                assert (_np(na) == ona).all() and (_np(out) == oout).all()
+    finally:
+        comm.close()
+
+
 def test_p2p_vocab_shard_two_processes_ipc(tmp_path):
     # the real multi-process path (CUDA IPC buffers, system-scope flags, epochs) with two ranks on the one
     # GPU of this box (time-sliced contexts), over gloo for the handle exchange; each rank checks the oracle
