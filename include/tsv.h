@@ -268,6 +268,7 @@ TSV_API tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_
  *    push), 2 (wait, emit) separately: lets one process drive G loopback ranks on
  *    one device (all phase 0, then all 1, then all 2). */
 #define TSV_P2P_MAX_WORLD 8
+#define TSV_P2P_MAX_SUMS 64
 typedef struct tsv_p2p tsv_p2p;
 TSV_API tsv_status tsv_p2p_buffer_size(int32_t B_max, size_t* bytes);
 TSV_API tsv_status tsv_p2p_alloc(int32_t B_max, void** buf_out, void* ipc_handle_out /* 64 B, nullable */);
@@ -278,6 +279,13 @@ TSV_API tsv_status tsv_p2p_init(tsv_p2p** out, int32_t rank, int32_t world, int3
 TSV_API tsv_status tsv_p2p_destroy(tsv_p2p* p);
 TSV_API tsv_status tsv_verify_accept_sharded_p2p(const tsv_verify_args* a, tsv_p2p* p, void* stream);
 TSV_API tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p2p* p, int32_t phase, void* stream);
+/* tsv_allreduce_i64_p2p: in-place exact sum over the ranks of count <= TSV_P2P_MAX_SUMS
+ * int64 (device) through the same buffers (one CTA; LL words; its own device epoch), the
+ * peer-memory replacement of tsv_allreduce_i64 for the request-sharded global sums
+ * (tsv_goodput_partial -> this -> tsv_goodput_finalize; tsv_update_partial -> this ->
+ * tsv_update_finalize).  device_status (nullable) gets TSV_DEVSTATUS_P2P_TIMEOUT. */
+TSV_API tsv_status tsv_allreduce_i64_p2p(int64_t* data, int32_t count, tsv_p2p* p, int32_t* device_status,
+                                         void* stream);
 
 /* --------------------------------------------------------------------------
  * Goodput k selection: ArgMaxGoodput (Listing 2) over

@@ -735,13 +735,14 @@ struct P2PView {
     unsigned char* buf[TSV_P2P_MAX_WORLD];  // rank g's symmetric buffer as mapped in this process
     int32_t rank, G, B_max;
 };
-constexpr size_t kP2PHdr = 256;  // u32 epoch at 0, u32 emit-arrival counter at 4
+constexpr size_t kP2PHdr = 256;  // u32 verify epoch at 0, emit-arrival counter at 4, all-reduce epoch at 8
 // round 1 slot: 16 B per request {acc, e, own, e}; round 2 slot: 32 B {key lo/hi, fb lo/hi, each with e}
 __host__ __device__ constexpr size_t p2p_masks_bytes(int32_t B_max) {
     return 2ull * TSV_P2P_MAX_WORLD * static_cast<size_t>(B_max) * 16ull;
 }
+constexpr size_t kP2PSumsBytes = 2ull * TSV_P2P_MAX_WORLD * TSV_P2P_MAX_SUMS * 16ull;  // [2][W][n] LL lines
 __host__ __device__ constexpr size_t p2p_buffer_bytes(int32_t B_max) {
-    return kP2PHdr + 3ull * p2p_masks_bytes(B_max);
+    return kP2PHdr + 3ull * p2p_masks_bytes(B_max) + kP2PSumsBytes;
 }
 __device__ __forceinline__ uint32_t* p2p_epoch(const P2PView& V) {
     return reinterpret_cast<uint32_t*>(V.buf[V.rank]);
@@ -783,6 +784,36 @@ __device__ __forceinline__ uint4 ld_ll_wait(const uint4* p, uint32_t e, int32_t*
         v = ld_ll(p);
     }
     return v;
+}
+
+// All-reduce (sum) of count <= TSV_P2P_MAX_SUMS int64 over the ranks (request-sharded global
+// goodput / acceptance sums): one CTA; thread j pushes data[j] as two LL words into slot
+// [rank][j] of every peer, then polls its own buffer's G slots and writes the exact sum.
+// Its own epoch (header word 2) advances at the end of every call.
+__global__ void __launch_bounds__(64) p2p_allreduce_i64_kernel(int64_t* data, int32_t count, const P2PView V,
+                                                               int32_t* devstatus) {
+    pdl_wait();
+    pdl_launch_dependents();
+    uint32_t* ep = reinterpret_cast<uint32_t*>(V.buf[V.rank]) + 2;
+    const uint32_t e = *reinterpret_cast<volatile uint32_t*>(ep) + 1u;
+    const int32_t j = threadIdx.x;
+    auto slot = [&](int32_t owner, int32_t from) {
+        return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr + 3ull * p2p_masks_bytes(V.B_max)) +
+               (static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + from) * TSV_P2P_MAX_SUMS + j;
+    };
+    if (j < count) {
+        const uint64_t x = static_cast<uint64_t>(data[j]);
+        for (int32_t g = 0; g < V.G; ++g)
+            st_ll(slot(g, V.rank), make_uint4(static_cast<uint32_t>(x), e, static_cast<uint32_t>(x >> 32), e));
+        uint64_t sum = 0;
+        for (int32_t g = 0; g < V.G; ++g) {
+            const uint4 v = ld_ll_wait(slot(V.rank, g), e, devstatus);
+            sum += (static_cast<uint64_t>(v.z) << 32) | v.x;
+        }
+        data[j] = static_cast<int64_t>(sum);
+    }
+    __syncthreads();
+    if (j == 0) *ep = e;
 }
 
 __global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams P, const P2PView V) {
@@ -1764,5 +1795,17 @@ extern "C" tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p
 
 extern "C" tsv_status tsv_verify_accept_sharded_p2p(const tsv_verify_args* a, tsv_p2p* p, void* stream) {
     for (int32_t ph = 0; ph < 3; ++ph) TSV_TRY(tsv_verify_shard_p2p_phase(a, p, ph, stream));
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_allreduce_i64_p2p(int64_t* data, int32_t count, tsv_p2p* p, int32_t* device_status,
+                                           void* stream) {
+    TSV_REQUIRE(data && p, "tsv_allreduce_i64_p2p: NULL argument");
+    TSV_REQUIRE(count >= 0 && count <= TSV_P2P_MAX_SUMS, "tsv_allreduce_i64_p2p: count %d outside [0, %d]", count,
+                TSV_P2P_MAX_SUMS);
+    TSV_TRY(check_device());
+    TSV_CUDA(launch_pdl(p2p_allreduce_i64_kernel, dim3(1), dim3(TSV_P2P_MAX_SUMS), 0, static_cast<cudaStream_t>(stream),
+                        data, count, p->view, device_status),
+             "p2p_allreduce_i64_kernel launch");
     return TSV_OK;
 }

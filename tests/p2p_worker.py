@@ -2,7 +2,8 @@
 
 Both ranks share the box's one GPU; each holds one vocab shard of the same batch, maps the
 other's symmetric buffer over CUDA IPC (tsv.P2PComm, handles exchanged over gloo) and runs
-tsv_verify_accept_sharded_p2p for several steps; outputs must equal the unsharded oracle."""
+tsv_verify_accept_sharded_p2p for several steps, then the request-sharded global goodput and
+alpha update over the same buffers; every result must equal the oracle on the whole batch."""
 import os
 import sys
 
@@ -48,6 +49,33 @@ def main():
         good = (na.cpu().numpy() == ona).all() and (out.cpu().numpy() == oout).all() and int(st.item()) == ost
         print(f"rank {rank} step {step}: {'match' if good else 'MISMATCH'} status {int(st.item())}", flush=True)
         ok = ok and good
+    # request-sharded global goodput and alpha update through the same buffers: rank r owns a
+    # contiguous half of a B = 300 batch; k* / goodput / alpha must equal the oracle on the whole batch
+    Bq, K = 300, 5
+    ctx, _ = synth.make_goodput_instance(Bq, K, seed=31)
+    cap = np.random.Generator(np.random.PCG64(31)).integers(0, K + 1, Bq).astype(np.int32)
+    lo_r, hi_r = Bq * rank // world, Bq * (rank + 1) // world
+    for pol in (0, 1):
+        ok_k, og = oracle.choose_k(0.7, ctx, cap, K, pol, synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT,
+                                   pld_cost_ms=0.05)
+        a = torch.tensor([0.7], dtype=torch.float64, device=dev)
+        k, gp, _ = tsv.tsv_goodput_choose_k_sharded(a, torch.tensor(ctx[lo_r:hi_r], device=dev),
+                                                    torch.tensor(cap[lo_r:hi_r], device=dev), K, pol,
+                                                    synth.SPEC_DESK_TARGET, comm, synth.SPEC_DESK_DRAFT, 0.05)
+        torch.cuda.synchronize()
+        good = int(k.item()) == ok_k and (gp.cpu().numpy().view(np.uint64) == og.view(np.uint64)).all()
+        print(f"rank {rank} goodput policy {pol}: {'match' if good else 'MISMATCH'}", flush=True)
+        ok = ok and good
+    ks = np.full(Bq, K)
+    m = np.minimum(np.arange(Bq) % 7, K).astype(np.int32)
+    want = oracle.update(0.5, m, np.concatenate([[0], np.cumsum(ks + 1)]).astype(np.int32), 0.9, 0)
+    ro = np.concatenate([[0], np.cumsum(ks[lo_r:hi_r] + 1)]).astype(np.int32)
+    a = torch.tensor([0.5], dtype=torch.float64, device=dev)
+    tsv.tsv_update_acceptance_sharded(a, torch.tensor(m[lo_r:hi_r], device=dev), torch.tensor(ro, device=dev), comm)
+    torch.cuda.synchronize()
+    good = (a.cpu().numpy().view(np.uint64) == np.atleast_1d(want).view(np.uint64)).all()
+    print(f"rank {rank} alpha update: {'match' if good else 'MISMATCH'}", flush=True)
+    ok = ok and good
     dist.barrier()
     comm.close()
     dist.destroy_process_group()

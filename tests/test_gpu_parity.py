@@ -675,6 +675,33 @@ def test_update_sharded_sums_equal_oracle(tsv):
         assert (_np(a).view(np.uint64) == np.atleast_1d(want).view(np.uint64)).all()
 
 
+def test_p2p_allreduce_loopback_streams(tsv):
+    # G virtual ranks on one device, each on its own stream (the kernels run concurrently and poll
+    # each other's LL words); exact int64 sums incl. wrap-around, three calls (both slot parities)
+    rng = np.random.Generator(np.random.PCG64(12))
+    for G in (1, 2, 4, 8):
+        lb = tsv.P2PLoopback(G, 8)
+        try:
+            streams = [torch.cuda.Stream() for _ in range(G)]
+            for call in range(3):
+                n = int(rng.integers(1, 65))
+                vals = rng.integers(-2 ** 62, 2 ** 62, (G, n), dtype=np.int64)
+                vals[:, 0] = 2 ** 62  # sum wraps modulo 2^64 like the NCCL int64 sum
+                data = [torch.tensor(vals[g], device=DEV) for g in range(G)]
+                st = torch.zeros(1, dtype=torch.int32, device=DEV)
+                torch.cuda.synchronize()
+                for g in range(G):
+                    tsv._check(tsv.lib().tsv_allreduce_i64_p2p(data[g].data_ptr(), n, lb.handles[g], st.data_ptr(),
+                                                               streams[g].cuda_stream))
+                torch.cuda.synchronize()
+                want = vals.astype(np.uint64).sum(axis=0).view(np.int64)
+                for g in range(G):
+                    assert (_np(data[g]) == want).all(), (G, call, g)
+                assert int(st.item()) == 0
+        finally:
+            lb.close()
+
+
 def test_sharded_goodput_and_update_nccl_world1(tsv):
     # the NCCL plumbing (partial -> ncclAllReduce -> finalize) on a one-rank communicator
     comm = tsv.Comm(0, 1)
