@@ -55,9 +55,10 @@ def parse():
                          "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling); logits: the fused "
                          "softmax-from-logits verify (NEXT 1) on the config-2 batch given as logits; config5: the "
                          "goodput sweep (B 1-512 x alpha 0.3-0.9, K = 8) as one batched choose-k launch")
-    ap.add_argument("--shard-mode", default="lazy", choices=["lazy", "dense", "p2p"],
+    ap.add_argument("--shard-mode", default="auto", choices=["auto", "lazy", "dense", "p2p"],
                     help="config4 sharding mode: lazy two rounds over NCCL all-reduces, one-round dense over an "
-                         "NCCL all-gather, or the lazy two rounds over NVLink peer memory (no NCCL)")
+                         "NCCL all-gather, or the lazy two rounds over NVLink peer memory (no NCCL); auto = p2p "
+                         "for N > 1, lazy for N = 1 (where NCCL's all-reduces are local copies)")
     return ap.parse_args()
 
 
@@ -463,6 +464,8 @@ def run_config4(args, rank, world, local_rank):
     seed = synth.DEFAULT_SEED
     lo, Vs = pdist.vocab_shards(V4, world)[rank]
     hi = lo + Vs
+    if args.shard_mode == "auto":
+        args.shard_mode = "p2p" if world > 1 else "lazy"
     p2p = args.shard_mode == "p2p"
     comm = tsv.P2PComm(rank, world, B_max=B) if p2p else tsv.Comm(rank, world)
     flags = tsv.VERIFY_SHARD_DENSE if args.shard_mode == "dense" else 0
