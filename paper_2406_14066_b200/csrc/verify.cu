@@ -1589,6 +1589,25 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
 }
 
 // Logits workspace: [verify workspace][partials (rows_p + rows_p) x n_chunks][lstats B]
+// The statistics pass streams every p and q row: its items are sized for ~one per resident warp
+// of ITS grid over all rows (so a row has only a few partials for the scan to combine), not the
+// lazy race's one-row-per-request items.  An explicit chunk is used for both passes (tests).
+#ifndef TSV_STATS_OWN_CHUNK
+#define TSV_STATS_OWN_CHUNK 1
+#endif
+static RaceParams stats_params(const tsv_verify_args* a, RaceParams P) {
+    if (a->chunk > 0 || !TSV_STATS_OWN_CHUNK) return P;
+    const int64_t warps = static_cast<int64_t>(sm_count()) * 8 * TSV_STATS_MINB;
+    const int64_t cells = 2 * static_cast<int64_t>(a->rows_p) * a->vocab;  // >= (rows_p + rows_q) V
+    int64_t c = (cells + warps - 1) / warps;
+    c = (c + 127) / 128 * 128;
+    if (c < 512) c = 512;
+    if (c > (1 << 20)) c = 1 << 20;
+    P.chunk = static_cast<int32_t>(c);
+    P.n_chunks = static_cast<int32_t>((a->vocab + c - 1) / c);
+    return P;
+}
+
 static size_t logits_extra_bytes(const tsv_verify_args* a, int32_t n_chunks) {
     return align256(sizeof(LogitPartial) * 2 * static_cast<size_t>(a->rows_p) * static_cast<size_t>(n_chunks)) +
            align256(sizeof(float4) * static_cast<size_t>(a->B));
@@ -1597,7 +1616,7 @@ static size_t logits_extra_bytes(const tsv_verify_args* a, int32_t n_chunks) {
 extern "C" tsv_status tsv_verify_logits_workspace_size(const tsv_verify_args* a, size_t* bytes) {
     TSV_REQUIRE(bytes != nullptr, "tsv_verify_logits_workspace_size: bytes is NULL");
     TSV_TRY(validate(a));
-    const RaceParams P = make_params(a);
+    const RaceParams P = stats_params(a, make_params(a));
     *bytes = align256(workspace_bytes(a)) + logits_extra_bytes(a, P.n_chunks);
     return TSV_OK;
 }
@@ -1611,24 +1630,25 @@ extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float t
     if (a->B == 0) return TSV_OK;
     TSV_TRY(check_device());
     RaceParams P = make_params(a);
-    const size_t need = align256(workspace_bytes(a)) + logits_extra_bytes(a, P.n_chunks);
+    RaceParams PS = stats_params(a, P);  // statistics pass + scan (partials per row)
+    const size_t need = align256(workspace_bytes(a)) + logits_extra_bytes(a, PS.n_chunks);
     TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= need,
                 "tsv_verify_accept_logits: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)need);
     char* ws = static_cast<char*>(a->workspace) + align256(workspace_bytes(a));
     LogitPartial* part = reinterpret_cast<LogitPartial*>(ws);
-    ws += align256(sizeof(LogitPartial) * 2 * static_cast<size_t>(a->rows_p) * static_cast<size_t>(P.n_chunks));
+    ws += align256(sizeof(LogitPartial) * 2 * static_cast<size_t>(a->rows_p) * static_cast<size_t>(PS.n_chunks));
     float4* lstats = reinterpret_cast<float4*>(ws);
-    P.lstats = lstats;
-    P.inv_tau = static_cast<float>(1.0 / static_cast<double>(temperature));
+    P.lstats = PS.lstats = lstats;
+    P.inv_tau = PS.inv_tau = static_cast<float>(1.0 / static_cast<double>(temperature));
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int64_t n_items = 2 * static_cast<int64_t>(a->rows_p) * P.n_chunks;
+    const int64_t n_items = 2 * static_cast<int64_t>(a->rows_p) * PS.n_chunks;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * TSV_STATS_MINB));
-    TSV_CUDA(launch_pdl(verify_logit_stats_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, P, part,
+    TSV_CUDA(launch_pdl(verify_logit_stats_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, PS, part,
                         a->rows_p),
              "verify_logit_stats_kernel launch");
     const dim3 req_grid(static_cast<unsigned>((a->B + 7) / 8));
-    TSV_CUDA(launch_pdl(verify_logit_scan_kernel, req_grid, dim3(256), 0, st, P,
+    TSV_CUDA(launch_pdl(verify_logit_scan_kernel, req_grid, dim3(256), 0, st, PS,
                         static_cast<const LogitPartial*>(part), lstats),
              "verify_logit_scan_kernel launch");
     const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
