@@ -1569,8 +1569,11 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
                 "tsv_verify_greedy: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
     tsv_verify_args b = *a;
-    if (b.chunk == 0) {  // about one item per resident warp over all rows
-        const int64_t warps = static_cast<int64_t>(sm_count()) * 32;
+#ifndef TSV_GREEDY_ITEM_WARPS  // items per SM: two per resident warp (config 2: 30.4 us; one: 32.1; 1/2: 32.3)
+#define TSV_GREEDY_ITEM_WARPS (2 * 8 * TSV_GREEDY_MINB)
+#endif
+    if (b.chunk == 0) {  // about two items per resident warp of the argmax grid over all rows
+        const int64_t warps = static_cast<int64_t>(sm_count()) * TSV_GREEDY_ITEM_WARPS;
         int64_t c = (static_cast<int64_t>(a->rows_p) * a->vocab + warps - 1) / warps;
         c = (c + 127) / 128 * 128;
         b.chunk = static_cast<int32_t>(std::min<int64_t>(std::max<int64_t>(c, 1024), kMaxChunk));
