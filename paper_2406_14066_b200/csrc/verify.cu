@@ -1600,7 +1600,10 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
 #endif
 static RaceParams stats_params(const tsv_verify_args* a, RaceParams P) {
     if (a->chunk > 0 || !TSV_STATS_OWN_CHUNK) return P;
-    const int64_t warps = static_cast<int64_t>(sm_count()) * 8 * TSV_STATS_MINB;
+#ifndef TSV_STATS_ITEMS_PER_WARP
+#define TSV_STATS_ITEMS_PER_WARP 1
+#endif
+    const int64_t warps = static_cast<int64_t>(sm_count()) * 8 * TSV_STATS_MINB * TSV_STATS_ITEMS_PER_WARP;
     const int64_t cells = 2 * static_cast<int64_t>(a->rows_p) * a->vocab;  // >= (rows_p + rows_q) V
     int64_t c = (cells + warps - 1) / warps;
     c = (c + 127) / 128 * 128;
