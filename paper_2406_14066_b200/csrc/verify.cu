@@ -1271,8 +1271,9 @@ static int sm_count();
 static int32_t auto_chunk(const tsv_verify_args* a) {
     if (a->chunk > 0) return a->chunk;
     const int64_t warps = static_cast<int64_t>(sm_count()) * 32;  // resident warps of the race kernel
-    const int64_t rows_x_cols = static_cast<int64_t>(a->B) * a->vocab;
-    int64_t c = (rows_x_cols + warps - 1) / warps;
+    // chunks per row so that B * chunks <= warps (one wave), then the chunk covering V in that many
+    const int64_t per_row = std::max<int64_t>(1, warps / std::max<int32_t>(a->B, 1));
+    int64_t c = (a->vocab + per_row - 1) / per_row;
     c = (c + 127) / 128 * 128;
     if (c < 512) c = 512;
     if (c > kMaxChunk) c = kMaxChunk;
