@@ -1,6 +1,7 @@
 """Worker of test_p2p_vocab_shard_two_processes_ipc (launched by torch.distributed.run, 2 ranks).
 
-Both ranks share the box's one GPU; each holds one vocab shard of the same batch, maps the
+Rank r runs on GPU r % device_count (two GPUs: a real NVLink peer mapping; one GPU: both ranks
+share it); each holds one vocab shard of the same batch, maps the
 other's symmetric buffer over CUDA IPC (tsv.P2PComm, handles exchanged over gloo) and runs
 tsv_verify_accept_sharded_p2p for several steps, then the request-sharded global goodput and
 alpha update over the same buffers; every result must equal the oracle on the whole batch."""
@@ -22,8 +23,9 @@ from paper_2406_14066_b200 import tsv  # noqa: E402
 def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
-    torch.cuda.set_device(0)
-    dev = torch.device("cuda", 0)
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", rank % ndev)  # distinct GPUs when there are enough (NVLink), else shared
+    torch.cuda.set_device(dev)
     vb = synth.make_verify_batch(B=48, V=32000, k_max=8, lam=0.7, seed=29)
     V, B = vb.vocab, vb.B
     Vs = V // world
