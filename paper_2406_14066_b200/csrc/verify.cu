@@ -930,6 +930,15 @@ __global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P
 }
 
 // ------------------------------------------------------------------ greedy verify (NEXT 2)
+__global__ void __launch_bounds__(256) clear_u64_kernel(unsigned long long* p, int64_t n) {
+    pdl_wait();  // the previous call's readers of these slots are done
+    pdl_launch_dependents();
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 1024 + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (i0 + 256 * k < n) p[i0 + 256 * k] = 0ull;
+}
+
 // Temperature 0 (reading R24): keep draft j iff x_j = argmax_v p_j[v]; emit the argmax of
 // row m.  Every row up to the first mismatch needs its full argmax, so the rows are streamed
 // densely: work items (row, chunk) grid-stride over all p rows of the batch; a lane keeps its
@@ -1581,8 +1590,16 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
     }
     RaceParams P = make_params(&b);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    TSV_CUDA(cudaMemsetAsync(P.rowkey, 0, sizeof(unsigned long long) * static_cast<size_t>(a->rows_p), st),
-             "cudaMemsetAsync");
+#ifndef TSV_GREEDY_CLEAR_KERNEL
+#define TSV_GREEDY_CLEAR_KERNEL 1
+#endif
+    if (TSV_GREEDY_CLEAR_KERNEL)  // a PDL kernel (its launch overlaps the previous kernel; a memset node does not)
+        TSV_CUDA(launch_pdl(clear_u64_kernel, dim3(static_cast<unsigned>((a->rows_p + 1023) / 1024)), dim3(256), 0, st,
+                            P.rowkey, static_cast<int64_t>(a->rows_p)),
+                 "clear_u64_kernel launch");
+    else
+        TSV_CUDA(cudaMemsetAsync(P.rowkey, 0, sizeof(unsigned long long) * static_cast<size_t>(a->rows_p), st),
+                 "cudaMemsetAsync");
     const int64_t n_items = static_cast<int64_t>(a->rows_p) * P.n_chunks;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * TSV_GREEDY_MINB));
     TSV_CUDA(launch_pdl(verify_greedy_argmax_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, P),
