@@ -55,10 +55,10 @@ def parse():
                          "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling); logits: the fused "
                          "softmax-from-logits verify (NEXT 1) on the config-2 batch given as logits; config5: the "
                          "goodput sweep (B 1-512 x alpha 0.3-0.9, K = 8) as one batched choose-k launch")
-    ap.add_argument("--shard-mode", default="auto", choices=["auto", "lazy", "dense", "p2p"],
+    ap.add_argument("--shard-mode", default="auto", choices=["auto", "none", "lazy", "dense", "p2p"],
                     help="config4 sharding mode: lazy two rounds over NCCL all-reduces, one-round dense over an "
-                         "NCCL all-gather, or the lazy two rounds over NVLink peer memory (no NCCL); auto = p2p "
-                         "for N > 1, lazy for N = 1 (where NCCL's all-reduces are local copies)")
+                         "NCCL all-gather, or the lazy two rounds over NVLink peer memory (no NCCL); none = the "
+                         "unsharded tsv_verify_accept (N = 1 only); auto = p2p for N > 1, none for N = 1")
     return ap.parse_args()
 
 
@@ -465,14 +465,20 @@ def run_config4(args, rank, world, local_rank):
     lo, Vs = pdist.vocab_shards(V4, world)[rank]
     hi = lo + Vs
     if args.shard_mode == "auto":
-        args.shard_mode = "p2p" if world > 1 else "lazy"
+        args.shard_mode = "p2p" if world > 1 else "none"
+    if args.shard_mode == "none" and world > 1:
+        raise SystemExit("--shard-mode none is the one-GPU (unsharded) call")
     p2p = args.shard_mode == "p2p"
-    comm = tsv.P2PComm(rank, world, B_max=B) if p2p else tsv.Comm(rank, world)
+    unsharded = args.shard_mode == "none"
+    comm = None if unsharded else (tsv.P2PComm(rank, world, B_max=B) if p2p else tsv.Comm(rank, world))
     flags = tsv.VERIFY_SHARD_DENSE if args.shard_mode == "dense" else 0
     entry = tsv.lib().tsv_verify_accept_sharded_p2p if p2p else tsv.lib().tsv_verify_accept_sharded
 
     def run_sharded(a, stream=None):
-        tsv._check(entry(tsv.ctypes.byref(a), comm.handle, tsv._stream(stream)))
+        if unsharded:  # one GPU holds the whole vocabulary: scan -> race -> emit, no exchange
+            tsv._check(tsv.lib().tsv_verify_accept(tsv.ctypes.byref(a), tsv._stream(stream)))
+        else:
+            tsv._check(entry(tsv.ctypes.byref(a), comm.handle, tsv._stream(stream)))
     na = torch.empty(B, dtype=torch.int32, device=dev)
     outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
     sets, footprint = [], 0
@@ -505,7 +511,7 @@ def run_config4(args, rank, world, local_rank):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=side):
         for a in args_list:
-            tsv._check(entry(tsv.ctypes.byref(a), comm.handle, side.cuda_stream))
+            run_sharded(a, stream=side)
     torch.cuda.synchronize()
     for _ in range((W + gl - 1) // gl):
         g.replay()
@@ -544,7 +550,8 @@ def run_config4(args, rank, world, local_rank):
         vbytes += float((rows * V4 * 4).sum()) / world
     tok_per_step, vbytes = tok / gl, vbytes / gl
     ms_step = t_ms / steps
-    comm.close()
+    if comm is not None:
+        comm.close()
     if rank != 0:
         return None
     peak, peak_src = load_peaks()
@@ -554,16 +561,18 @@ def run_config4(args, rank, world, local_rank):
         "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
         "config": {"workload": f"config4 Llama-3 verify (B={B}, k~U{{0..{K_MAX}}}, V={V4}, fp32 p+q, lambda=0.7), "
-                               f"vocab-sharded x{world} ({args.shard_mode})",
-                   "global_batch": B, "vocab": V4, "k_max": K_MAX, "parallelism": f"vocab-sharded x{world}",
+                               + ("one GPU, unsharded" if unsharded else f"vocab-sharded x{world} ({args.shard_mode})"),
+                   "global_batch": B, "vocab": V4, "k_max": K_MAX,
+                   "parallelism": "unsharded x1" if unsharded else f"vocab-sharded x{world}",
                    "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank",
                    "graph_steps": gl},
-        "roofline": {"kernel": f"tsv_verify_accept_sharded{'_p2p' if p2p else ''} (per rank)", "bound": "hbm",
+        "roofline": {"kernel": "tsv_verify_accept (unsharded, one GPU)" if unsharded else
+                     f"tsv_verify_accept_sharded{'_p2p' if p2p else ''} (per rank)", "bound": "hbm",
                      "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),
-        "gpu_launches": (3 if flags else 5) * steps,
+        "gpu_launches": (3 if (flags or unsharded) else 5) * steps,
         "e2e": None,
         "tokens_per_step": tok_per_step,
         "requests_per_s": B / (ms_step * 1e-3),
