@@ -64,7 +64,8 @@ struct GpTotals {  // per lane k of warp 0: L[k], N[k]; every lane: c[0..3]
 // Each thread accumulates its requests for every candidate k (the Horner recurrence
 // l(a, j+1) = fma(a, l(a, j), 1) advanced once each time min(k, cap_i) grows, op-for-op a
 // fresh evaluation); warp sums are exact redux.sync limb sums, then one shared-memory step.
-__device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A) {
+constexpr int kGpCapCache = 4;  // caps kept in registers for k_i = min(k*, cap_i) (B <= 4 kGpThreads)
+__device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A, int32_t* cap_cache = nullptr) {
     __shared__ long long sL[kGpWarps][kGpMaxK];
     __shared__ long long sN[kGpWarps][kGpMaxK];
     __shared__ long long sC[kGpWarps][3];
@@ -77,9 +78,11 @@ __device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A) {
     long long n_ctx = 0, n_ctx_spec = 0;
     uint32_t b_spec = 0;
     const double a_glob = A.alpha_per_request ? 0.0 : __ldcg(A.alpha);
-    for (int32_t i = threadIdx.x; i < B; i += kGpThreads) {
+    int slot = 0;
+    for (int32_t i = threadIdx.x; i < B; i += kGpThreads, ++slot) {
         const double a = A.alpha_per_request ? __ldcg(A.alpha + i) : a_glob;
         const int32_t ci = __ldcg(A.cap + i);
+        if (cap_cache && slot < kGpCapCache) cap_cache[slot] = ci;
         const int32_t cl = __ldcg(A.ctx_len + i);
         n_ctx += cl;
         if (ci > 0) {
@@ -178,10 +181,12 @@ __device__ __forceinline__ int gp_argmax_warp(const ChooseArgs& A, const GpTotal
     return best_k;
 }
 
-// k_i = min(k*, cap_i) for this CTA's requests (all threads; k* from shared memory).
-__device__ __forceinline__ void gp_write_k_per_request(const ChooseArgs& A, int kb) {
-    for (int32_t i = threadIdx.x; i < A.B; i += kGpThreads) {
-        const int32_t ci = __ldcg(A.cap + i);
+// k_i = min(k*, cap_i) for this CTA's requests (all threads; k* from shared memory; caps from
+// the registers of gp_sums_block when given, else reloaded).
+__device__ __forceinline__ void gp_write_k_per_request(const ChooseArgs& A, int kb, const int32_t* cap_cache = nullptr) {
+    int slot = 0;
+    for (int32_t i = threadIdx.x; i < A.B; i += kGpThreads, ++slot) {
+        const int32_t ci = (cap_cache && slot < kGpCapCache) ? cap_cache[slot] : __ldcg(A.cap + i);
         const int32_t ki = kb < ci ? kb : ci;
         A.k_per_request[i] = ki < 0 ? 0 : ki;
     }
@@ -191,14 +196,15 @@ __device__ __forceinline__ void gp_write_k_per_request(const ChooseArgs& A, int 
 // with ld.global.cg so values written by other CTAs of a fused kernel are seen.
 __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
     __shared__ int s_best;
-    const GpTotals t = gp_sums_block(A);
+    int32_t caps[kGpCapCache];
+    const GpTotals t = gp_sums_block(A, caps);
     if ((threadIdx.x >> 5) == 0) {
         const int kb = gp_argmax_warp(A, t);
         if (threadIdx.x == 0) s_best = kb;
     }
     if (A.k_per_request) {
         __syncthreads();
-        gp_write_k_per_request(A, s_best);
+        gp_write_k_per_request(A, s_best, caps);
     }
 }
 
