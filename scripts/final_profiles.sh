@@ -6,7 +6,7 @@ bash scripts/gpu_all.sh all
 for wl in greedy logits config5; do
   timeout 600 python bench.py --workload $wl > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err; echo "bench $wl rc=$?"
 done
-for m in lazy dense p2p; do
+for m in none lazy dense p2p; do
   timeout 600 python bench.py --workload config4 --shard-mode $m > gpurun_out/bench_config4_$m.json 2> gpurun_out/bench_config4_$m.err; echo "bench config4 $m rc=$?"
 done
 BENCH_ARGS="--breakdown --no-cpu-baseline --e2e-steps 0" timeout 600 python bench.py --breakdown --no-cpu-baseline --e2e-steps 0 > gpurun_out/bench_breakdown.json 2> gpurun_out/bench_breakdown.err; echo "breakdown rc=$?"
