@@ -64,11 +64,13 @@ struct GpTotals {  // per lane k of warp 0: L[k], N[k]; every lane: c[0..3]
 // Each thread accumulates its requests for every candidate k (the Horner recurrence
 // l(a, j+1) = fma(a, l(a, j), 1) advanced once each time min(k, cap_i) grows, op-for-op a
 // fresh evaluation); warp sums are exact redux.sync limb sums, then one shared-memory step.
-constexpr int kGpCapCache = 4;  // caps kept in registers for k_i = min(k*, cap_i) (B <= 4 kGpThreads)
+constexpr int kGpCapCache = 4;  // caps kept in registers for k_i = min(k*, cap_i) (B <= 4 NT)
+template <int NT = kGpThreads>
 __device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A, int32_t* cap_cache = nullptr) {
-    __shared__ long long sL[kGpWarps][kGpMaxK];
-    __shared__ long long sN[kGpWarps][kGpMaxK];
-    __shared__ long long sC[kGpWarps][3];
+    constexpr int NW = NT / 32;
+    __shared__ long long sL[NW][kGpMaxK];
+    __shared__ long long sN[NW][kGpMaxK];
+    __shared__ long long sC[NW][3];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t B = A.B, k_max = A.k_max;
     long long Lk[kGpMaxK];
@@ -79,7 +81,7 @@ __device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A, int32_t* 
     uint32_t b_spec = 0;
     const double a_glob = A.alpha_per_request ? 0.0 : __ldcg(A.alpha);
     int slot = 0;
-    for (int32_t i = threadIdx.x; i < B; i += kGpThreads, ++slot) {
+    for (int32_t i = threadIdx.x; i < B; i += NT, ++slot) {
         const double a = A.alpha_per_request ? __ldcg(A.alpha + i) : a_glob;
         const int32_t ci = __ldcg(A.cap + i);
         if (cap_cache && slot < kGpCapCache) cap_cache[slot] = ci;
@@ -126,14 +128,14 @@ __device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A, int32_t* 
     GpTotals t = {0, 0, 0, 0, 0, static_cast<long long>(B)};
     if (warp == 0) {
 #pragma unroll
-        for (int w = 0; w < kGpWarps; ++w) {
+        for (int w = 0; w < NW; ++w) {
             t.c0 += sC[w][0];
             t.c1 += sC[w][1];
             t.c2 += sC[w][2];
         }
         if (lane <= k_max) {
 #pragma unroll
-            for (int w = 0; w < kGpWarps; ++w) {
+            for (int w = 0; w < NW; ++w) {
                 t.L += sL[w][lane];
                 t.N += sN[w][lane];
             }
@@ -183,9 +185,10 @@ __device__ __forceinline__ int gp_argmax_warp(const ChooseArgs& A, const GpTotal
 
 // k_i = min(k*, cap_i) for this CTA's requests (all threads; k* from shared memory; caps from
 // the registers of gp_sums_block when given, else reloaded).
+template <int NT = kGpThreads>
 __device__ __forceinline__ void gp_write_k_per_request(const ChooseArgs& A, int kb, const int32_t* cap_cache = nullptr) {
     int slot = 0;
-    for (int32_t i = threadIdx.x; i < A.B; i += kGpThreads, ++slot) {
+    for (int32_t i = threadIdx.x; i < A.B; i += NT, ++slot) {
         const int32_t ci = (cap_cache && slot < kGpCapCache) ? cap_cache[slot] : __ldcg(A.cap + i);
         const int32_t ki = kb < ci ? kb : ci;
         A.k_per_request[i] = ki < 0 ? 0 : ki;
@@ -194,17 +197,18 @@ __device__ __forceinline__ void gp_write_k_per_request(const ChooseArgs& A, int 
 
 // ArgMaxGoodput over one CTA of kGpThreads threads (all threads must call).  Inputs are read
 // with ld.global.cg so values written by other CTAs of a fused kernel are seen.
+template <int NT = kGpThreads>
 __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
     __shared__ int s_best;
     int32_t caps[kGpCapCache];
-    const GpTotals t = gp_sums_block(A, caps);
+    const GpTotals t = gp_sums_block<NT>(A, caps);
     if ((threadIdx.x >> 5) == 0) {
         const int kb = gp_argmax_warp(A, t);
         if (threadIdx.x == 0) s_best = kb;
     }
     if (A.k_per_request) {
         __syncthreads();
-        gp_write_k_per_request(A, s_best, caps);
+        gp_write_k_per_request<NT>(A, s_best, caps);
     }
 }
 
