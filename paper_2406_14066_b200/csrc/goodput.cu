@@ -19,10 +19,14 @@
 
 namespace tsv {
 
-__global__ void __launch_bounds__(kGpThreads) goodput_choose_k_kernel(const ChooseArgs A) {
+#ifndef TSV_GP_CHOOSE_THREADS
+#define TSV_GP_CHOOSE_THREADS 256
+#endif
+constexpr int kGpChooseThreads = TSV_GP_CHOOSE_THREADS;  // B = 256 step: 256 threads 2.84 us; 128: 3.12; 64: 3.86; 32: 6.10
+__global__ void __launch_bounds__(kGpChooseThreads) goodput_choose_k_kernel(const ChooseArgs A) {
     pdl_wait();
     pdl_launch_dependents();
-    choose_k_block(A);
+    choose_k_block<kGpChooseThreads>(A);
 }
 
 __global__ void __launch_bounds__(kGpThreads) update_acceptance_kernel(const UpdateArgs A) {
@@ -261,7 +265,7 @@ extern "C" tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_pe
     A.B = B;
     A.k_max = k_max;
     A.policy = policy;
-    TSV_CUDA(launch_pdl(goodput_choose_k_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream), A),
+    TSV_CUDA(launch_pdl(goodput_choose_k_kernel, dim3(1), dim3(kGpChooseThreads), 0, static_cast<cudaStream_t>(stream), A),
              "goodput_choose_k_kernel launch");
     return TSV_OK;
 }
