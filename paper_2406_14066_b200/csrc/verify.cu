@@ -331,7 +331,10 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
 #endif
 constexpr int kRaceThreads = TSV_RACE_THREADS;
 constexpr int kRaceWarps = kRaceThreads / 32;
-constexpr int kUnroll = 2;
+#ifndef TSV_RACE_UNROLL
+#define TSV_RACE_UNROLL 2
+#endif
+constexpr int kUnroll = TSV_RACE_UNROLL;
 
 #ifndef TSV_TRACE
 #define TSV_TRACE 0
