@@ -1093,7 +1093,7 @@ __device__ __forceinline__ float sum_term(float z, float m, float inv_tau, float
 // for all lanes -- no divergent rescaling) and per-lane sums of expf((z - m) / tau): four
 // exponentials added in fp32, then accumulated in binary64.  Stored as (m, sum).
 #ifndef TSV_STATS_MINB
-#define TSV_STATS_MINB 6
+#define TSV_STATS_MINB 4
 #endif
 __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel(const RaceParams P, LogitPartial* part,
                                                                     int32_t rows_q_max) {
@@ -1118,21 +1118,25 @@ __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel
         const int32_t nq = (col_end - col_begin + 3) >> 2;
         float m = -INFINITY;
         double s = 0.0;
-        auto load2 = [&](int32_t f0, float4 (&z)[2]) {
+#ifndef TSV_STATS_U
+#define TSV_STATS_U 4
+#endif
+        constexpr int SU = TSV_STATS_U;  // float4 per lane per step
+        auto load2 = [&](int32_t f0, float4 (&z)[SU]) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < SU; ++h) {
                 const int32_t f = f0 + 32 * h + lane;
                 z[h] = f < nq ? ldg_stream(z4 + f) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
             }
         };
-        float4 cur[2];
+        float4 cur[SU];
         load2(0, cur);
-        for (int32_t f0 = 0; f0 < nq; f0 += 64) {  // two float4 per lane; the next two in flight
-            float4 nxt[2];
-            if (f0 + 64 < nq) load2(f0 + 64, nxt);
-            float e[8];
+        for (int32_t f0 = 0; f0 < nq; f0 += 32 * SU) {  // SU float4 per lane; the next SU in flight
+            float4 nxt[SU];
+            if (f0 + 32 * SU < nq) load2(f0 + 32 * SU, nxt);
+            float e[4 * SU];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < SU; ++h) {
                 const int32_t v = col_begin + 4 * (f0 + 32 * h + lane);
                 e[4 * h + 0] = cur[h].x;
                 e[4 * h + 1] = v + 1 < col_end ? cur[h].y : -INFINITY;
@@ -1141,7 +1145,7 @@ __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel
             }
             float lm = e[0];
 #pragma unroll
-            for (int t = 1; t < 8; ++t) lm = fmaxf(lm, e[t]);
+            for (int t = 1; t < 4 * SU; ++t) lm = fmaxf(lm, e[t]);
             const float wm = from_ordered_bits(__reduce_max_sync(0xFFFFFFFFu, ordered_bits(lm)));
             if (wm > m) {  // warp-uniform
                 if (m > -INFINITY) s *= static_cast<double>(expf(exp_arg(m, wm, it)));
@@ -1149,15 +1153,15 @@ __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel
             }
             float acc = 0.0f;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < SU; ++h) {
                 float x[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t) x[t] = e[4 * h + t] > -INFINITY ? sum_term(e[4 * h + t], m, it, l2e) : 0.0f;
                 acc = __fadd_rn(acc, __fadd_rn(__fadd_rn(x[0], x[1]), __fadd_rn(x[2], x[3])));
             }
             s += static_cast<double>(acc);
-            cur[0] = nxt[0];
-            cur[1] = nxt[1];
+#pragma unroll
+            for (int h = 0; h < SU; ++h) cur[h] = nxt[h];
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
@@ -1626,7 +1630,7 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
 static RaceParams stats_params(const tsv_verify_args* a, RaceParams P) {
     if (a->chunk > 0 || !TSV_STATS_OWN_CHUNK) return P;
 #ifndef TSV_STATS_ITEMS_PER_WARP
-#define TSV_STATS_ITEMS_PER_WARP 1
+#define TSV_STATS_ITEMS_PER_WARP 2
 #endif
     const int64_t warps = static_cast<int64_t>(sm_count()) * 8 * TSV_STATS_MINB * TSV_STATS_ITEMS_PER_WARP;
     const int64_t cells = 2 * static_cast<int64_t>(a->rows_p) * a->vocab;  // >= (rows_p + rows_q) V
