@@ -58,6 +58,8 @@ struct RaceParams {
     uint32_t k0, k1, step;
     int32_t B, k_max, vocab, vocab_offset, vocab_global, chunk, n_chunks, rows_p;
     uint32_t ks0[10], ks1[10];  // Philox key schedule k + r W (constant bank)
+    int32_t race_update;        // lazy race: one extra CTA runs the alpha update (ua) beside the race
+    UpdateArgs ua;
 };
 
 enum Mode { kLazy = 0, kShard = 1 };
@@ -315,6 +317,45 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     }
 }
 
+// UpdateGlobalAcceptance (Listing 1 line 19) over one CTA of any size (all threads call):
+// exact int64 sums of m and tested, then the EWMA -- the arithmetic of update_block.
+__device__ __forceinline__ void update_cta(const UpdateArgs& A) {
+    __shared__ long long red2[32][2];
+    long long sm = 0, stt = 0;
+    for (int32_t i = threadIdx.x; i < A.B; i += blockDim.x) {
+        const int32_t k = A.row_offsets[i + 1] - A.row_offsets[i] - 1;
+        const int32_t m = __ldcg(A.num_accepted + i);
+        if (m < 0) continue;
+        const long long t = A.estimator == TSV_EST_PROPOSED ? k : (m + (m < k ? 1 : 0));
+        if (A.per_request) {
+            if (t > 0) {
+                const double r = __ddiv_rn(static_cast<double>(m), static_cast<double>(t));
+                A.alpha[i] = __fma_rn(A.decay, __dsub_rn(A.alpha[i], r), r);
+            }
+        } else {
+            sm += m;
+            stt += t;
+        }
+    }
+    if (A.per_request) return;
+    sm = warp_sum_i64(sm);
+    stt = warp_sum_i64(stt);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red2[warp][0] = sm;
+        red2[warp][1] = stt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long a = 0, b = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            a += red2[w][0];
+            b += red2[w][1];
+        }
+        ewma_apply(A.alpha, a, b, A.decay);
+    }
+}
+
 // ------------------------------------------------------------------ 2. the race
 // Warp-independent: every warp races work items -- (request [, position], chunk of P.chunk
 // columns) -- interleaved over all warps of the grid so residual (p and q) and bonus (p
@@ -360,9 +401,14 @@ template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false>
 __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kernel(const RaceParams P) {
     pdl_wait();  // the scan kernel's ReqMeta / rowT / rowkey are complete and visible
     pdl_launch_dependents();
+    const int32_t race_ctas = gridDim.x - (MODE == kLazy && P.race_update ? 1 : 0);
+    if (MODE == kLazy && P.race_update && static_cast<int32_t>(blockIdx.x) == race_ctas) {
+        update_cta(P.ua);  // the accepted counts are final after the scan; runs beside the race
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const int32_t warp_id = blockIdx.x * kRaceWarps + (threadIdx.x >> 5);
-    const int32_t n_warps = gridDim.x * kRaceWarps;
+    const int32_t n_warps = race_ctas * kRaceWarps;
     const int32_t per_req = (MODE == kLazy) ? P.n_chunks : (P.k_max + 1) * P.n_chunks;
     const int32_t n_items = P.B * per_req;
     const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
@@ -1357,6 +1403,8 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.vocab_global = a->vocab_global;
     P.chunk = chunk;
     P.n_chunks = (a->vocab + chunk - 1) / chunk;
+    P.race_update = 0;
+    P.ua = UpdateArgs{};
     P.rows_p = a->rows_p;
     const size_t n_chunks = static_cast<size_t>(P.n_chunks);
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);
@@ -1393,7 +1441,8 @@ static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
     const int64_t n_items = static_cast<int64_t>(P.B) * per_req;
     TSV_REQUIRE(n_items < (1ll << 31), "verify: too many work items");
     const int64_t want = (n_items + kRaceWarps - 1) / kRaceWarps;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * occ));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * occ)) +
+                         ((MODE == kLazy && P.race_update) ? 1 : 0);
     TSV_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kRaceThreads), 0, st, P), "verify_race_kernel launch");
     return TSV_OK;
 }
@@ -1401,6 +1450,14 @@ static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
 template <int MODE>
 static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_t st, const UpdateArgs* ua = nullptr) {
     const bool race_only = (a->flags & TSV_VERIFY_RACE_ONLY) != 0;  // measurement of the dominant kernel
+#ifndef TSV_UPDATE_IN_RACE
+#define TSV_UPDATE_IN_RACE 1
+#endif
+    if (TSV_UPDATE_IN_RACE && MODE == kLazy && ua && !race_only) {  // the alpha update beside the race
+        P.race_update = 1;
+        P.ua = *ua;
+        ua = nullptr;
+    }
     const unsigned scan_blocks = static_cast<unsigned>((a->B + 7) / 8);
     if (!race_only)
         TSV_CUDA(launch_pdl(verify_scan_kernel<MODE>, dim3(scan_blocks), dim3(256), 0, st, P), "verify_scan_kernel launch");
