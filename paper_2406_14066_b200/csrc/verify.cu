@@ -15,11 +15,12 @@
 //     the provably conservative prune test that skips the exact
 //     double-log + IEEE-division score of elements that cannot reach the best score seen,
 //     deferred exact evaluation of survivors, and a packed (score, ~index) u64 key per
-//     row combined with red.max.  No shared memory, no barriers.
+//     row combined with red.max.  No shared memory, no barriers in the race itself; with
+//     tsv_verify_accept_update one extra CTA runs the alpha update beside the race (the
+//     accepted counts are final after the scan).
 //  3. verify_emit_kernel: one warp per request (or p row in shard mode) reads the row key,
 //     falls back to the p_m race when the residual was identically zero (R5), and emits
-//     out_tokens / num_accepted (or the shard tuple); optionally one extra CTA runs the
-//     alpha update.
+//     the correction / bonus token (or the shard tuple).
 // Also here: the lazy two-round vocab sharding kernels (flags / meta / keys / emit), the
 // greedy verify (dense row argmax + first-mismatch emit), the fused softmax-from-logits
 // verify (online-softmax partials + logits scan; the race and emit take a LOGITS flag),
