@@ -752,7 +752,9 @@ def test_fused_lookup_choose_k_equals_separate(tsv):
         assert int(k2.item()) == ok
 
 
-def test_fused_verify_update_equals_separate(tsv):
+@pytest.mark.parametrize("est", [0, 1])  # TESTED (default), PROPOSED
+def test_fused_verify_update_equals_separate(tsv, est):
+    # the fused update runs as an extra CTA of the race kernel: same alpha bits as the separate call
     vb = synth.make_verify_batch(B=256, V=32000, k_max=8, lam=0.7, seed=22).to(DEV)
     for per in (False, True):
         na = torch.empty(256, dtype=torch.int32, device=DEV)
@@ -763,10 +765,10 @@ def test_fused_verify_update_equals_separate(tsv):
         a0 = torch.rand(256 if per else 1, dtype=torch.float64, device=DEV, generator=torch.Generator(DEV).manual_seed(1))
         alpha1 = a0.clone()
         tsv._check(tsv.lib().tsv_verify_accept(tsv.ctypes.byref(a), tsv._stream(None)))
-        tsv.tsv_update_acceptance(alpha1, na, vb.row_offsets, 0.9, per_request=per)
+        tsv.tsv_update_acceptance(alpha1, na, vb.row_offsets, 0.9, estimator=est, per_request=per)
         out1, na1 = out.clone(), na.clone()
         alpha2 = a0.clone()
-        tsv.tsv_verify_accept_update(a, alpha2, 0.9, per_request=per)
+        tsv.tsv_verify_accept_update(a, alpha2, 0.9, estimator=est, per_request=per)
         torch.cuda.synchronize()
         assert torch.equal(out1, out) and torch.equal(na1, na)
         assert torch.equal(alpha1.view(torch.int64), alpha2.view(torch.int64))
