@@ -11,6 +11,10 @@ ragged k in [0, 8], V = 32000, dense fp32 p and q, lambda = 0.7) -> alpha update
 Inputs are seeded synthetic data (synth/), resident in HBM, rotating over R sets
 whose footprint is > 3x L2 so no step reads another's rows from L2.
 Metric: generated (verified) tokens/s = sum_i (m_i + 1) / time, whole job.
+Roofline: the dominant kernel (verify_race_kernel) timed alone -- 64 race-only launches per graph
+(TSV_VERIFY_RACE_ONLY) over per-step workspaces -- against its algorithmic bytes (the rows the
+steps actually select) and MEASURED_PEAKS.json's HBM copy bandwidth; the whole verify call is
+reported beside it.  e2e: the same ABI calls with the inputs in pinned host memory.
 Multi-GPU: request-sharded weak scaling -- every rank runs its own B = 256 batch with
 global request ids; no data-path collective; time = max over ranks.
 """
