@@ -281,7 +281,7 @@ def run_ours(args, rank, world, local_rank):
         s = t % R
         vb = vbs[s]
         a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t,
-                                 K_MAX, na, outt, None, ws, chunk=args.chunk)
+                                 K_MAX, na, outt, None, ws, chunk=args.chunk, flags=tsv.VERIFY_META_READY)
         vargs.append(a)
     side = torch.cuda.Stream()
     with torch.cuda.stream(side):

@@ -161,6 +161,13 @@ typedef struct tsv_verify_args {
                                   /* max-combines into the same row keys, so outputs  */
                                   /* are unchanged.  bench.py times the dominant     */
                                   /* kernel with it.                                  */
+#define TSV_VERIFY_META_READY 8   /* row_offsets, draft_tokens and request_ids were   */
+                                  /* NOT written by the kernel immediately preceding  */
+                                  /* this call on the stream (e.g. they come from the */
+                                  /* proposer, before the target forward): the scan   */
+                                  /* reads them while that kernel drains and waits   */
+                                  /* only before reading p and q (tsv_verify_accept, */
+                                  /* tsv_verify_accept_update)                        */
 
 /* Workspace: device scratch for per-request scan results and per-chunk race
  * keys (size from tsv_verify_workspace_size; no initialisation needed).  One

@@ -59,6 +59,7 @@ struct RaceParams {
     uint32_t k0, k1, step;
     int32_t B, k_max, vocab, vocab_offset, vocab_global, chunk, n_chunks, rows_p;
     uint32_t ks0[10], ks1[10];  // Philox key schedule k + r W (constant bank)
+    int32_t meta_ready;         // TSV_VERIFY_META_READY: the scan reads row_offsets/drafts/rids before its wait
     int32_t race_update;        // lazy race: one extra CTA runs the alpha update (ua) beside the race
     UpdateArgs ua;
 };
@@ -248,8 +249,12 @@ __device__ __forceinline__ void emit_prefix(const RaceParams& P, int32_t i, int3
 // Shard: writes the accept / owner flags of every p row of the request into its tuple.
 template <int MODE>
 __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
-    pdl_wait();               // inputs of this step are complete
-    pdl_launch_dependents();  // let the race kernel launch and set up while we scan
+    // TSV_VERIFY_META_READY: row_offsets / draft_tokens / request_ids were not written by the
+    // preceding kernel, so they are read while it drains; p and q only after the wait.
+    if (!P.meta_ready) {
+        pdl_wait();               // inputs of this step are complete
+        pdl_launch_dependents();  // let the race kernel launch and set up while we scan
+    }
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= P.B) return;
     const int lane = threadIdx.x & 31;
@@ -261,8 +266,12 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     const uint32_t rid = P.rids[i];
     int32_t x = -1;
     bool bad = false, acc = false, own = false;
+    if (ok && lane < k) x = P.drafts[qbase + lane];
+    if (P.meta_ready) {
+        pdl_wait();
+        pdl_launch_dependents();
+    }
     if (ok && lane < k) {
-        x = P.drafts[qbase + lane];
         bad = x < 0 || x >= P.vocab_global;
         const int32_t xl = x - P.vocab_offset;
         own = !bad && xl >= 0 && xl < P.vocab;
@@ -1406,6 +1415,7 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.n_chunks = (a->vocab + chunk - 1) / chunk;
     P.race_update = 0;
     P.ua = UpdateArgs{};
+    P.meta_ready = (a->flags & TSV_VERIFY_META_READY) ? 1 : 0;
     P.rows_p = a->rows_p;
     const size_t n_chunks = static_cast<size_t>(P.n_chunks);
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);

@@ -95,9 +95,11 @@ class SpecStep:
         self.fused = fused
         self.args = []
         for vb in inp.verify:
+            # the batch's row_offsets / drafts / request ids are inputs of the step, never written by
+            # the step's own kernels (the proposer's output goes through the target forward first)
             a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids,
                                      inp.seed, 0, K, self.num_accepted, self.out_tokens, self.status,
-                                     chunk=chunk)
+                                     chunk=chunk, flags=tsv.VERIFY_META_READY)
             self.args.append(a)
         ws_bytes = max(tsv.tsv_verify_workspace_size(a) for a in self.args)
         self.workspace = tsv.alloc_workspace(ws_bytes, dev)

@@ -26,6 +26,7 @@ DEVSTATUS_NO_WEIGHT = 4
 VERIFY_NO_PRUNE = 1
 VERIFY_SHARD_DENSE = 2
 VERIFY_RACE_ONLY = 4  # measurement: the race kernel alone over a previous call's workspace
+VERIFY_META_READY = 8  # row_offsets/drafts/request_ids not written by the preceding kernel on the stream
 LOOKUP_CHOOSE_SCRATCH = 512  # TSV_LOOKUP_CHOOSE_SCRATCH
 POLICY_DRAFT = 0
 POLICY_PLD = 1

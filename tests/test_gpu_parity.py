@@ -752,6 +752,15 @@ def test_fused_lookup_choose_k_equals_separate(tsv):
         assert int(k2.item()) == ok
 
 
+def test_meta_ready_flag_same_outputs(tsv):
+    # TSV_VERIFY_META_READY only moves the scan's first loads before its grid-dependency wait
+    vb = synth.make_verify_batch(B=200, V=32000, k_max=8, lam=0.6, seed=31)
+    ona, oout, _ = oracle_verify(vb, 3, 4)
+    for flags in (tsv.VERIFY_META_READY, tsv.VERIFY_META_READY | tsv.VERIFY_NO_PRUNE):
+        na, out, st = gpu_verify(tsv, vb, 3, 4, flags=flags)
+        assert (na == ona).all() and (out == oout).all() and st == 0
+
+
 @pytest.mark.parametrize("est", [0, 1])  # TESTED (default), PROPOSED
 def test_fused_verify_update_equals_separate(tsv, est):
     # the fused update runs as an extra CTA of the race kernel: same alpha bits as the separate call
