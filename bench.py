@@ -487,6 +487,8 @@ def run_config4(args, rank, world, local_rank):
     unsharded = args.shard_mode == "none"
     comm = None if unsharded else (tsv.P2PComm(rank, world, B_max=B) if p2p else tsv.Comm(rank, world))
     flags = tsv.VERIFY_SHARD_DENSE if args.shard_mode == "dense" else 0
+    if unsharded:  # the batch's offsets / drafts / ids are inputs, not written by the preceding kernel
+        flags = tsv.VERIFY_META_READY
     entry = tsv.lib().tsv_verify_accept_sharded_p2p if p2p else tsv.lib().tsv_verify_accept_sharded
 
     def run_sharded(a, stream=None):
@@ -560,7 +562,7 @@ def run_config4(args, rank, world, local_rank):
         m = na.cpu().numpy()
         k = sets[t % R][0].k.cpu().numpy()
         tok += int((m + 1).sum())
-        dense = flags != 0
+        dense = args.shard_mode == "dense"
         rows = (2 * k + 1) if dense else (1 + (m < k))  # rows streamed per request (all ranks together)
         vbytes += float((rows * V4 * 4).sum()) / world
     tok_per_step, vbytes = tok / gl, vbytes / gl
@@ -587,7 +589,7 @@ def run_config4(args, rank, world, local_rank):
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                      "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),
-        "gpu_launches": (3 if (flags or unsharded) else 5) * steps,
+        "gpu_launches": (3 if (args.shard_mode == "dense" or unsharded) else 5) * steps,
         "e2e": None,
         "tokens_per_step": tok_per_step,
         "requests_per_s": B / (ms_step * 1e-3),
