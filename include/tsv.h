@@ -29,9 +29,13 @@
  *    means nothing was launched.  tsv_last_error() returns a thread-local
  *    message for the last non-OK status of the calling thread.
  *  - Data errors that can only be seen on the device (token id out of range,
- *    ragged offsets decreasing, k_i > k_max) never trap: the affected
- *    request's outputs are -1 and, when `device_status` is non-NULL, the
- *    matching TSV_DEVSTATUS_* bit is OR-ed into *device_status.
+ *    ragged offsets decreasing or reaching past rows_p / the draft rows,
+ *    k_i > k_max, a context longer than TSV_MAX_CONTEXT) never trap and
+ *    never touch memory outside the caller's arrays: the affected request's
+ *    outputs are -1 and, when `device_status` is non-NULL, the matching
+ *    TSV_DEVSTATUS_* bit is OR-ed into *device_status.
+ *  - Workspaces: a NULL or too small workspace / scratch returns
+ *    TSV_ERR_WORKSPACE (nothing launched).
  *  - Results are a pure function of (inputs, seed, step, request_ids): they do
  *    not depend on grid size, chunking, vocab sharding, batch order or stream.
  *  - Floating point: no fast-math, no FTZ; IEEE binary32 for probabilities
@@ -48,7 +52,7 @@
 extern "C" {
 #endif
 
-#define TSV_ABI_VERSION 1
+#define TSV_ABI_VERSION 2  /* 2: device_status on the lookups, step_counts in tsv_verify_args */
 
 #if defined(__GNUC__)
 #define TSV_API __attribute__((visibility("default")))
@@ -62,7 +66,8 @@ typedef enum {
     TSV_ERR_CUDA = 2,               /* a CUDA runtime call failed                   */
     TSV_ERR_NCCL = 3,               /* NCCL unavailable or an NCCL call failed      */
     TSV_ERR_UNSUPPORTED_DEVICE = 4, /* current device is not sm_100                 */
-    TSV_ERR_WORKSPACE = 5           /* workspace NULL or smaller than required      */
+    TSV_ERR_WORKSPACE = 5           /* workspace / scratch NULL or smaller than     */
+                                    /* required (its *_workspace_size call)         */
 } tsv_status;
 
 /* bits OR-ed into *device_status by the kernels */
@@ -71,6 +76,8 @@ typedef enum {
 #define TSV_DEVSTATUS_NO_WEIGHT 4u  /* selected p row has no positive entry        */
 #define TSV_DEVSTATUS_P2P_TIMEOUT 8u /* a peer-memory exchange wait gave up (a peer
                                         never arrived); outputs are not valid      */
+#define TSV_DEVSTATUS_BAD_CONTEXT 16u /* lookup: ctx_offsets negative or decreasing,
+                                          or L_i > TSV_MAX_CONTEXT                 */
 
 TSV_API const char* tsv_last_error(void);
 TSV_API int tsv_abi_version(void);
@@ -91,6 +98,10 @@ TSV_API int tsv_abi_version(void);
  *   k_fixed      FIXED_PROPOSED_LEN, 1..TSV_MAX_K (Listing 1 line 26)
  *   proposals    int32 [B, k_fixed] out, -1 padded
  *   proposal_len int32 [B] out (0..k_fixed)
+ *   device_status int32 [1] nullable; TSV_DEVSTATUS_BAD_CONTEXT is OR-ed in for a
+ *                request whose offsets are negative / decreasing or whose L_i >
+ *                TSV_MAX_CONTEXT (the kernel packs the end position in 20 bits);
+ *                that request proposes nothing (length 0, all -1)
  * Errors: INVALID_ARG for B < 0, bad n/k range, NULL arrays (B > 0).
  * ------------------------------------------------------------------------ */
 #define TSV_MAX_CONTEXT (1 << 20)
@@ -99,7 +110,8 @@ TSV_API int tsv_abi_version(void);
 
 TSV_API tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                               int32_t n_min, int32_t n_max, int32_t k_fixed,
-                              int32_t* proposals, int32_t* proposal_len, void* stream);
+                              int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
+                              void* stream);
 
 /* --------------------------------------------------------------------------
  * Verify / accept.  PAPER.md:18 [AD] "we utilize rejection sampling to
@@ -151,6 +163,12 @@ typedef struct tsv_verify_args {
                                   /* up to 16384: a tuning / test knob that never   */
                                   /* changes results                                */
     int32_t flags;                /* TSV_VERIFY_* bits                              */
+    int64_t* step_counts;         /* nullable, device [2] out: (sum_i m_i, sum_i     */
+                                  /* tested_i) over the valid requests, tested_i =  */
+                                  /* m_i + [m_i < k_i] -- the per-step numerator and */
+                                  /* denominator of the acceptance-rate estimate    */
+                                  /* (R18); written by every verify */
+                                  /* flavour (lazy, greedy, logits, sharded)        */
 } tsv_verify_args;
 
 #define TSV_VERIFY_NO_PRUNE 1     /* evaluate every race element exactly (test)     */
@@ -161,13 +179,22 @@ typedef struct tsv_verify_args {
                                   /* max-combines into the same row keys, so outputs  */
                                   /* are unchanged.  bench.py times the dominant     */
                                   /* kernel with it.                                  */
-#define TSV_VERIFY_META_READY 8   /* row_offsets, draft_tokens and request_ids were   */
-                                  /* NOT written by the kernel immediately preceding  */
-                                  /* this call on the stream (e.g. they come from the */
-                                  /* proposer, before the target forward): the scan   */
-                                  /* reads them while that kernel drains and waits   */
-                                  /* only before reading p and q (tsv_verify_accept, */
-                                  /* tsv_verify_accept_update)                        */
+#define TSV_VERIFY_META_READY 8   /* Contract: row_offsets, draft_tokens and          */
+                                  /* request_ids are COMPLETE before the kernel that  */
+                                  /* immediately precedes this call on the stream     */
+                                  /* could start, i.e. no kernel still in flight when */
+                                  /* this call's first kernel launches writes them    */
+                                  /* (e.g. they come from the proposer, before the    */
+                                  /* target forward).  Under PDL a kernel may launch  */
+                                  /* while its predecessor drains, so "not written by */
+                                  /* the preceding kernel" is not enough if that      */
+                                  /* kernel itself triggered early.  The scan then    */
+                                  /* reads them before its grid-dependency wait and   */
+                                  /* waits only before reading p and q.  Honoured by  */
+                                  /* tsv_verify_accept and tsv_verify_accept_update;  */
+                                  /* ignored by every other entry point (sharded,     */
+                                  /* greedy, logits).  libtsv's own kernels trigger   */
+                                  /* their dependents only after their own wait.      */
 
 /* Workspace: device scratch for per-request scan results and per-chunk race
  * keys (size from tsv_verify_workspace_size; no initialisation needed).  One
@@ -350,7 +377,8 @@ TSV_API tsv_status tsv_goodput_choose_k_batched(const double* alpha, const int32
  * Outputs are identical to the two separate calls.
  *   counter  device scratch of TSV_LOOKUP_CHOOSE_SCRATCH bytes (8-byte aligned),
  *            zero-filled once after allocation (tsv_workspace_clear); every call
- *            leaves it zero.  One per stream.
+ *            leaves it zero.  One per stream.  NULL: TSV_ERR_WORKSPACE.
+ *   device_status as tsv_propose_lookup.
  * ------------------------------------------------------------------------ */
 #define TSV_LOOKUP_CHOOSE_SCRATCH 512
 TSV_API tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
@@ -360,7 +388,7 @@ TSV_API tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int32_t
                                        const int32_t* ctx_len, tsv_latency_model target,
                                        double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
                                        double* goodput_out, int32_t* k_per_request,
-                                       uint32_t* counter, void* stream);
+                                       uint32_t* counter, int32_t* device_status, void* stream);
 
 /* --------------------------------------------------------------------------
  * Acceptance-rate update: UpdateGlobalAcceptance (Listing 1 line 19,

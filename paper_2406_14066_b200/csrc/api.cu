@@ -168,7 +168,7 @@ extern "C" tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_co
     TSV_TRY(nccl_ready());
     size_t need = 0, slots = 0;
     TSV_TRY(tsv_verify_sharded_workspace_size(a, comm->world, &need));
-    TSV_REQUIRE(a->workspace && a->workspace_bytes >= need, "tsv_verify_accept_sharded: workspace too small (%llu < %llu)",
+    TSV_REQUIRE_WS(a->workspace && a->workspace_bytes >= need, "tsv_verify_accept_sharded: workspace too small (%llu < %llu)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)need);
     if (a->B == 0) return TSV_OK;
     TSV_TRY(tsv_verify_workspace_size(a, &slots));

@@ -25,6 +25,15 @@ tsv_status cuda_status(cudaError_t e, const char* what);
         }                                              \
     } while (0)
 
+// workspace NULL or smaller than required (TSV_ERR_WORKSPACE, tsv.h)
+#define TSV_REQUIRE_WS(cond, ...)                      \
+    do {                                               \
+        if (!(cond)) {                                 \
+            ::tsv::set_error(__VA_ARGS__);             \
+            return TSV_ERR_WORKSPACE;                  \
+        }                                              \
+    } while (0)
+
 #define TSV_CUDA(call, what)                                               \
     do {                                                                   \
         cudaError_t e__ = (call);                                          \

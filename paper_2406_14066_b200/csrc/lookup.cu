@@ -167,14 +167,20 @@ template <bool FUSED>
 __global__ void __launch_bounds__(kLookupThreads)
     ngram_lookup_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ ctx_offsets, int32_t B,
                         int32_t n_min, int32_t n_max, int32_t K, int32_t* __restrict__ proposals,
-                        int32_t* __restrict__ proposal_len, ChooseArgs ca, uint32_t* counter) {
+                        int32_t* __restrict__ proposal_len, ChooseArgs ca, uint32_t* counter, int32_t* devstatus) {
     __shared__ uint32_t s_red[kLookupThreads / 32];
     pdl_wait();
     pdl_launch_dependents();
     const int32_t i = blockIdx.x;
     const int tid = threadIdx.x;
     const int32_t off = __ldg(ctx_offsets + i);
-    const int32_t L = __ldg(ctx_offsets + i + 1) - off;
+    const int32_t end = __ldg(ctx_offsets + i + 1);
+    // device-side data errors (tsv.h): offsets negative or decreasing, or L_i > TSV_MAX_CONTEXT (the
+    // packed key holds e in 20 bits) -> no proposal and TSV_DEVSTATUS_BAD_CONTEXT
+    const int64_t L64 = static_cast<int64_t>(end) - off;
+    const bool bad_ctx = off < 0 || L64 < 0 || L64 > TSV_MAX_CONTEXT;
+    const int32_t L = bad_ctx ? 0 : static_cast<int32_t>(L64);
+    if (bad_ctx && tid == 0 && devstatus) atomicOr(reinterpret_cast<unsigned int*>(devstatus), TSV_DEVSTATUS_BAD_CONTEXT);
     const int32_t* c = ctx + off;
     int32_t my_len = 0;  // this request's proposal length (warp 0)
     uint32_t best = 0;
@@ -231,7 +237,8 @@ using namespace tsv;
 
 extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                                          int32_t n_min, int32_t n_max, int32_t k_fixed,
-                                         int32_t* proposals, int32_t* proposal_len, void* stream) {
+                                         int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
+                                         void* stream) {
     TSV_REQUIRE(B >= 0, "tsv_propose_lookup: B < 0 (%d)", B);
     TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
                 "tsv_propose_lookup: need 1 <= n_min (%d) <= n_max (%d) <= %d", n_min, n_max, TSV_MAX_NGRAM);
@@ -242,7 +249,7 @@ extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_
     ChooseArgs none = {};
     TSV_CUDA(launch_pdl(ngram_lookup_kernel<false>, dim3(B), dim3(kLookupThreads), 0,
                         static_cast<cudaStream_t>(stream), ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals,
-                        proposal_len, none, static_cast<uint32_t*>(nullptr)),
+                        proposal_len, none, static_cast<uint32_t*>(nullptr), device_status),
              "ngram_lookup_kernel launch");
     return TSV_OK;
 }
@@ -254,13 +261,14 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
                                                   const int32_t* ctx_len, tsv_latency_model target,
                                                   double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
                                                   double* goodput_out, int32_t* k_per_request,
-                                                  uint32_t* counter, void* stream) {
+                                                  uint32_t* counter, int32_t* device_status, void* stream) {
     TSV_REQUIRE(B >= 1, "tsv_propose_lookup_choose_k: B must be >= 1 (got %d)", B);
     TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
                 "tsv_propose_lookup_choose_k: need 1 <= n_min (%d) <= n_max (%d) <= %d", n_min, n_max, TSV_MAX_NGRAM);
     TSV_REQUIRE(k_fixed >= 1 && k_fixed <= TSV_MAX_K, "tsv_propose_lookup_choose_k: k_fixed %d outside [1, %d]", k_fixed, TSV_MAX_K);
-    TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len && alpha && ctx_len && k_out && counter,
+    TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len && alpha && ctx_len && k_out,
                 "tsv_propose_lookup_choose_k: a required array is NULL");
+    TSV_REQUIRE_WS(counter != nullptr, "tsv_propose_lookup_choose_k: scratch (counter) is NULL");
     TSV_REQUIRE((reinterpret_cast<uintptr_t>(counter) & 7u) == 0, "tsv_propose_lookup_choose_k: scratch must be 8-byte aligned");
     TSV_TRY(check_device());
     ChooseArgs A = {};
@@ -280,7 +288,7 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
     A.policy = TSV_POLICY_PLD;
     TSV_CUDA(launch_pdl(ngram_lookup_kernel<true>, dim3(B), dim3(kLookupThreads), 0,
                         static_cast<cudaStream_t>(stream), ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals,
-                        proposal_len, A, counter),
+                        proposal_len, A, counter, device_status),
              "ngram_lookup_kernel launch");
     return TSV_OK;
 }

@@ -49,6 +49,7 @@ struct RaceParams {
     int32_t* num_accepted;
     int32_t* out_tokens;
     int32_t* devstatus;
+    long long* step_counts;    // nullable: (sum m_i, sum tested_i) over valid requests (tsv_verify_args)
     ReqMeta* meta;             // [B]
     uint32_t* rowT;            // [n_key_rows] shared race threshold per raced row (float bits)
     unsigned long long* rowkey;  // [n_key_rows] max race key per raced row (0: nothing evaluated)
@@ -218,6 +219,47 @@ __device__ __forceinline__ void report(int32_t* devstatus, uint32_t bits) {
     if (devstatus && bits) atomicOr(reinterpret_cast<unsigned int*>(devstatus), bits);
 }
 
+// Request i's rows lie inside the allocations (tsv.h: device-side data errors): k_i in
+// [0, k_max], its p rows r0 .. r1-1 below rows_lim, and its drafts / q rows qbase .. qbase+k-1
+// (qbase = r0 - i) below rows_lim - B.  rows_lim is the host-known rows_p, or for the dense
+// passes min(row_offsets[B], rows_p) -- the rows they actually covered.  int64: no overflow.
+__device__ __forceinline__ bool request_rows_ok(int32_t r0, int32_t r1, int32_t i, int32_t k_max, int32_t rows_lim,
+                                                int32_t B) {
+    const int64_t k = static_cast<int64_t>(r1) - r0 - 1, qbase = static_cast<int64_t>(r0) - i;
+    return k >= 0 && k <= k_max && qbase >= 0 && r1 <= rows_lim && qbase + k <= static_cast<int64_t>(rows_lim) - B;
+}
+
+// step_counts (tsv.h): (sum m_i, sum tested_i), tested_i = m_i + [m_i < k_i], over the valid
+// requests of the call.  Zeroed by the call's first kernel (after its grid-dependency wait, so
+// the previous call's adds are complete); the final kernel adds one shared-memory sum per CTA.
+// Called by every thread of the CTA; `mine`: this thread carries request (m, k) (warp lane 0).
+__device__ __forceinline__ void zero_step_counts(long long* sc) {
+    if (sc && blockIdx.x == 0 && threadIdx.x == 0) {
+        sc[0] = 0;
+        sc[1] = 0;
+    }
+}
+__device__ __forceinline__ void add_step_counts(long long* sc, bool mine, int32_t m, int32_t k) {
+    __shared__ unsigned long long s_c[2];
+    if (threadIdx.x == 0) s_c[0] = s_c[1] = 0ull;
+    __syncthreads();
+    if (mine && m >= 0) {
+        atomicAdd(&s_c[0], static_cast<unsigned long long>(m));
+        atomicAdd(&s_c[1], static_cast<unsigned long long>(m + (m < k ? 1 : 0)));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (s_c[0] | s_c[1])) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(sc), s_c[0]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(sc) + 1, s_c[1]);
+    }
+}
+
+// Rows covered by a dense pass over the batch: row_offsets[B] clamped to [0, rows_p].
+__device__ __forceinline__ int32_t dense_rows(const int32_t* row_offsets, int32_t B, int32_t rows_p) {
+    const int32_t r = row_offsets[B];
+    return r < 0 ? 0 : (r > rows_p ? rows_p : r);
+}
+
 // Emit (R1-R4 step 4): lanes j <= k_max of one warp.
 __device__ __forceinline__ void emit(const RaceParams& P, int32_t i, int32_t qbase, int32_t m, int32_t t) {
     const int lane = threadIdx.x & 31;
@@ -262,7 +304,7 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     const int32_t r1 = P.row_offsets[i + 1];
     const int32_t k = r1 - r0 - 1;
     const int32_t qbase = r0 - i;
-    int32_t ok = (k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p) ? 1 : 0;
+    int32_t ok = request_rows_ok(r0, r1, i, P.k_max, P.rows_p, P.B) ? 1 : 0;
     const uint32_t rid = P.rids[i];
     int32_t x = -1;
     bool bad = false, acc = false, own = false;
@@ -271,6 +313,7 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
         pdl_wait();
         pdl_launch_dependents();
     }
+    zero_step_counts(P.step_counts);
     if (ok && lane < k) {
         bad = x < 0 || x >= P.vocab_global;
         const int32_t xl = x - P.vocab_offset;
@@ -564,13 +607,13 @@ __device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_
 }
 
 template <int MODE, bool PRUNE, bool LOGITS = false>
-__device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
+__device__ __forceinline__ int2 emit_unit(const RaceParams& P, int32_t unit) {  // (m, k) of a valid request
     const int lane = threadIdx.x & 31;
-    if (unit >= P.B) return;
+    if (unit >= P.B) return make_int2(-1, 0);
     // lazy: the row key is loaded next to the meta (one round trip)
     uint64_t key = (MODE == kLazy) ? P.rowkey[unit] : 0ull;
     const ReqMeta rm = P.meta[unit];
-    if (rm.ok != 1) return;  // lazy: emitted by the scan kernel; shard: flagged by the combine
+    if (rm.ok != 1) return make_int2(-1, 0);  // lazy: emitted by the scan kernel; shard: flagged by the combine
     if (MODE == kLazy) {
         if (key == 0 && rm.m < rm.k) {  // R5: residual identically zero -> race over p_m
             const float4 ls = LOGITS ? P.lstats[unit] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -595,6 +638,7 @@ __device__ __forceinline__ void emit_unit(const RaceParams& P, int32_t unit) {
             }
         }
     }
+    return make_int2(rm.m, rm.k);
 }
 
 // UPDATE: one extra CTA (the last) runs UpdateGlobalAcceptance (Listing 1 line 19) next to
@@ -609,25 +653,22 @@ __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P, Up
         update_block(ua);
         return;
     }
-    emit_unit<MODE, PRUNE, LOGITS>(P, blockIdx.x * 8 + (threadIdx.x >> 5));
+    const int2 mk = emit_unit<MODE, PRUNE, LOGITS>(P, blockIdx.x * 8 + (threadIdx.x >> 5));
+    if (MODE == kLazy && P.step_counts) add_step_counts(P.step_counts, (threadIdx.x & 31) == 0, mk.x, mk.y);
 }
 
 // ------------------------------------------------------------------------ shard combine
 // One warp per request: OR the accept flags of the G shards, scan m, take the max key of
 // row m over shards (fallback keys if every shard's residual was zero), emit.
-__global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_tuple* __restrict__ g,
-                                            int32_t G, int32_t rows_p) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int32_t warps_per_block = blockDim.x >> 5;
-    const int32_t i = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
-    if (i >= P.B) return;
+__device__ __forceinline__ int2 combine_unit(const RaceParams& P, const tsv_shard_tuple* __restrict__ g, int32_t G,
+                                             int32_t rows_p, int32_t i) {
+    if (i >= P.B) return make_int2(-1, 0);
     const int lane = threadIdx.x & 31;
     const int32_t r0 = P.row_offsets[i];
     const int32_t r1 = P.row_offsets[i + 1];
     const int32_t k = r1 - r0 - 1;
     const int32_t qbase = r0 - i;
-    const bool ok = k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= rows_p;
+    const bool ok = request_rows_ok(r0, r1, i, P.k_max, rows_p, P.B);
     uint32_t flags = 0;
     bool bad = false;
     if (ok && lane < k) {
@@ -641,7 +682,7 @@ __global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_
     if (!ok || badm) {
         emit(P, i, 0, -1, -1);
         if (lane == 0) report(P.devstatus, ok ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
-        return;
+        return make_int2(-1, 0);
     }
     const uint32_t kmask = k > 0 ? ((1u << k) - 1u) : 0u;
     const uint32_t rej = ~accm & kmask;
@@ -657,6 +698,16 @@ __global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_
     if (key == 0 && m < k) key = fb;
     emit(P, i, qbase, m, key ? key_index(key) : -1);
     if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+    return make_int2(m, k);
+}
+
+__global__ void verify_shard_combine_kernel(const RaceParams P, const tsv_shard_tuple* __restrict__ g,
+                                            int32_t G, int32_t rows_p) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int32_t i = blockIdx.x * static_cast<int32_t>(blockDim.x >> 5) + static_cast<int32_t>(threadIdx.x >> 5);
+    const int2 mk = combine_unit(P, g, G, rows_p, i);
+    if (P.step_counts) add_step_counts(P.step_counts, (threadIdx.x & 31) == 0, mk.x, mk.y);
 }
 
 // ------------------------------------------------------------ lazy two-round vocab sharding
@@ -672,7 +723,7 @@ __device__ __forceinline__ unsigned long long shard_flags_mask(const RaceParams&
     const int32_t r1 = P.row_offsets[i + 1];
     const int32_t k = r1 - r0 - 1;
     const int32_t qbase = r0 - i;
-    const bool ok = k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p;
+    const bool ok = request_rows_ok(r0, r1, i, P.k_max, P.rows_p, P.B);
     bool acc = false, own = false;
     if (ok && lane < k) {
         const int32_t x = P.drafts[qbase + lane];
@@ -696,6 +747,7 @@ __device__ __forceinline__ unsigned long long shard_flags_mask(const RaceParams&
 __global__ void __launch_bounds__(256) verify_shard_flags_kernel(const RaceParams P, unsigned long long* masks) {
     pdl_wait();
     pdl_launch_dependents();
+    zero_step_counts(P.step_counts);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= P.B) return;
     const unsigned long long mask = shard_flags_mask(P, i);
@@ -710,7 +762,7 @@ __device__ __forceinline__ ReqMeta shard_meta_from_masks(const RaceParams& P, in
     const int32_t r1 = P.row_offsets[i + 1];
     const int32_t k = r1 - r0 - 1;
     const int32_t qbase = r0 - i;
-    int32_t ok = (k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p) ? 1 : 0;
+    int32_t ok = request_rows_ok(r0, r1, i, P.k_max, P.rows_p, P.B) ? 1 : 0;
     int32_t x = -1;
     bool bad = false;
     if (ok && lane < k) {
@@ -769,23 +821,29 @@ __global__ void __launch_bounds__(256) verify_shard_keys_kernel(const RaceParams
     }
 }
 
-__global__ void __launch_bounds__(256) verify_shard_emit_kernel(const RaceParams P, const unsigned long long* masks,
-                                                                const unsigned long long* keys) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= P.B) return;
+__device__ __forceinline__ int2 shard_emit_unit(const RaceParams& P, const unsigned long long* masks,
+                                                const unsigned long long* keys, int32_t i) {
+    if (i >= P.B) return make_int2(-1, 0);
     const int lane = threadIdx.x & 31;
     const ReqMeta rm = shard_meta_from_masks(P, i, masks[i]);
     if (rm.ok != 1) {
         emit(P, i, 0, -1, -1);
         if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
-        return;
+        return make_int2(-1, 0);
     }
     uint64_t key = keys[2 * i];
     if (key == 0 && rm.m < rm.k) key = keys[2 * i + 1];
     emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
     if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+    return make_int2(rm.m, rm.k);
+}
+
+__global__ void __launch_bounds__(256) verify_shard_emit_kernel(const RaceParams P, const unsigned long long* masks,
+                                                                const unsigned long long* keys) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int2 mk = shard_emit_unit(P, masks, keys, blockIdx.x * 8 + (threadIdx.x >> 5));
+    if (P.step_counts) add_step_counts(P.step_counts, (threadIdx.x & 31) == 0, mk.x, mk.y);
 }
 
 // ------------------------------------------------ vocab sharding over peer memory (NEXT 3)
@@ -889,6 +947,7 @@ __global__ void __launch_bounds__(64) p2p_allreduce_i64_kernel(int64_t* data, in
 __global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams P, const P2PView V) {
     pdl_wait();
     pdl_launch_dependents();
+    zero_step_counts(P.step_counts);
     const uint32_t e = p2p_load_epoch(V);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= P.B) return;
@@ -949,6 +1008,7 @@ __global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P
     pdl_launch_dependents();
     const uint32_t e = p2p_load_epoch(V);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    int2 mk = make_int2(-1, 0);
     if (i < P.B) {
         const int lane = threadIdx.x & 31;
         const ReqMeta rm = P.meta[i];  // written by this rank's meta kernel (same m_i on every rank)
@@ -975,8 +1035,10 @@ __global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P
             if (key == 0 && rm.m < rm.k) key = fb;
             emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
             if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+            mk = make_int2(rm.m, rm.k);
         }
     }
+    if (P.step_counts) add_step_counts(P.step_counts, (threadIdx.x & 31) == 0, mk.x, mk.y);
     // advance the device epoch once every CTA of this kernel has read it (last CTA, GPU scope)
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -989,9 +1051,10 @@ __global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P
 }
 
 // ------------------------------------------------------------------ greedy verify (NEXT 2)
-__global__ void __launch_bounds__(256) clear_u64_kernel(unsigned long long* p, int64_t n) {
+__global__ void __launch_bounds__(256) clear_u64_kernel(unsigned long long* p, int64_t n, long long* step_counts) {
     pdl_wait();  // the previous call's readers of these slots are done
     pdl_launch_dependents();
+    zero_step_counts(step_counts);
     const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 1024 + threadIdx.x;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -1020,8 +1083,8 @@ __global__ void __launch_bounds__(256, TSV_GREEDY_MINB) verify_greedy_argmax_ker
     const int lane = threadIdx.x & 31;
     const int32_t warp_id = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int32_t n_warps = gridDim.x * 8;
-    const int32_t rows = P.row_offsets[P.B];  // p rows that belong to requests
-    const int64_t n_items = static_cast<int64_t>(rows > 0 ? rows : 0) * P.n_chunks;
+    const int32_t rows = dense_rows(P.row_offsets, P.B, P.rows_p);  // p rows that belong to requests
+    const int64_t n_items = static_cast<int64_t>(rows) * P.n_chunks;
     for (int64_t item = warp_id; item < n_items; item += n_warps) {
         const int32_t r = static_cast<int32_t>(item % rows);  // row-minor: neighbours stream different rows
         const int32_t c = static_cast<int32_t>(item / rows);
@@ -1069,17 +1132,14 @@ __global__ void __launch_bounds__(256, TSV_GREEDY_MINB) verify_greedy_argmax_ker
     }
 }
 
-__global__ void __launch_bounds__(256) verify_greedy_emit_kernel(const RaceParams P) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= P.B) return;
+__device__ __forceinline__ int2 greedy_emit_unit(const RaceParams& P, int32_t i) {
+    if (i >= P.B) return make_int2(-1, 0);
     const int lane = threadIdx.x & 31;
     const int32_t r0 = P.row_offsets[i];
     const int32_t r1 = P.row_offsets[i + 1];
     const int32_t k = r1 - r0 - 1;
     const int32_t qbase = r0 - i;
-    const bool ok = k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p;
+    const bool ok = request_rows_ok(r0, r1, i, P.k_max, dense_rows(P.row_offsets, P.B, P.rows_p), P.B);
     int32_t x = -1, g = -1;
     bool bad = false;
     if (ok && lane <= k) {
@@ -1093,13 +1153,21 @@ __global__ void __launch_bounds__(256) verify_greedy_emit_kernel(const RaceParam
     if (!ok || __ballot_sync(0xFFFFFFFFu, bad)) {
         emit(P, i, 0, -1, -1);
         if (lane == 0) report(P.devstatus, ok ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
-        return;
+        return make_int2(-1, 0);
     }
     const uint32_t mism = __ballot_sync(0xFFFFFFFFu, lane < k && x != g);
     const int32_t m = mism ? __ffs(mism) - 1 : k;
     const int32_t t = __shfl_sync(0xFFFFFFFFu, g, m);
     emit(P, i, qbase, m, t);
     if (lane == 0 && t < 0) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+    return make_int2(m, k);
+}
+
+__global__ void __launch_bounds__(256) verify_greedy_emit_kernel(const RaceParams P) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int2 mk = greedy_emit_unit(P, blockIdx.x * 8 + (threadIdx.x >> 5));
+    if (P.step_counts) add_step_counts(P.step_counts, (threadIdx.x & 31) == 0, mk.x, mk.y);
 }
 
 // ------------------------------------------------------------ fused softmax from logits (NEXT 1)
@@ -1158,8 +1226,8 @@ __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel
     const int lane = threadIdx.x & 31;
     const int32_t warp_id = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int32_t n_warps = gridDim.x * 8;
-    const int32_t rp = P.row_offsets[P.B];  // p rows in use; q rows: rp - B
-    const int32_t rq = (P.q != nullptr) ? rp - P.B : 0;
+    const int32_t rp = dense_rows(P.row_offsets, P.B, P.rows_p);  // p rows in use; q rows: rp - B
+    const int32_t rq = (P.q != nullptr) ? max(0, min(rp - P.B, rows_q_max)) : 0;
     const int64_t n_items = static_cast<int64_t>(rp + rq) * P.n_chunks;
     const float it = P.inv_tau;
     const float l2e = __fmul_rn(1.4426950408889634f, it);  // RN32(log2(e) / tau)
@@ -1228,7 +1296,6 @@ __global__ void __launch_bounds__(256, TSV_STATS_MINB) verify_logit_stats_kernel
             part[slot].s = s;
         }
     }
-    (void)rows_q_max;
 }
 
 // (M, RN32(1/S)) of one row from its chunk partials.
@@ -1247,6 +1314,7 @@ __global__ void __launch_bounds__(256) verify_logit_scan_kernel(const RaceParams
                                                                 float4* lstats) {
     pdl_wait();
     pdl_launch_dependents();
+    zero_step_counts(P.step_counts);
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (i >= P.B) return;
     const int lane = threadIdx.x & 31;
@@ -1254,7 +1322,7 @@ __global__ void __launch_bounds__(256) verify_logit_scan_kernel(const RaceParams
     const int32_t r1 = P.row_offsets[i + 1];
     const int32_t k = r1 - r0 - 1;
     const int32_t qbase = r0 - i;
-    int32_t ok = (k >= 0 && k <= P.k_max && qbase >= 0 && r1 <= P.rows_p) ? 1 : 0;
+    int32_t ok = request_rows_ok(r0, r1, i, P.k_max, dense_rows(P.row_offsets, P.B, P.rows_p), P.B) ? 1 : 0;
     const uint32_t rid = P.rids[i];
     int32_t x = -1;
     bool bad = false, acc = false;
@@ -1395,6 +1463,7 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.num_accepted = a->num_accepted;
     P.out_tokens = a->out_tokens;
     P.devstatus = a->device_status;
+    P.step_counts = reinterpret_cast<long long*>(a->step_counts);
     P.tuples = nullptr;
     P.lstats = nullptr;
     P.inv_tau = 1.0f;
@@ -1513,10 +1582,10 @@ extern "C" tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream) 
                 "tsv_verify_accept: unsharded call needs vocab_offset == 0 and vocab == vocab_global "
                 "(use tsv_verify_shard_partial/combine for vocab shards)");
     if (a->B == 0) return TSV_OK;
-    TSV_TRY(check_device());
-    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_accept: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    TSV_TRY(check_device());
     return run_verify<kLazy>(a, make_params(a), static_cast<cudaStream_t>(stream));
 }
 
@@ -1529,10 +1598,10 @@ extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double*
     TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_verify_accept_update: decay %g outside [0, 1]", decay);
     TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED, "tsv_verify_accept_update: unknown estimator");
     if (a->B == 0) return TSV_OK;
-    TSV_TRY(check_device());
-    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_accept_update: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    TSV_TRY(check_device());
     UpdateArgs ua;
     ua.alpha = alpha;
     ua.num_accepted = a->num_accepted;
@@ -1548,11 +1617,11 @@ extern "C" tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_sha
                                                void* stream) {
     TSV_TRY(validate(a));
     if (a->B == 0) return TSV_OK;
-    TSV_TRY(check_device());
-    TSV_REQUIRE(tuples_out != nullptr, "tsv_verify_shard_partial: tuples_out is NULL");
-    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_shard_partial: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    TSV_REQUIRE(tuples_out != nullptr, "tsv_verify_shard_partial: tuples_out is NULL");
+    TSV_TRY(check_device());
     RaceParams P = make_params(a);
     P.tuples = tuples_out;
     return run_verify<kShard>(a, P, static_cast<cudaStream_t>(stream));
@@ -1590,11 +1659,11 @@ extern "C" tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint
                                             void* stream) {
     TSV_TRY(validate(a));
     if (a->B == 0) return TSV_OK;
-    TSV_TRY(check_device());
-    TSV_REQUIRE(masks && keys_out, "tsv_verify_shard_race: NULL argument");
-    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_shard_race: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    TSV_REQUIRE(masks && keys_out, "tsv_verify_shard_race: NULL argument");
+    TSV_TRY(check_device());
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     RaceParams P = make_params(a);
     const dim3 grid(static_cast<unsigned>((a->B + 7) / 8));
@@ -1653,10 +1722,10 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
     TSV_REQUIRE(a->rows_p >= a->B, "tsv_verify_greedy: rows_p %d < B %d", a->rows_p, a->B);
     TSV_REQUIRE(a->chunk == 0 || (a->chunk >= 128 && a->chunk % 128 == 0 && a->chunk <= kMaxChunk),
                 "tsv_verify_greedy: chunk must be 0 or a multiple of 128 in [128, %d]", kMaxChunk);
-    TSV_TRY(check_device());
-    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_greedy: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    TSV_TRY(check_device());
     tsv_verify_args b = *a;
 #ifndef TSV_GREEDY_ITEM_WARPS  // items per SM: two per resident warp (config 2: 30.4 us; one: 32.1; 1/2: 32.3)
 #define TSV_GREEDY_ITEM_WARPS (2 * 8 * TSV_GREEDY_MINB)
@@ -1674,11 +1743,13 @@ extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) 
 #endif
     if (TSV_GREEDY_CLEAR_KERNEL)  // a PDL kernel (its launch overlaps the previous kernel; a memset node does not)
         TSV_CUDA(launch_pdl(clear_u64_kernel, dim3(static_cast<unsigned>((a->rows_p + 1023) / 1024)), dim3(256), 0, st,
-                            P.rowkey, static_cast<int64_t>(a->rows_p)),
+                            P.rowkey, static_cast<int64_t>(a->rows_p), P.step_counts),
                  "clear_u64_kernel launch");
-    else
+    else {
         TSV_CUDA(cudaMemsetAsync(P.rowkey, 0, sizeof(unsigned long long) * static_cast<size_t>(a->rows_p), st),
                  "cudaMemsetAsync");
+        if (P.step_counts) TSV_CUDA(cudaMemsetAsync(P.step_counts, 0, 2 * sizeof(long long), st), "cudaMemsetAsync");
+    }
     const int64_t n_items = static_cast<int64_t>(a->rows_p) * P.n_chunks;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * TSV_GREEDY_MINB));
     TSV_CUDA(launch_pdl(verify_greedy_argmax_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, P),
@@ -1735,7 +1806,7 @@ extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float t
     RaceParams P = make_params(a);
     RaceParams PS = stats_params(a, P);  // statistics pass + scan (partials per row)
     const size_t need = align256(workspace_bytes(a)) + logits_extra_bytes(a, PS.n_chunks);
-    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= need,
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= need,
                 "tsv_verify_accept_logits: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)need);
     char* ws = static_cast<char*>(a->workspace) + align256(workspace_bytes(a));
@@ -1748,7 +1819,7 @@ extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float t
     const int64_t n_items = 2 * static_cast<int64_t>(a->rows_p) * PS.n_chunks;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_items + 7) / 8, static_cast<int64_t>(sm_count()) * TSV_STATS_MINB));
     TSV_CUDA(launch_pdl(verify_logit_stats_kernel, dim3(static_cast<unsigned>(grid)), dim3(256), 0, st, PS, part,
-                        a->rows_p),
+                        a->rows_p - a->B),
              "verify_logit_stats_kernel launch");
     const dim3 req_grid(static_cast<unsigned>((a->B + 7) / 8));
     TSV_CUDA(launch_pdl(verify_logit_scan_kernel, req_grid, dim3(256), 0, st, PS,
@@ -1900,10 +1971,10 @@ extern "C" tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p
     TSV_REQUIRE(p != nullptr, "tsv_verify_shard_p2p_phase: p2p handle is NULL");
     TSV_REQUIRE(phase >= 0 && phase <= 2, "tsv_verify_shard_p2p_phase: phase %d", phase);
     TSV_REQUIRE(a->B <= p->view.B_max, "tsv_verify_shard_p2p_phase: B %d > B_max %d", a->B, p->view.B_max);
-    TSV_TRY(check_device());
-    TSV_REQUIRE(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
                 "tsv_verify_shard_p2p_phase: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    TSV_TRY(check_device());
     if (a->B == 0) return TSV_OK;  // (all ranks skip the exchange together; the epoch does not advance)
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     RaceParams P = make_params(a);

@@ -74,7 +74,8 @@ class ClosedLoop:
         B, K = self.B, self.K
         cin, cout = self.ctx[t % 2], self.ctx[(t + 1) % 2]
         tsv._check(L_.tsv_propose_lookup(cin.data_ptr(), self.ctx_offsets.data_ptr(), B, self.n_min, self.n_max, K,
-                                         self.proposals.data_ptr(), self.proposal_len.data_ptr(), st))
+                                         self.proposals.data_ptr(), self.proposal_len.data_ptr(),
+                                         self.status.data_ptr(), st))
         tsv._check(L_.tsv_goodput_choose_k(self.alpha.data_ptr(), 0, self.ctx_len.data_ptr(),
                                            self.proposal_len.data_ptr(), B, K, tsv.POLICY_PLD, self.target,
                                            tsv.LatencyModel(0.0, 0.0, 0.0), self.pld_cost_ms, -1,

@@ -14,18 +14,25 @@ sm_100a kernels.  Inputs rotate over ``sets`` to keep the timed region out of L2
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Optional
+from typing import Any, List, Optional
 
-import numpy as np
 import torch
 
-import synth
 from . import tsv
+
+# Defaults of the step's configuration (not arithmetic): the SPEC.md desk latency profiles
+# (ctx_ms_per_tok, batched_ms_per_tok, fixed_ms) -- SPEC.md:50, 59-60 (target), 69 (draft) --
+# and the Philox seed of the synthetic workloads.
+DESK_TARGET = (0.001, 0.05, 2.0)
+DESK_DRAFT = (0.0001, 0.005, 0.2)
+DEFAULT_SEED = 240614066
 
 
 @dataclass
 class StepInputs:
-    verify: List[synth.VerifyBatch]        # one per rotation set (device)
+    """The step's device inputs.  ``verify[s]`` is any object carrying the tsv_verify_args arrays
+    of rotation set s as attributes: p, q (or None), row_offsets, draft_tokens, request_ids."""
+    verify: List[Any]                      # one per rotation set (device)
     ctx: List[torch.Tensor]                # int32 contexts per set (device)
     ctx_offsets: List[torch.Tensor]        # int32 [B+1] per set (device)
     ctx_len: List[torch.Tensor]            # int32 [B] per set (device)
@@ -33,32 +40,19 @@ class StepInputs:
     n_min: int = 1
     n_max: int = 4
     k_fixed: int = 5
-    target: tuple = synth.SPEC_DESK_TARGET
-    draft: tuple = synth.SPEC_DESK_DRAFT
+    target: tuple = DESK_TARGET
+    draft: tuple = DESK_DRAFT
     pld_cost_ms: float = 0.05
     kv_free_slots: int = -1
-    seed: int = synth.DEFAULT_SEED
+    seed: int = DEFAULT_SEED
 
     @property
     def B(self) -> int:
-        return self.verify[0].B
+        return int(self.verify[0].row_offsets.numel()) - 1
 
     @property
     def sets(self) -> int:
         return len(self.verify)
-
-    @staticmethod
-    def synthetic(B: int, V: int, L: int, k_max: int = 8, seed: int = synth.DEFAULT_SEED,
-                  device="cuda", sets: int = 1, lam: float = 0.7) -> "StepInputs":
-        vbs, ctxs, offs, lens = [], [], [], []
-        for s in range(sets):
-            vbs.append(synth.make_verify_batch(B=B, V=V, k_max=k_max, lam=lam, seed=seed + 1000 * s,
-                                               device=device))
-            c, o = synth.make_contexts(B=B, L=L, V=V, seed=seed + 1000 * s)
-            ctxs.append(torch.tensor(c, device=device))
-            offs.append(torch.tensor(o, device=device))
-            lens.append(torch.tensor(np.diff(o).astype(np.int32), device=device))
-        return StepInputs(vbs, ctxs, offs, lens, k_max, seed=seed)
 
     def input_bytes(self, s: int) -> int:
         """Bytes of one set's inputs (what an end-to-end call copies host -> device)."""
@@ -124,7 +118,7 @@ class SpecStep:
                 self.proposals.data_ptr(), self.proposal_len.data_ptr(), self.alpha.data_ptr(), 0,
                 inp.ctx_len[s].data_ptr(), tsv.LatencyModel(*inp.target), float(inp.pld_cost_ms),
                 int(inp.kv_free_slots), self.k_star.data_ptr(), self.goodput.data_ptr(), self.k_req.data_ptr(),
-                self.counter.data_ptr(), st))
+                self.counter.data_ptr(), self.status.data_ptr(), st))
             a = self.args[s]
             a.step = step & 0xFFFFFFFF
             tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
@@ -132,7 +126,7 @@ class SpecStep:
             return
         tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
                                         inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
-                                        self.proposal_len.data_ptr(), st))
+                                        self.proposal_len.data_ptr(), self.status.data_ptr(), st))
         tsv._check(L.tsv_goodput_choose_k(self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(),
                                           self.proposal_len.data_ptr(), inp.B, inp.k_fixed,
                                           tsv.POLICY_PLD, tsv.LatencyModel(*inp.target),
@@ -153,7 +147,7 @@ class SpecStep:
         if name == "lookup":
             tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
                                             inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
-                                            self.proposal_len.data_ptr(), st))
+                                            self.proposal_len.data_ptr(), self.status.data_ptr(), st))
         elif name == "choose_k":
             tsv._check(L.tsv_goodput_choose_k(self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(),
                                               self.proposal_len.data_ptr(), inp.B, inp.k_fixed,

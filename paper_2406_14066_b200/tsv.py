@@ -23,6 +23,8 @@ STATUS_NAMES = {1: "TSV_ERR_INVALID_ARG", 2: "TSV_ERR_CUDA", 3: "TSV_ERR_NCCL",
 DEVSTATUS_BAD_TOKEN = 1
 DEVSTATUS_BAD_K = 2
 DEVSTATUS_NO_WEIGHT = 4
+DEVSTATUS_P2P_TIMEOUT = 8
+DEVSTATUS_BAD_CONTEXT = 16
 VERIFY_NO_PRUNE = 1
 VERIFY_SHARD_DENSE = 2
 VERIFY_RACE_ONLY = 4  # measurement: the race kernel alone over a previous call's workspace
@@ -73,6 +75,7 @@ class VerifyArgs(ctypes.Structure):
         ("step", ctypes.c_uint32), ("B", ctypes.c_int32), ("k_max", ctypes.c_int32),
         ("rows_p", ctypes.c_int32), ("vocab", ctypes.c_int32), ("vocab_offset", ctypes.c_int32),
         ("vocab_global", ctypes.c_int32), ("chunk", ctypes.c_int32), ("flags", ctypes.c_int32),
+        ("step_counts", ctypes.c_void_p),
     ]
 
 
@@ -95,7 +98,7 @@ def _load() -> ctypes.CDLL:
     sig = {
         "tsv_last_error": ([], ctypes.c_char_p),
         "tsv_abi_version": ([], ctypes.c_int),
-        "tsv_propose_lookup": ([P, P, i32, i32, i32, i32, P, P, P], ctypes.c_int),
+        "tsv_propose_lookup": ([P, P, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
         "tsv_verify_workspace_size": ([ctypes.POINTER(VerifyArgs), ctypes.POINTER(sz)], ctypes.c_int),
         "tsv_workspace_clear": ([P, sz, P], ctypes.c_int),
         "tsv_verify_accept": ([ctypes.POINTER(VerifyArgs), P], ctypes.c_int),
@@ -112,7 +115,7 @@ def _load() -> ctypes.CDLL:
         "tsv_verify_accept_sharded": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
         "tsv_allreduce_i64": ([P, sz, P, P], ctypes.c_int),
         "tsv_propose_lookup_choose_k": ([P, P, i32, i32, i32, i32, P, P, P, i32, P, LatencyModel, f64, i64,
-                                         P, P, P, P, P], ctypes.c_int),
+                                         P, P, P, P, P, P], ctypes.c_int),
         "tsv_verify_accept_update": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P], ctypes.c_int),
         "tsv_debug_race_E": ([ctypes.c_uint32, ctypes.c_uint32, P, P], ctypes.c_int),
         "tsv_debug_philox": ([P, P, ctypes.c_uint32, P, i32, P], ctypes.c_int),
@@ -208,7 +211,7 @@ def tsv_abi_version() -> int:
 # ----------------------------------------------------------------------------- lookup
 def tsv_propose_lookup(ctx: torch.Tensor, ctx_offsets: torch.Tensor, n_min: int, n_max: int,
                        k_fixed: int, proposals: Optional[torch.Tensor] = None,
-                       proposal_len: Optional[torch.Tensor] = None, stream=None):
+                       proposal_len: Optional[torch.Tensor] = None, device_status=None, stream=None):
     """Prompt-lookup proposal.  Returns (proposals[B, k], proposal_len[B])."""
     B = ctx_offsets.numel() - 1
     _want(ctx, torch.int32, None, "ctx")
@@ -220,14 +223,15 @@ def tsv_propose_lookup(ctx: torch.Tensor, ctx_offsets: torch.Tensor, n_min: int,
         proposal_len = torch.empty(B, dtype=torch.int32, device=dev)
     ctx_p = _ptr(ctx) if ctx.numel() else _ptr(ctx_offsets)  # any valid pointer when empty
     _check(_lib.tsv_propose_lookup(ctx_p, _ptr(ctx_offsets), B, n_min, n_max, k_fixed,
-                                   _ptr(proposals), _ptr(proposal_len), _stream(stream)))
+                                   _ptr(proposals), _ptr(proposal_len), _ptr(device_status), _stream(stream)))
     return proposals, proposal_len
 
 
 # ----------------------------------------------------------------------------- verify
 def make_verify_args(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max,
                      num_accepted, out_tokens, device_status=None, workspace=None,
-                     vocab=None, vocab_offset=0, vocab_global=None, chunk=0, flags=0) -> VerifyArgs:
+                     vocab=None, vocab_offset=0, vocab_global=None, chunk=0, flags=0,
+                     step_counts=None) -> VerifyArgs:
     B = row_offsets.numel() - 1
     _want(p, torch.float32, None, "p")
     if q is not None:
@@ -263,6 +267,9 @@ def make_verify_args(p, q, row_offsets, draft_tokens, request_ids, seed, step, k
     a.vocab_global = int(vocab_global) if vocab_global is not None else V
     a.chunk = int(chunk)
     a.flags = int(flags)
+    if step_counts is not None:
+        _want(step_counts, torch.int64, 2, "step_counts")
+    a.step_counts = _ptr(step_counts)
     return a
 
 
@@ -284,7 +291,7 @@ def alloc_workspace(nbytes: int, device) -> torch.Tensor:
 
 def tsv_verify_accept(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max,
                       num_accepted=None, out_tokens=None, device_status=None, workspace=None,
-                      chunk=0, flags=0, vocab=None, stream=None):
+                      chunk=0, flags=0, vocab=None, step_counts=None, stream=None):
     """Rejection-sampling verify/accept.  Returns (num_accepted, out_tokens)."""
     B = row_offsets.numel() - 1
     dev = _dev(row_offsets)
@@ -294,7 +301,7 @@ def tsv_verify_accept(p, q, row_offsets, draft_tokens, request_ids, seed, step, 
         out_tokens = torch.empty((B, k_max + 1), dtype=torch.int32, device=dev)
     a = make_verify_args(p, q, row_offsets, draft_tokens, request_ids, seed, step, k_max,
                          num_accepted, out_tokens, device_status, workspace, vocab=vocab,
-                         chunk=chunk, flags=flags)
+                         chunk=chunk, flags=flags, step_counts=step_counts)
     if workspace is None and B > 0:
         workspace = alloc_workspace(tsv_verify_workspace_size(a), dev)
         a.workspace = workspace.data_ptr()
@@ -304,7 +311,7 @@ def tsv_verify_accept(p, q, row_offsets, draft_tokens, request_ids, seed, step, 
 
 
 def tsv_verify_greedy(p, row_offsets, draft_tokens, k_max, num_accepted=None, out_tokens=None,
-                      device_status=None, workspace=None, vocab=None, chunk=0, stream=None):
+                      device_status=None, workspace=None, vocab=None, chunk=0, step_counts=None, stream=None):
     """Greedy (temperature-0) verify (reading R24).  Returns (num_accepted, out_tokens)."""
     B = row_offsets.numel() - 1
     dev = _dev(p)
@@ -314,7 +321,8 @@ def tsv_verify_greedy(p, row_offsets, draft_tokens, k_max, num_accepted=None, ou
         out_tokens = torch.empty((B, k_max + 1), dtype=torch.int32, device=dev)
     rids = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)  # unused by the greedy rule
     a = make_verify_args(p, None, row_offsets, draft_tokens, rids[:B] if B else rids, 0, 0, k_max,
-                         num_accepted, out_tokens, device_status, workspace, vocab=vocab, chunk=chunk)
+                         num_accepted, out_tokens, device_status, workspace, vocab=vocab, chunk=chunk,
+                         step_counts=step_counts)
     if workspace is None and B > 0:
         workspace = alloc_workspace(tsv_verify_workspace_size(a), dev)
         a.workspace = workspace.data_ptr()
@@ -331,7 +339,7 @@ def tsv_verify_logits_workspace_size(args: VerifyArgs) -> int:
 
 def tsv_verify_accept_logits(zp, zq, row_offsets, draft_tokens, request_ids, seed, step, k_max,
                              temperature=1.0, num_accepted=None, out_tokens=None, device_status=None,
-                             workspace=None, vocab=None, chunk=0, flags=0, stream=None):
+                             workspace=None, vocab=None, chunk=0, flags=0, step_counts=None, stream=None):
     """Fused softmax-from-logits verify (reading R23).  Returns (num_accepted, out_tokens)."""
     B = row_offsets.numel() - 1
     dev = _dev(zp)
@@ -340,7 +348,8 @@ def tsv_verify_accept_logits(zp, zq, row_offsets, draft_tokens, request_ids, see
     if out_tokens is None:
         out_tokens = torch.empty((B, k_max + 1), dtype=torch.int32, device=dev)
     a = make_verify_args(zp, zq, row_offsets, draft_tokens, request_ids, seed, step, k_max,
-                         num_accepted, out_tokens, device_status, workspace, vocab=vocab, chunk=chunk, flags=flags)
+                         num_accepted, out_tokens, device_status, workspace, vocab=vocab, chunk=chunk, flags=flags,
+                         step_counts=step_counts)
     if workspace is None and B > 0:
         workspace = alloc_workspace(tsv_verify_logits_workspace_size(a), dev)
         a.workspace = workspace.data_ptr()
@@ -394,7 +403,7 @@ def lookup_choose_scratch(device) -> torch.Tensor:
 def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, ctx_len, target,
                                 pld_cost_ms, counter, kv_free_slots=-1, alpha_per_request=None,
                                 proposals=None, proposal_len=None, k_out=None, goodput_out=None,
-                                k_per_request=None, stream=None):
+                                k_per_request=None, device_status=None, stream=None):
     """Fused prompt lookup + PLD goodput selection.  ``counter``: device scratch of
     LOOKUP_CHOOSE_SCRATCH bytes (e.g. lookup_choose_scratch()), zeroed once.
     Returns (proposals, proposal_len, k_out, goodput_out)."""
@@ -417,7 +426,7 @@ def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, 
                                             1 if per else 0, _ptr(ctx_len), LatencyModel(*target),
                                             float(pld_cost_ms), int(kv_free_slots), _ptr(k_out),
                                             _ptr(goodput_out), _ptr(k_per_request), _ptr(counter),
-                                            _stream(stream)))
+                                            _ptr(device_status), _stream(stream)))
     return proposals, proposal_len, k_out, goodput_out
 
 

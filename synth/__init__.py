@@ -166,6 +166,21 @@ def make_goodput_instance(B: int, k_max: int = 8, seed: int = DEFAULT_SEED, ctx_
     return ctx_len, caps
 
 
+def make_step_inputs(B: int, V: int, L: int, k_max: int = 8, seed: int = DEFAULT_SEED, device="cuda",
+                     sets: int = 1, lam: float = 0.7):
+    """A SpecStep's inputs (paper_2406_14066_b200.step.StepInputs) from this module's generators:
+    `sets` rotation sets of a config-2-shaped verify batch and config-3-shaped PLD contexts."""
+    from paper_2406_14066_b200.step import StepInputs  # lazy: only the container type
+    vbs, ctxs, offs, lens = [], [], [], []
+    for s in range(sets):
+        vbs.append(make_verify_batch(B=B, V=V, k_max=k_max, lam=lam, seed=seed + 1000 * s, device=device))
+        c, o = make_contexts(B=B, L=L, V=V, seed=seed + 1000 * s)
+        ctxs.append(torch.tensor(c, device=device))
+        offs.append(torch.tensor(o, device=device))
+        lens.append(torch.tensor(np.diff(o).astype(np.int32), device=device))
+    return StepInputs(vbs, ctxs, offs, lens, k_max, seed=seed)
+
+
 # Latency profiles (DESIGN.md §4): (ctx_ms_per_tok, batched_ms_per_tok, fixed_ms)
 SPEC_DESK_TARGET = (0.001, 0.05, 2.0)        # SPEC.md:50, 59-60
 SPEC_DESK_DRAFT = (0.0001, 0.005, 0.2)       # SPEC.md:69

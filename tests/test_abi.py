@@ -39,7 +39,7 @@ def test_every_declared_symbol_exported(tsv):
 
 
 def test_abi_version(tsv):
-    assert tsv.tsv_abi_version() == 1
+    assert tsv.tsv_abi_version() == 2
 
 
 PROBE = r"""
@@ -55,7 +55,7 @@ int main(void) {
   F(tsv_verify_args, workspace_bytes) F(tsv_verify_args, ld) F(tsv_verify_args, seed)
   F(tsv_verify_args, step) F(tsv_verify_args, B) F(tsv_verify_args, k_max) F(tsv_verify_args, rows_p)
   F(tsv_verify_args, vocab) F(tsv_verify_args, vocab_offset) F(tsv_verify_args, vocab_global)
-  F(tsv_verify_args, chunk) F(tsv_verify_args, flags)
+  F(tsv_verify_args, chunk) F(tsv_verify_args, flags) F(tsv_verify_args, step_counts)
   printf("tsv_shard_tuple sizeof %zu\n", sizeof(tsv_shard_tuple));
   printf("tsv_latency_model sizeof %zu\n", sizeof(tsv_latency_model));
   return 0;
@@ -85,11 +85,11 @@ def test_ctypes_layout_matches_c(tsv):
 def test_host_validation_without_gpu(tsv):
     L = tsv.lib()
     # bad n-gram range: rejected before any device work
-    assert L.tsv_propose_lookup(None, None, 4, 3, 2, 5, None, None, None) == 1
+    assert L.tsv_propose_lookup(None, None, 4, 3, 2, 5, None, None, None, None) == 1
     assert b"n_min" in L.tsv_last_error()
-    assert L.tsv_propose_lookup(None, None, -1, 1, 2, 5, None, None, None) == 1
+    assert L.tsv_propose_lookup(None, None, -1, 1, 2, 5, None, None, None, None) == 1
     # B = 0 is a no-op
-    assert L.tsv_propose_lookup(None, None, 0, 1, 2, 5, None, None, None) == 0
+    assert L.tsv_propose_lookup(None, None, 0, 1, 2, 5, None, None, None, None) == 0
     a = tsv.VerifyArgs()
     a.B, a.k_max = 4, 16
     assert L.tsv_verify_accept(ctypes.byref(a), None) == 1
@@ -132,3 +132,37 @@ def test_empty_batch_is_a_noop_without_device_work(tsv):
     assert L.tsv_softmax_rows(None, 16, 16, 0, 1.0, None, None) == 0
     m = tsv.LatencyModel(0.001, 0.05, 2.0)
     assert L.tsv_goodput_choose_k_batched(None, None, None, None, 0, 8, 0, m, m, 0.0, -1, None, None, None, None) == 0
+
+
+def test_workspace_errors_return_tsv_err_workspace(tsv):
+    # a NULL or too small workspace is TSV_ERR_WORKSPACE (5), checked on the host before any launch
+    L = tsv.lib()
+    buf = ctypes.create_string_buffer(64 * 1024 + 16)
+    base = (ctypes.addressof(buf) + 15) // 16 * 16  # host addresses: validation never dereferences them
+    a = tsv.VerifyArgs()
+    a.B, a.k_max, a.rows_p, a.vocab, a.vocab_global, a.ld = 4, 4, 20, 64, 64, 64
+    for f in ("p", "q", "row_offsets", "draft_tokens", "request_ids", "num_accepted", "out_tokens"):
+        setattr(a, f, base)
+    need = ctypes.c_size_t(0)
+    assert L.tsv_verify_workspace_size(ctypes.byref(a), ctypes.byref(need)) == 0 and need.value > 0
+    a.workspace, a.workspace_bytes = None, 0
+    assert L.tsv_verify_accept(ctypes.byref(a), None) == 5
+    assert b"workspace" in L.tsv_last_error()
+    a.workspace, a.workspace_bytes = base, need.value - 1
+    assert L.tsv_verify_accept(ctypes.byref(a), None) == 5
+    assert L.tsv_verify_accept_update(ctypes.byref(a), base, 0, 0.9, 0, None) == 5
+    assert L.tsv_verify_greedy(ctypes.byref(a), None) == 5
+    assert L.tsv_verify_shard_partial(ctypes.byref(a), base, None) == 5
+    assert L.tsv_verify_shard_race(ctypes.byref(a), base, base, None) == 5
+    m = tsv.LatencyModel(0.001, 0.05, 2.0)
+    assert L.tsv_propose_lookup_choose_k(base, base, 4, 1, 4, 5, base, base, base, 0, base, m, 0.05, -1, base,
+                                         None, None, None, None, None) == 5
+    assert tsv.STATUS_NAMES[5] == "TSV_ERR_WORKSPACE"
+
+
+def test_devstatus_bits_match_header(tsv):
+    txt = open(HDR).read()
+    bits = dict((n, int(v)) for n, v in re.findall(r"#define TSV_DEVSTATUS_(\w+) (\d+)u", txt))
+    assert bits == {"BAD_TOKEN": tsv.DEVSTATUS_BAD_TOKEN, "BAD_K": tsv.DEVSTATUS_BAD_K,
+                    "NO_WEIGHT": tsv.DEVSTATUS_NO_WEIGHT, "P2P_TIMEOUT": tsv.DEVSTATUS_P2P_TIMEOUT,
+                    "BAD_CONTEXT": tsv.DEVSTATUS_BAD_CONTEXT}

@@ -787,7 +787,7 @@ def test_fused_verify_update_equals_separate(tsv, est):
 @pytest.mark.parametrize("fused", [False, True])
 def test_step_graph_capture_matches_eager(tsv, fused):
     from paper_2406_14066_b200.step import SpecStep, StepInputs
-    inp = StepInputs.synthetic(B=64, V=32000, L=1024, k_max=8, seed=20, device=DEV)
+    inp = synth.make_step_inputs(B=64, V=32000, L=1024, k_max=8, seed=20, device=DEV)
     st = SpecStep(inp, fused=fused)
     st.run(step=0)
     torch.cuda.synchronize()
