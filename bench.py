@@ -15,8 +15,14 @@ Roofline: the dominant kernel (verify_race_kernel) timed alone -- 64 race-only l
 (TSV_VERIFY_RACE_ONLY) over per-step workspaces -- against its algorithmic bytes (the rows the
 steps actually select) and MEASURED_PEAKS.json's HBM copy bandwidth; the whole verify call is
 reported beside it.  e2e: the same ABI calls with the inputs in pinned host memory.
-Multi-GPU: request-sharded weak scaling -- every rank runs its own B = 256 batch with
-global request ids; no data-path collective; time = max over ranks.
+Multi-GPU: one server over the N ranks, request-sharded -- every rank runs B = 256
+requests (global request ids) and alpha / k* are GLOBAL: the exact int64 ArgMaxGoodput sums and the
+(sum m, sum t) acceptance pair are summed over the ranks through NVLink peer memory inside the
+goodput kernel and the verify's update CTA (no NCCL launch; --comm nccl for NCCL all-reduces);
+time = max over ranks ("scaling": "weak").  Sub-objects ("workloads"): the strong-scaling line
+(one B = 256 batch split by request), config 4 vocab-sharded over the N ranks, greedy, logits,
+the config-5 goodput sweep and the closed decode loop, each with its own roofline, clocks and
+device status (--no-extras omits them; --workload X prints X alone).
 """
 from __future__ import annotations
 
@@ -53,7 +59,13 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
-    ap.add_argument("--workload", default="step", choices=["step", "config4", "greedy", "logits", "config5"],
+    ap.add_argument("--comm", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 exchange of the request-sharded global sums: NVLink peer memory inside the goodput "
+                         "and update kernels (p2p) or NCCL all-reduces (nccl)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="omit the other workloads' sub-objects (config4, greedy, logits, config5, loop, strong)")
+    ap.add_argument("--workload", default="step",
+                    choices=["step", "config4", "greedy", "logits", "config5", "loop", "strong"],
                     help="step: the default decode step; config4: Llama-3 vocab-sharded verify (V=128256) "
                          "through tsv_verify_accept_sharded over the N ranks (strong scaling); greedy: the "
                          "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling); logits: the fused "
@@ -178,39 +190,64 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------- our arm
-def run_ours(args, rank, world, local_rank):
+def _sets_for(args, bytes_per_set, l2):
+    """Rotating input sets: at least --sets, and enough that R x footprint >= 3 x L2."""
+    need = int(np.ceil(3.0 * l2 / max(1, bytes_per_set)))
+    return int(min(16, max(args.sets, need)))
+
+
+def build_step_inputs(mode, rank, world, dev, args, B_total):
+    """The step's rotating input sets on this rank.
+    weak:   the rank's own B_total requests (global ids rank * B_total + i): one server whose batch
+            grows with N (global alpha / k* over all ranks);
+    strong: requests [lo, hi) of ONE B_total batch (the same seed on every rank), split by
+            dist.partition_requests (balanced sum(2 k_i + 1))."""
     import torch
-    import torch.distributed as dist
 
     import synth
     from paper_2406_14066_b200 import dist as pdist
-    from paper_2406_14066_b200 import tsv
-    from paper_2406_14066_b200.step import SpecStep, StepInputs
-
-    dev = torch.device("cuda", _dev_index(local_rank))
-    torch.cuda.set_device(dev)
-    R = max(1, args.sets)
+    from paper_2406_14066_b200.step import StepInputs
     seed = synth.DEFAULT_SEED
-    # every rank owns a distinct slice of global request ids (weak scaling, R6: Philox keyed by global ids)
-    vbs, ctxs, offs, lens = [], [], [], []
-    for s in range(R):
-        vb = synth.make_verify_batch(B=B, V=V, k_max=K_MAX, lam=0.7, seed=seed + 7919 * s + rank,
-                                     device=dev, request_id_base=rank * B)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    vbs, ctxs, offs, lens, ks = [], [], [], [], []
+    R, s = max(1, args.sets), 0
+    while s < R:
+        if mode == "weak":
+            vb = synth.make_verify_batch(B=B_total, V=V, k_max=K_MAX, lam=0.7, seed=seed + 7919 * s + rank,
+                                         device=dev, request_id_base=rank * B_total)
+            c, o = synth.make_contexts(B=B_total, L=L_CTX, V=V, seed=seed + 7919 * s + rank)
+            k = vb.k
+        else:
+            whole = synth.make_verify_batch(B=B_total, V=V, k_max=K_MAX, lam=0.7, seed=seed + 7919 * s, device=dev)
+            c, o = synth.make_contexts(B=B_total, L=L_CTX, V=V, seed=seed + 7919 * s)
+            lo, hi = pdist.partition_requests(whole.k.cpu().numpy(), world)[rank]
+            p, q, ro, d, rid = pdist.request_slice(whole.p, whole.q, whole.row_offsets, whole.draft_tokens,
+                                                   whole.request_ids, lo, hi)
+            vb = synth.VerifyBatch(p.clone(), q.clone(), ro.clone(), d.clone(), rid.clone(), whole.k[lo:hi].clone(),
+                                   V, K_MAX)
+            c, o = c[o[lo]:o[hi]], (o[lo:hi + 1] - o[lo]).astype(np.int32)
+            k = vb.k
+            del whole
         vbs.append(vb)
-        c, o = synth.make_contexts(B=B, L=L_CTX, V=V, seed=seed + 7919 * s + rank)
         ctxs.append(torch.tensor(c, device=dev))
         offs.append(torch.tensor(o, device=dev))
         lens.append(torch.tensor(np.diff(o).astype(np.int32), device=dev))
+        ks.append(k.cpu().numpy())
+        if s == 0:  # enough sets that R x footprint >= 3 x L2 (strong scaling shrinks the per-rank set)
+            R = _sets_for(args, (vb.p.numel() + vb.q.numel()) * 4 + c.size * 4, l2)
+        s += 1
+    torch.cuda.empty_cache()
     inp = StepInputs(vbs, ctxs, offs, lens, K_MAX, seed=seed)
-    st = SpecStep(inp, device=dev, chunk=args.chunk, fused=args.fused)
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    footprint = sum(inp.input_bytes(s) for s in range(R))
+    return inp, ks, l2
 
-    def barrier():
-        if world > 1:
-            _barrier(dist, local_rank)
 
-    # ---- graphs: warm-up and timed steps with distinct Philox step counters
+def time_step_graphs(args, st, world, local_rank, dev):
+    """Warm-up, then exactly K steps replayed from CUDA graphs (distinct Philox step counters),
+    timed with CUDA events on the launching stream between barriers; max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_14066_b200 import dist as pdist
     W, K = max(3, args.warmup), args.steps
     gl = max(1, min(args.graph_steps, K))
     st.capture(list(range(0, gl)))  # main graph: steps 0..gl-1 (replayed)
@@ -225,9 +262,13 @@ def run_ours(args, rank, world, local_rank):
         main_graph.replay()
     torch.cuda.synchronize()
 
+    def barrier():
+        if world > 1:
+            _barrier(dist, local_rank)
+
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(_dev_index(local_rank))
     barrier()
     torch.cuda.synchronize()
     with sampler:
@@ -239,11 +280,11 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    t_ms = e0.elapsed_time(e1)
-    t_max = pdist.max_over_ranks(t_ms, dev)
+    t_max = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
     # spread: a second pass with an event around every graph replay (kept out of the timed region)
     n_rep = max(1, min(K // gl, 64))
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(n_rep + 1)]
+    barrier()
     evs[0].record(stream)
     for r in range(n_rep):
         main_graph.replay()
@@ -252,26 +293,84 @@ def run_ours(args, rank, world, local_rank):
     per_step = sorted(evs[r].elapsed_time(evs[r + 1]) / gl for r in range(n_rep))
     spread = {f"p{q}": per_step[min(n_rep - 1, int(q / 100 * n_rep))] for q in (10, 50, 90)}
     spread["replays"] = n_rep
+    spread["steps_per_replay"] = gl
+    step_ids = [t for _ in range(K // gl) for t in range(gl)] + [gl + t for t in range(rem)]
+    return {"t_max": t_max, "W": W, "K": K, "gl": gl, "spread": spread, "step_ids": step_ids,
+            "clocks": sampler.summary(), "stream": stream}
+
+
+def step_tokens(st, inp, ks, step_ids, dev, workspace_from=None):
+    """Generated tokens and verify algorithmic bytes of exactly the timed steps on this rank (the
+    verify outputs do not depend on alpha / k*: a plain verify call per distinct step reproduces them)."""
+    import torch
+
+    from paper_2406_14066_b200 import tsv
+    R = inp.sets
+    per_step_tokens, per_step_vbytes = {}, {}
+    Bl = inp.B
+    na = torch.empty(Bl, dtype=torch.int32, device=dev)
+    outt = torch.empty((Bl, K_MAX + 1), dtype=torch.int32, device=dev)
+    for t in sorted(set(step_ids)):
+        vb = inp.verify[t % R]
+        tsv.tsv_verify_accept(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, inp.seed, t,
+                              K_MAX, num_accepted=na, out_tokens=outt, workspace=st.workspace)
+        m = na.cpu().numpy()
+        per_step_tokens[t] = int((m + 1).sum())
+        per_step_vbytes[t] = verify_alg_bytes(m, ks[t % R], True, V, K_MAX)
+    return per_step_tokens, per_step_vbytes
+
+
+def global_state_consistent(st, world, dev):
+    """Every rank must hold the same alpha bits and k* after the timed steps (one server)."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return True
+    mine = torch.tensor([int(st.alpha.view(torch.int64).item()), int(st.k_star.item())], dtype=torch.int64)
+    allv = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allv, mine.to(dev) if dist.get_backend() == "nccl" else mine)
+    return all(bool(torch.equal(a.cpu(), allv[0].cpu())) for a in allv)
+
+
+def make_comm(args, rank, world, B_max):
+    """The request-sharded exchange: NVLink peer memory (default) or NCCL (--comm nccl)."""
+    if world <= 1:
+        return None
+    from paper_2406_14066_b200 import tsv
+    if args.comm == "nccl" and not SHARED_GPU:
+        return tsv.Comm(rank, world)
+    return tsv.P2PComm(rank, world, B_max=B_max)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2406_14066_b200 import dist as pdist
+    from paper_2406_14066_b200 import tsv
+    from paper_2406_14066_b200.step import SpecStep, StepInputs
+
+    import synth
+    dev = torch.device("cuda", _dev_index(local_rank))
+    torch.cuda.set_device(dev)
+    seed = synth.DEFAULT_SEED
+    # weak scaling, one server: every rank owns B = 256 requests (global ids), alpha and k* are global
+    inp, ks, l2 = build_step_inputs("weak", rank, world, dev, args, B)
+    R = inp.sets
+    vbs = inp.verify
+    comm = make_comm(args, rank, world, B)
+    st = SpecStep(inp, device=dev, chunk=args.chunk, fused=args.fused and comm is None, comm=comm)
+    footprint = sum(inp.input_bytes(s) for s in range(R))
+    tm = time_step_graphs(args, st, world, local_rank, dev)
+    t_max, W, K, gl, stream = tm["t_max"], tm["W"], tm["K"], tm["gl"], tm["stream"]
+    consistent = global_state_consistent(st, world, dev)
 
     # ---- generated tokens and algorithmic bytes of exactly the timed steps (deterministic)
-    step_ids = [t for _ in range(K // gl) for t in range(gl)] + [gl + t for t in range(rem)]
-    uniq = sorted(set(step_ids))
-    per_step_tokens, per_step_vbytes = {}, {}
-    na = torch.empty(B, dtype=torch.int32, device=dev)
-    outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
-    for t in uniq:
-        s = t % R
-        vb = vbs[s]
-        tsv.tsv_verify_accept(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t,
-                              K_MAX, num_accepted=na, out_tokens=outt, workspace=st.workspace,
-                              chunk=args.chunk)
-        m = na.cpu().numpy()
-        k = vb.k.cpu().numpy()
-        per_step_tokens[t] = int((m + 1).sum())
-        per_step_vbytes[t] = verify_alg_bytes(m, k, True, V, K_MAX)
-    tokens_rank = sum(per_step_tokens[t] for t in step_ids)
+    per_step_tokens, per_step_vbytes = step_tokens(st, inp, ks, tm["step_ids"], dev)
+    tokens_rank = sum(per_step_tokens[t] for t in tm["step_ids"])
     tokens_total = pdist.sum_over_ranks(tokens_rank, dev)
     value = tokens_total / (t_max / 1e3)
+    na = torch.empty(B, dtype=torch.int32, device=dev)
+    outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
 
     # ---- the dominant kernel alone, timed live with CUDA events over K launches
     vgraph = torch.cuda.CUDAGraph()
@@ -347,6 +446,8 @@ def run_ours(args, rank, world, local_rank):
     if args.breakdown:
         breakdown = {}
         for comp in ("lookup", "choose_k", "verify", "update", "verify_update"):
+            if comm is not None and comp in ("update", "verify"):
+                continue
             cg = torch.cuda.CUDAGraph()
             with torch.cuda.stream(side):
                 st.run_component(comp, 0, stream=side)
@@ -371,6 +472,8 @@ def run_ours(args, rank, world, local_rank):
     #    kernels read exactly the bytes the lazy path needs over PCIe (UVA), counted per step;
     #  full copy ("e2e_full_copy"): cudaMemcpy of every input tensor (all p and q rows) first.
     e2e = e2e_copy = None
+    st_h = None
+    ctxs, offs, lens = inp.ctx, inp.ctx_offsets, inp.ctx_len
     if args.e2e_steps > 0:
         vb = vbs[0]
         names = ["p", "q", "row_offsets", "draft_tokens", "request_ids"]
@@ -383,14 +486,16 @@ def run_ours(args, rank, world, local_rank):
         ne = args.e2e_steps
         hv = synth.VerifyBatch(host[0], host[1], host[2], host[3], host[4], vb.k, V, K_MAX)
         st_h = SpecStep(StepInputs([hv], [hctx[0]], [hctx[1]], [hctx[2]], K_MAX, seed=seed), device=dev,
-                        chunk=args.chunk)
-        k_np = vb.k.cpu().numpy()
+                        chunk=args.chunk, comm=comm)
+        k_np = ks[0]
         ctx_bytes = hctx[0].numel() * 4 + hctx[1].numel() * 4 + hctx[2].numel() * 4
 
         def run_e2e(step_fn, outs_from):
             toks, h2d_zc = 0, 0
             torch.cuda.synchronize()
-            barrier()
+            if world > 1:
+                import torch.distributed as dist
+                _barrier(dist, local_rank)
             w0 = time.perf_counter()
             x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             x0.record(stream)
@@ -427,35 +532,109 @@ def run_ours(args, rank, world, local_rank):
                     "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in host + hctx)),
                     "d2h_bytes_per_step": int(d2h), "steps": ne, "wall_s": round(wall_c, 4),
                     "mode": "cudaMemcpy of every input tensor (all p and q rows) each step"}
-
+    st_status = int(pdist.max_over_ranks(int(st.status.item()), dev))
+    del st, st_h
+    close_comm(comm, world, local_rank)
     if rank != 0:
         return None
-    st_status = int(st.status.item())
+    par = "request-sharded x1" if world == 1 else (
+        f"request-sharded x{world}, one server: global alpha / k* through "
+        + ("NVLink peer memory inside the goodput and update kernels (p2p)" if comm is not None and
+           not isinstance(comm, tsv.Comm) else "NCCL all-reduce (nccl)"))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": t_max / K, "ms_per_step_spread": spread, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t_max / K, "ms_per_step_spread": tm["spread"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
         "config": {"workload": WORKLOAD, "global_batch": B * world, "vocab": V, "k_max": K_MAX,
-                   "ctx_len": L_CTX, "parallelism": f"request-sharded x{world}",
+                   "ctx_len": L_CTX, "parallelism": par,
                    "l2_defeat": f"{R} rotating input sets, footprint {footprint / 1e6:.0f} MB vs L2 {l2 / 1e6:.0f} MB",
-                   "graph_steps": gl, "fused": bool(args.fused)},
+                   "graph_steps": gl, "fused": bool(args.fused and comm is None)},
         "roofline": {"kernel": "verify_race_kernel (the dominant kernel: streams every algorithmic byte of the verify call)",
                      "bound": "hbm", "achieved": race_achieved, "peak": peak,
                      "unit": "GB/s", "frac": race_achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": vbytes, "launch_us": race_ms * 1e3, "peak_source": peak_src,
                      "verify_call": {"kernels": "verify_scan + verify_race + verify_emit", "launch_us": verify_ms * 1e3,
                                      "achieved": achieved, "frac": achieved / peak}},
-        "clocks": sampler.summary(),
-        "gpu_launches": st.launches_per_step * K,
+        "clocks": tm["clocks"],
+        "gpu_launches": st_launches(comm, args) * K,
         "e2e": e2e,
         "e2e_full_copy": e2e_copy,
         "tokens_per_step": tokens_total / K,
         "requests_per_s": B * world * K / (t_max / 1e3),
         "device_status": st_status,
+        "global_state_consistent": consistent,
     }
     if breakdown is not None:
         line["breakdown_us_per_launch"] = breakdown
     return line
+
+
+def close_comm(comm, world, local_rank):
+    """Every rank's exchanges are complete (streams synchronised) before any buffer is freed."""
+    if comm is None:
+        return
+    import torch
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        _barrier(dist, local_rank)
+    comm.close()
+
+
+def st_launches(comm, args):
+    from paper_2406_14066_b200 import tsv
+    if comm is not None and isinstance(comm, tsv.Comm):
+        return 10
+    return 4 if (args.fused and comm is None) else 5
+
+
+def run_strong(args, rank, world, local_rank):
+    """Strong scaling: ONE B = 256 batch split across the N ranks by request
+    (partition_requests), global alpha / k* through the same exchange as the weak line."""
+    import torch
+
+    from paper_2406_14066_b200 import dist as pdist
+    from paper_2406_14066_b200.step import SpecStep
+    dev = torch.device("cuda", _dev_index(local_rank))
+    torch.cuda.set_device(dev)
+    inp, ks, l2 = build_step_inputs("strong", rank, world, dev, args, B)
+    comm = make_comm(args, rank, world, B)
+    st = SpecStep(inp, device=dev, chunk=args.chunk, comm=comm)
+    tm = time_step_graphs(args, st, world, local_rank, dev)
+    consistent = global_state_consistent(st, world, dev)
+    per_step_tokens, per_step_vbytes = step_tokens(st, inp, ks, tm["step_ids"], dev)
+    tokens_total = pdist.sum_over_ranks(sum(per_step_tokens[t] for t in tm["step_ids"]), dev)
+    vbytes = pdist.sum_over_ranks(sum(per_step_vbytes[t] for t in tm["step_ids"]), dev) / tm["K"]
+    lbytes = pdist.sum_over_ranks(lookup_alg_bytes(inp.ctx_len[0].cpu().numpy(), inp.k_fixed), dev)
+    st_status = int(pdist.max_over_ranks(int(st.status.item()), dev))
+    footprint = sum(inp.input_bytes(s) for s in range(inp.sets))
+    R, Bl = inp.sets, inp.B
+    del st
+    close_comm(comm, world, local_rank)
+    if rank != 0:
+        return None
+    t_max, K = tm["t_max"], tm["K"]
+    ms = t_max / K
+    peak, peak_src = load_peaks()
+    step_bytes = vbytes + lbytes
+    achieved = step_bytes / (ms * 1e-3) / 1e9
+    return {
+        "metric": METRIC, "value": tokens_total / (t_max / 1e3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": tm["W"], "ms_per_step": ms, "ms_per_step_spread": tm["spread"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
+        "config": {"workload": WORKLOAD + f" -- one B={B} batch split by request over {world} ranks",
+                   "global_batch": B, "local_batch_rank0": Bl, "vocab": V, "k_max": K_MAX, "ctx_len": L_CTX,
+                   "parallelism": f"request-sharded x{world} (strong), global alpha / k* over the ranks",
+                   "l2_defeat": f"{R} rotating input sets, rank 0 footprint {footprint / 1e6:.0f} MB vs L2 {l2 / 1e6:.0f} MB",
+                   "graph_steps": tm["gl"]},
+        "roofline": {"kernel": "whole step per rank (lookup + choose-k + verify + update)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak * world, "unit": "GB/s", "frac": achieved / (peak * world),
+                     "traffic": None, "alg_bytes_per_launch": step_bytes, "launch_us": ms * 1e3,
+                     "peak_source": peak_src + f" x {world} GPUs"},
+        "clocks": tm["clocks"], "gpu_launches": st_launches(comm, args) * K, "e2e": None,
+        "tokens_per_step": tokens_total / K, "requests_per_s": B * K / (t_max / 1e3), "device_status": st_status,
+        "global_state_consistent": consistent,
+    }
 
 
 # ------------------------------------------------------------------ config 4 (vocab sharded)
@@ -498,6 +677,7 @@ def run_config4(args, rank, world, local_rank):
             tsv._check(entry(tsv.ctypes.byref(a), comm.handle, tsv._stream(stream)))
     na = torch.empty(B, dtype=torch.int32, device=dev)
     outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
+    dstat = torch.zeros(1, dtype=torch.int32, device=dev)
     sets, footprint = [], 0
     for s in range(R):  # the same logical batch on every rank (same seed), this rank's columns kept
         vb = synth.make_verify_batch(B=B, V=V4, k_max=K_MAX, lam=0.7, seed=seed + 104729 * s, device=dev)
@@ -513,7 +693,7 @@ def run_config4(args, rank, world, local_rank):
     for t in range(gl):
         vb, p, q = sets[t % R]
         a = tsv.make_verify_args(p, q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t, K_MAX, na, outt,
-                                 None, None, vocab=Vs, vocab_offset=lo, vocab_global=V4, chunk=args.chunk,
+                                 dstat, None, vocab=Vs, vocab_offset=lo, vocab_global=V4, chunk=args.chunk,
                                  flags=flags)
         args_list.append(a)
     ws = tsv.alloc_workspace(max(tsv.tsv_verify_sharded_workspace_size(a, world) for a in args_list), dev)
@@ -567,8 +747,10 @@ def run_config4(args, rank, world, local_rank):
         vbytes += float((rows * V4 * 4).sum()) / world
     tok_per_step, vbytes = tok / gl, vbytes / gl
     ms_step = t_ms / steps
-    if comm is not None:
-        comm.close()
+    st_status = int(pdist.max_over_ranks(int(dstat.item()), dev))
+    del sets
+    close_comm(comm, world, local_rank)
+    torch.cuda.empty_cache()
     if rank != 0:
         return None
     peak, peak_src = load_peaks()
@@ -593,6 +775,7 @@ def run_config4(args, rank, world, local_rank):
         "e2e": None,
         "tokens_per_step": tok_per_step,
         "requests_per_s": B / (ms_step * 1e-3),
+        "device_status": st_status,
     }
 
 
@@ -625,13 +808,14 @@ def run_greedy(args, rank, world, local_rank):
     torch.cuda.empty_cache()
     na = torch.empty(B, dtype=torch.int32, device=dev)
     outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
+    dstat = torch.zeros(1, dtype=torch.int32, device=dev)
     W, K = max(3, args.warmup), args.steps
     gl = max(1, min(args.graph_steps, K))
     args_list = []
     for t in range(gl):
         p, ro, d, _ = sets[t % R]
         rids = torch.zeros(B, dtype=torch.int32, device=dev)
-        args_list.append(tsv.make_verify_args(p, None, ro, d, rids, 0, 0, K_MAX, na, outt, None, None,
+        args_list.append(tsv.make_verify_args(p, None, ro, d, rids, 0, 0, K_MAX, na, outt, dstat, None,
                                               chunk=args.chunk))
     ws = tsv.alloc_workspace(max(tsv.tsv_verify_workspace_size(a) for a in args_list), dev)
     for a in args_list:
@@ -674,6 +858,9 @@ def run_greedy(args, rank, world, local_rank):
     tok_total = pdist.sum_over_ranks(tok, dev) / gl
     vbytes /= gl
     ms_step = t_ms / steps
+    st_status = int(pdist.max_over_ranks(int(dstat.item()), dev))
+    del sets
+    torch.cuda.empty_cache()
     if rank != 0:
         return None
     peak, peak_src = load_peaks()
@@ -681,7 +868,7 @@ def run_greedy(args, rank, world, local_rank):
     return {
         "metric": METRIC, "value": tok_total / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)", "device_status": st_status,
         "config": {"workload": f"greedy verify (temperature 0, NEXT 2): B={B}, k~U{{0..{K_MAX}}}, V={V}, fp32 p, "
                                f"drafts = target argmax w.p. 0.7", "global_batch": B * world, "vocab": V,
                    "k_max": K_MAX, "parallelism": f"request-sharded x{world}",
@@ -719,13 +906,14 @@ def run_logits(args, rank, world, local_rank):
         sets.append(vb)
     na = torch.empty(B, dtype=torch.int32, device=dev)
     outt = torch.empty((B, K_MAX + 1), dtype=torch.int32, device=dev)
+    dstat = torch.zeros(1, dtype=torch.int32, device=dev)
     W, K = max(3, args.warmup), args.steps
     gl = max(1, min(args.graph_steps, K))
     args_list = []
     for t in range(gl):
         vb = sets[t % R]
         args_list.append(tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, seed, t,
-                                              K_MAX, na, outt, None, None, chunk=args.chunk))
+                                              K_MAX, na, outt, dstat, None, chunk=args.chunk))
     ws = tsv.alloc_workspace(max(tsv.tsv_verify_logits_workspace_size(a) for a in args_list), dev)
     for a in args_list:
         a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
@@ -771,6 +959,9 @@ def run_logits(args, rank, world, local_rank):
     tok_total = pdist.sum_over_ranks(tok, dev) / gl
     vbytes /= gl
     ms_step = t_ms / steps
+    st_status = int(pdist.max_over_ranks(int(dstat.item()), dev))
+    del sets
+    torch.cuda.empty_cache()
     if rank != 0:
         return None
     peak, peak_src = load_peaks()
@@ -778,7 +969,7 @@ def run_logits(args, rank, world, local_rank):
     return {
         "metric": METRIC, "value": tok_total / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": W, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, synth/)", "device_status": st_status,
         "config": {"workload": f"fused softmax-from-logits verify (NEXT 1): B={B}, k~U{{0..{K_MAX}}}, V={V}, "
                                f"fp32 target and draft logits, temperature 1, lambda=0.7",
                    "global_batch": B * world, "vocab": V, "k_max": K_MAX, "parallelism": f"request-sharded x{world}",
@@ -885,6 +1076,87 @@ def run_config5(args, rank, world, local_rank):
         "gpu_launches": steps,
         "e2e": None,
         "requests_per_s": n_req * world / (ms_step * 1e-3),
+        "device_status": None,
+        "device_status_note": "tsv_goodput_choose_k_batched has no device-side data-error path (inputs are counts)",
+    }
+
+
+# ------------------------------------------------------------- closed decode loop (NEXT 4)
+def run_loop(args, rank, world, local_rank):
+    """The closed loop (paper_2406_14066_b200/loop.py) timed per step: lookup ->
+    choose-k (PLD, cap = proposal lengths, alpha of the previous step) -> tsv_sim_target (the synthetic
+    target's rows: the stand-in for the model forward, each draft kept w.p. alpha_true = 0.7) -> verify +
+    alpha update -> context append; B = 256 contexts of 4096 tokens, V = 32000, K = 5.  T = 64 steps per
+    CUDA graph, the graph starting from the initial state so every replay repeats the same 64 steps
+    (the generated tokens of a logged replay are exactly those of every timed replay).  Weak scaling."""
+    import torch
+
+    import synth
+    from paper_2406_14066_b200 import dist as pdist
+    from paper_2406_14066_b200.loop import ClosedLoop
+
+    dev = torch.device("cuda", _dev_index(local_rank))
+    torch.cuda.set_device(dev)
+    T, K, Lc = 64, 5, L_CTX
+    ctx, _ = synth.make_contexts(B=B, L=Lc, V=V, seed=synth.DEFAULT_SEED + 17 * rank)
+    lp = ClosedLoop(ctx, Lc, np.full(B, Lc, np.int32), V, K, synth.SPEC_DESK_TARGET, 0.05, [0.7] * T, alpha0=0.7,
+                    seed=synth.DEFAULT_SEED + rank, device=dev)
+    lp.capture(log=True, with_reset=True)  # logged replay: tokens, k*, bytes
+    lp.graph.replay()
+    torch.cuda.synchronize()
+    logs = lp.logs()
+    lp.capture(log=False, with_reset=True)
+    W, Kst = max(3, args.warmup), args.steps
+    reps = max(1, (Kst + T - 1) // T)
+    for _ in range(max(1, (W + T - 1) // T)):
+        lp.graph.replay()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(_dev_index(local_rank))
+    if world > 1:
+        import torch.distributed as dist
+        _barrier(dist, local_rank)
+    torch.cuda.synchronize()
+    with sampler:
+        e0.record(stream)
+        for _ in range(reps):
+            lp.graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    steps = reps * T
+    t_ms = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
+    m, kreq = logs["num_accepted"], logs["k_req"]
+    tok = int((m + 1).sum())  # per replay (T steps)
+    # algorithmic bytes per step: lookup (contexts) + the synthetic target rows actually used (written)
+    # + the lazy verify with one-hot drafts (row m of p; one gather per tested position) + the context
+    # append (read + write of every window)
+    rows = (kreq + 1).sum(axis=1)
+    vb = [verify_alg_bytes(m[t], kreq[t], False, V, K) for t in range(T)]
+    per_step = [lookup_alg_bytes(np.full(B, Lc), K) + int(rows[t]) * V * 4 + vb[t] + 2 * 4 * Lc * B for t in range(T)]
+    st_status = int(pdist.max_over_ranks(int(lp.status.item()), dev))
+    tok_total = pdist.sum_over_ranks(tok, dev) * reps
+    if rank != 0:
+        return None
+    ms = t_ms / steps
+    peak, peak_src = load_peaks()
+    alg = float(np.mean(per_step))
+    achieved = alg / (ms * 1e-3) / 1e9
+    return {
+        "metric": METRIC, "value": tok_total / (t_ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded, synth/; synthetic target rows from tsv_sim_target)",
+        "config": {"workload": f"closed decode loop (NEXT 4): B={B} x {Lc}-token contexts, V={V}, K={K} PLD, "
+                               f"alpha_true=0.7, {T} steps per graph", "global_batch": B * world, "vocab": V,
+                   "parallelism": f"independent loops x{world}", "graph_steps": T,
+                   "l2_defeat": "none needed: every step writes 197 MB of synthetic target rows (> L2)"},
+        "roofline": {"kernel": "whole closed-loop step (lookup, choose-k, sim_target, verify + update, append)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "alg_bytes_per_launch": alg, "launch_us": ms * 1e3, "peak_source": peak_src,
+                     "note": "tsv_sim_target writes all B (K+1) rows (197 MB); only the used rows count as algorithmic"},
+        "clocks": sampler.summary(), "gpu_launches": 8 * steps, "e2e": None,
+        "tokens_per_step": tok / T, "k_star_mean": float(np.mean(logs["k_star"])),
+        "alpha_last": float(logs["alpha"][-1]), "device_status": st_status,
     }
 
 
@@ -1047,9 +1319,10 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if args.workload in ("config4", "greedy", "logits", "config5"):
-        fn = {"config4": run_config4, "greedy": run_greedy, "logits": run_logits, "config5": run_config5}[args.workload]
-        line = fn(args, rank, world, local_rank)
+    runners = {"config4": run_config4, "greedy": run_greedy, "logits": run_logits, "config5": run_config5,
+               "loop": run_loop, "strong": run_strong}
+    if args.workload in runners:
+        line = runners[args.workload](args, rank, world, local_rank)
         if line is not None:
             print(json.dumps(line), file=_JSON_OUT, flush=True)
         if world > 1:
@@ -1058,6 +1331,30 @@ def main():
             dist.destroy_process_group()
         return
     line = run_ours(args, rank, world, local_rank)
+    if not args.no_extras:
+        # every other workload of BASELINE.json / SURVEY.md 8(f) as a sub-object of the one JSON line, each
+        # timed the same way (its own CUDA events, roofline, clocks and device status)
+        extras = {}
+        plan = [("strong", run_strong, {})] if world > 1 else []
+        plan += [("config4", run_config4, {"shard_mode": "auto"})]
+        if world == 1:
+            plan += [("config4_sharded_p2p", run_config4, {"shard_mode": "p2p"})]
+        plan += [("greedy", run_greedy, {}), ("logits", run_logits, {}), ("config5", run_config5, {}),
+                 ("loop", run_loop, {})]
+        for name, fn, over in plan:
+            a2 = argparse.Namespace(**vars(args))
+            for k, v in over.items():
+                setattr(a2, k, v)
+            t0 = time.perf_counter()
+            try:
+                sub = fn(a2, rank, world, local_rank)
+            except Exception as e:  # noqa: BLE001  (a failed sub-workload must not hide the main line)
+                sub = {"error": f"{type(e).__name__}: {e}"[:300]} if rank == 0 else None
+            if sub is not None:
+                sub["wall_s"] = round(time.perf_counter() - t0, 2)
+                extras[name] = sub
+        if line is not None:
+            line["workloads"] = extras
     if line is not None:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()

@@ -415,6 +415,35 @@ TSV_API tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, con
 TSV_API tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                     double decay, int32_t estimator, void* stream);
 
+/* --------------------------------------------------------------------------
+ * Request-sharded step over NVLink peer memory (the exchange fused into
+ * its producing kernels, no NCCL launch): every rank holds a disjoint set of the batch's
+ * requests (global request ids) and one tsv_p2p handle (tsv_p2p_alloc/open/init below).
+ *  tsv_goodput_choose_k_p2p: ONE kernel -- this rank's exact int64 ArgMaxGoodput sums
+ *    (tsv_goodput_partial), summed over the ranks through peer memory, then Listing 2 on
+ *    the global sums (tsv_goodput_finalize): k*, goodput and k_i = min(k*, cap_i) for the
+ *    local requests, bit-identical to one device holding the whole batch.  B may be 0
+ *    (the rank still takes part).  Arguments as tsv_goodput_choose_k.
+ *  tsv_update_acceptance_p2p: UpdateGlobalAcceptance with (sum m, sum t) summed over the
+ *    ranks before the EWMA (every rank applies the same update); per_request != 0 updates
+ *    the local alphas with no exchange.
+ *  tsv_verify_accept_update_p2p: tsv_verify_accept_update whose update CTA (beside the
+ *    race) performs that exchange -- the global alpha costs no extra launch.
+ * All ranks must make the same sequence of exchange calls (tsv_goodput_choose_k_p2p,
+ * tsv_update_acceptance_p2p, tsv_verify_accept_update_p2p, tsv_allreduce_i64_p2p share
+ * one epoch).  device_status (nullable) gets TSV_DEVSTATUS_P2P_TIMEOUT.
+ * ------------------------------------------------------------------------ */
+TSV_API tsv_status tsv_goodput_choose_k_p2p(const double* alpha, int32_t alpha_per_request, const int32_t* ctx_len,
+                                            const int32_t* cap, int32_t B, int32_t k_max, int32_t policy,
+                                            tsv_latency_model target, tsv_latency_model draft, double pld_cost_ms,
+                                            int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
+                                            int32_t* k_per_request, tsv_p2p* p, int32_t* device_status, void* stream);
+TSV_API tsv_status tsv_update_acceptance_p2p(double* alpha, int32_t per_request, const int32_t* num_accepted,
+                                             const int32_t* row_offsets, int32_t B, double decay, int32_t estimator,
+                                             tsv_p2p* p, int32_t* device_status, void* stream);
+TSV_API tsv_status tsv_verify_accept_update_p2p(const tsv_verify_args* a, double* alpha, int32_t per_request,
+                                                double decay, int32_t estimator, tsv_p2p* p, void* stream);
+
 /* Latency-model fit (reading R25; "fits a linear regression
  * model"): ordinary least squares of ms[i] on (ctx_tokens[i],
  * batched_tokens[i], 1) over n >= 3 HOST samples; while a coefficient is negative,

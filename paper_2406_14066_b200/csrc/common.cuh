@@ -235,6 +235,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // Every kernel of a step is launched with programmaticStreamSerialization: it may start
 // while its predecessor drains, runs its prologue, and blocks in griddepcontrol.wait
 // before touching data the predecessor produced (full completion + visibility).
+// OR status bits into the caller's device_status word (nullable).
+__device__ __forceinline__ void report(int32_t* devstatus, uint32_t bits) {
+    if (devstatus && bits) atomicOr(reinterpret_cast<unsigned int*>(devstatus), bits);
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -29,6 +29,51 @@ __global__ void __launch_bounds__(kGpChooseThreads) goodput_choose_k_kernel(cons
     choose_k_block<kGpChooseThreads>(A);
 }
 
+// Request-sharded ArgMaxGoodput in ONE kernel (the exchange step fused with its
+// producer and consumer): this rank's exact int64 batch sums, summed over the ranks through
+// NVLink peer memory (p2p.cuh), then Listing 2 on the global sums -- bit-identical to one device
+// holding the whole batch.  k_i = min(k*, cap_i) for this rank's requests.
+__global__ void __launch_bounds__(kGpChooseThreads) goodput_choose_k_p2p_kernel(const ChooseArgs A, const P2PView V,
+                                                                              int32_t* devstatus) {
+    __shared__ long long s_sums[2 * kGpMaxK + 4];
+    __shared__ int s_best;
+    pdl_wait();
+    pdl_launch_dependents();
+    int32_t caps[kGpCapCache];
+    const GpTotals t = gp_sums_block<kGpChooseThreads>(A, caps);
+    const int lane = threadIdx.x & 31;
+    const int32_t K1 = A.k_max + 1;
+    if (threadIdx.x < 32) {
+        if (lane <= A.k_max) {
+            s_sums[lane] = t.L;
+            s_sums[K1 + lane] = t.N;
+        }
+        if (lane == 0) {
+            s_sums[2 * K1] = t.c0;
+            s_sums[2 * K1 + 1] = t.c1;
+            s_sums[2 * K1 + 2] = t.c2;
+            s_sums[2 * K1 + 3] = t.c3;
+        }
+    }
+    __syncthreads();
+    p2p_allreduce_block(s_sums, 2 * K1 + 4, V, devstatus);  // ends with a CTA barrier
+    if (threadIdx.x < 32) {
+        GpTotals g;
+        g.L = lane <= A.k_max ? s_sums[lane] : 0;
+        g.N = lane <= A.k_max ? s_sums[K1 + lane] : 0;
+        g.c0 = s_sums[2 * K1];
+        g.c1 = s_sums[2 * K1 + 1];
+        g.c2 = s_sums[2 * K1 + 2];
+        g.c3 = s_sums[2 * K1 + 3];
+        const int kb = gp_argmax_warp(A, g);
+        if (lane == 0) s_best = kb;
+    }
+    if (A.k_per_request && A.B > 0) {
+        __syncthreads();
+        gp_write_k_per_request<kGpChooseThreads>(A, s_best, caps);
+    }
+}
+
 __global__ void __launch_bounds__(kGpThreads) update_acceptance_kernel(const UpdateArgs A) {
     pdl_wait();
     pdl_launch_dependents();
@@ -279,7 +324,7 @@ extern "C" tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, 
     if (B == 0) return TSV_OK;
     TSV_REQUIRE(alpha && num_accepted && row_offsets, "tsv_update_acceptance: a required array is NULL");
     TSV_TRY(check_device());
-    UpdateArgs A;
+    UpdateArgs A = {};
     A.alpha = alpha;
     A.num_accepted = num_accepted;
     A.row_offsets = row_offsets;
@@ -287,6 +332,67 @@ extern "C" tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, 
     A.per_request = per_request;
     A.B = B;
     A.estimator = estimator;
+    TSV_CUDA(launch_pdl(update_acceptance_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream), A),
+             "update_acceptance_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_goodput_choose_k_p2p(const double* alpha, int32_t alpha_per_request, const int32_t* ctx_len,
+                                               const int32_t* cap, int32_t B, int32_t k_max, int32_t policy,
+                                               tsv_latency_model target, tsv_latency_model draft, double pld_cost_ms,
+                                               int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
+                                               int32_t* k_per_request, tsv_p2p* p, int32_t* device_status,
+                                               void* stream) {
+    TSV_REQUIRE(B >= 0, "tsv_goodput_choose_k_p2p: B < 0 (%d)", B);
+    TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_choose_k_p2p: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
+    TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_choose_k_p2p: unknown policy %d",
+                policy);
+    TSV_REQUIRE(p != nullptr, "tsv_goodput_choose_k_p2p: p2p handle is NULL");
+    TSV_REQUIRE(alpha && k_out && (B == 0 || (ctx_len && cap)), "tsv_goodput_choose_k_p2p: a required array is NULL");
+    TSV_TRY(check_device());
+    ChooseArgs A = {};
+    A.alpha = alpha;
+    A.ctx_len = ctx_len;
+    A.cap = cap;
+    A.k_out = k_out;
+    A.goodput_out = goodput_out;
+    A.k_per_request = k_per_request;
+    A.target = target;
+    A.draft = draft;
+    A.pld_cost_ms = pld_cost_ms;
+    A.kv_free = static_cast<long long>(kv_free_slots);
+    A.alpha_per_request = alpha_per_request;
+    A.B = B;
+    A.k_max = k_max;
+    A.policy = policy;
+    TSV_CUDA(launch_pdl(goodput_choose_k_p2p_kernel, dim3(1), dim3(kGpChooseThreads), 0,
+                        static_cast<cudaStream_t>(stream), A, p->view, device_status),
+             "goodput_choose_k_p2p_kernel launch");
+    return TSV_OK;
+}
+
+extern "C" tsv_status tsv_update_acceptance_p2p(double* alpha, int32_t per_request, const int32_t* num_accepted,
+                                                const int32_t* row_offsets, int32_t B, double decay, int32_t estimator,
+                                                tsv_p2p* p, int32_t* device_status, void* stream) {
+    TSV_REQUIRE(B >= 0, "tsv_update_acceptance_p2p: B < 0");
+    TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_update_acceptance_p2p: decay %g outside [0, 1]", decay);
+    TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED,
+                "tsv_update_acceptance_p2p: unknown estimator");
+    TSV_REQUIRE(p != nullptr && alpha != nullptr, "tsv_update_acceptance_p2p: NULL argument");
+    TSV_REQUIRE(B == 0 || (num_accepted && row_offsets), "tsv_update_acceptance_p2p: a required array is NULL");
+    if (per_request && B == 0) return TSV_OK;  // per-request alphas: no exchange
+    TSV_TRY(check_device());
+    UpdateArgs A = {};
+    A.alpha = alpha;
+    A.num_accepted = num_accepted;
+    A.row_offsets = row_offsets;
+    A.decay = decay;
+    A.per_request = per_request;
+    A.B = B;
+    A.estimator = estimator;
+    A.use_p2p = per_request ? 0 : 1;
+    A.devstatus = device_status;
+    A.p2p = p->view;
     TSV_CUDA(launch_pdl(update_acceptance_kernel, dim3(1), dim3(kGpThreads), 0, static_cast<cudaStream_t>(stream), A),
              "update_acceptance_kernel launch");
     return TSV_OK;

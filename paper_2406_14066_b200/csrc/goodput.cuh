@@ -4,6 +4,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "p2p.cuh"
 
 namespace tsv {
 
@@ -49,6 +50,11 @@ struct UpdateArgs {
     const int32_t* row_offsets;
     double decay;
     int32_t per_request, B, estimator;
+    // request-sharded global alpha: the (sum m, sum t) pair is summed over the
+    // ranks through peer memory (p2p.cuh) before the EWMA; every rank applies the same update
+    int32_t use_p2p;
+    int32_t* devstatus;  // TSV_DEVSTATUS_P2P_TIMEOUT (nullable)
+    P2PView p2p;
 };
 
 // Batch sums of ArgMaxGoodput, exact int64 (fixed point 2^-32 for the token sums):
@@ -250,6 +256,7 @@ __device__ __forceinline__ void update_block(const UpdateArgs& A, long long* sum
         red[warp][1] = stt;
     }
     __syncthreads();
+    __shared__ long long s_ab[2];
     if (threadIdx.x == 0) {
         long long a = 0, b = 0;
 #pragma unroll
@@ -260,9 +267,16 @@ __device__ __forceinline__ void update_block(const UpdateArgs& A, long long* sum
         if (sums_out) {
             sums_out[0] = a;
             sums_out[1] = b;
-        } else {
+        } else if (!A.use_p2p) {
             ewma_apply(A.alpha, a, b, A.decay);
         }
+        s_ab[0] = a;
+        s_ab[1] = b;
+    }
+    if (A.use_p2p && !sums_out) {  // the ranks' pairs summed over peer memory, then the same EWMA everywhere
+        __syncthreads();
+        p2p_allreduce_block(s_ab, 2, A.p2p, A.devstatus);
+        if (threadIdx.x == 0) ewma_apply(A.alpha, s_ab[0], s_ab[1], A.decay);
     }
 }
 

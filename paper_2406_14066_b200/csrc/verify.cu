@@ -31,6 +31,7 @@
 #include <algorithm>
 
 #include "goodput.cuh"
+#include "p2p.cuh"
 
 namespace tsv {
 
@@ -215,10 +216,6 @@ __device__ __forceinline__ void quad_weights(float (&w)[4], const float4& a, con
     }
 }
 
-__device__ __forceinline__ void report(int32_t* devstatus, uint32_t bits) {
-    if (devstatus && bits) atomicOr(reinterpret_cast<unsigned int*>(devstatus), bits);
-}
-
 // Request i's rows lie inside the allocations (tsv.h: device-side data errors): k_i in
 // [0, k_max], its p rows r0 .. r1-1 below rows_lim, and its drafts / q rows qbase .. qbase+k-1
 // (qbase = r0 - i) below rows_lim - B.  rows_lim is the host-known rows_p, or for the dense
@@ -399,13 +396,21 @@ __device__ __forceinline__ void update_cta(const UpdateArgs& A) {
         red2[warp][1] = stt;
     }
     __syncthreads();
+    __shared__ long long s_ab[2];
     if (threadIdx.x == 0) {
         long long a = 0, b = 0;
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
             a += red2[w][0];
             b += red2[w][1];
         }
-        ewma_apply(A.alpha, a, b, A.decay);
+        if (!A.use_p2p) ewma_apply(A.alpha, a, b, A.decay);
+        s_ab[0] = a;
+        s_ab[1] = b;
+    }
+    if (A.use_p2p) {  // request-sharded global alpha: sum the pair over the ranks (p2p.cuh), same EWMA everywhere
+        __syncthreads();
+        p2p_allreduce_block(s_ab, 2, A.p2p, A.devstatus);
+        if (threadIdx.x == 0) ewma_apply(A.alpha, s_ab[0], s_ab[1], A.decay);
     }
 }
 
@@ -859,89 +864,13 @@ __global__ void __launch_bounds__(256) verify_shard_emit_kernel(const RaceParams
 // lives on the device (own buffer), read by every kernel of a call and advanced by the
 // emit kernel's last CTA, so captured CUDA graphs replay with advancing epochs.  A wait
 // gives up after seconds and sets TSV_DEVSTATUS_P2P_TIMEOUT instead of hanging.
-struct P2PView {
-    unsigned char* buf[TSV_P2P_MAX_WORLD];  // rank g's symmetric buffer as mapped in this process
-    int32_t rank, G, B_max;
-};
-constexpr size_t kP2PHdr = 256;  // u32 verify epoch at 0, emit-arrival counter at 4, all-reduce epoch at 8
-// round 1 slot: 16 B per request {acc, e, own, e}; round 2 slot: 32 B {key lo/hi, fb lo/hi, each with e}
-__host__ __device__ constexpr size_t p2p_masks_bytes(int32_t B_max) {
-    return 2ull * TSV_P2P_MAX_WORLD * static_cast<size_t>(B_max) * 16ull;
-}
-constexpr size_t kP2PSumsBytes = 2ull * TSV_P2P_MAX_WORLD * TSV_P2P_MAX_SUMS * 16ull;  // [2][W][n] LL lines
-__host__ __device__ constexpr size_t p2p_buffer_bytes(int32_t B_max) {
-    return kP2PHdr + 3ull * p2p_masks_bytes(B_max) + kP2PSumsBytes;
-}
-__device__ __forceinline__ uint32_t* p2p_epoch(const P2PView& V) {
-    return reinterpret_cast<uint32_t*>(V.buf[V.rank]);
-}
-__device__ __forceinline__ uint32_t* p2p_counter(const P2PView& V) {
-    return reinterpret_cast<uint32_t*>(V.buf[V.rank]) + 1;
-}
-__device__ __forceinline__ uint32_t p2p_load_epoch(const P2PView& V) {
-    return *reinterpret_cast<volatile uint32_t*>(p2p_epoch(V)) + 1u;  // this call's epoch (E + 1)
-}
-__device__ __forceinline__ uint4* p2p_masks(const P2PView& V, uint32_t e, int32_t owner, int32_t slot) {
-    return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr) +
-           (static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + slot) * V.B_max;
-}
-__device__ __forceinline__ uint4* p2p_keys(const P2PView& V, uint32_t e, int32_t owner, int32_t slot) {
-    return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr + p2p_masks_bytes(V.B_max)) +
-           (static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + slot) * 2 * V.B_max;
-}
-__device__ __forceinline__ void st_ll(uint4* p, uint4 v) {
-    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
-}
-__device__ __forceinline__ uint4 ld_ll(const uint4* p) {
-    uint4 v;
-    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p) : "memory");
-    return v;
-}
-// Poll one 16-byte LL line until both 8-byte halves carry epoch e (bounded).
-__device__ __forceinline__ uint4 ld_ll_wait(const uint4* p, uint32_t e, int32_t* devstatus) {
-    uint4 v = ld_ll(p);
-    uint32_t n = 0;
-    while (v.y != e || v.w != e) {
-        __nanosleep(32);
-        if (++n == (1u << 26)) {  // seconds: a peer never arrived
-            report(devstatus, TSV_DEVSTATUS_P2P_TIMEOUT);
-            break;
-        }
-        v = ld_ll(p);
-    }
-    return v;
-}
-
 // All-reduce (sum) of count <= TSV_P2P_MAX_SUMS int64 over the ranks (request-sharded global
-// goodput / acceptance sums): one CTA; thread j pushes data[j] as two LL words into slot
-// [rank][j] of every peer, then polls its own buffer's G slots and writes the exact sum.
-// Its own epoch (header word 2) advances at the end of every call.
+// goodput / acceptance sums, p2p.cuh): one CTA, data in global memory.
 __global__ void __launch_bounds__(64) p2p_allreduce_i64_kernel(int64_t* data, int32_t count, const P2PView V,
                                                                int32_t* devstatus) {
     pdl_wait();
     pdl_launch_dependents();
-    uint32_t* ep = reinterpret_cast<uint32_t*>(V.buf[V.rank]) + 2;
-    const uint32_t e = *reinterpret_cast<volatile uint32_t*>(ep) + 1u;
-    const int32_t j = threadIdx.x;
-    auto slot = [&](int32_t owner, int32_t from) {
-        return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr + 3ull * p2p_masks_bytes(V.B_max)) +
-               (static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + from) * TSV_P2P_MAX_SUMS + j;
-    };
-    if (j < count) {
-        const uint64_t x = static_cast<uint64_t>(data[j]);
-        for (int32_t g = 0; g < V.G; ++g)
-            st_ll(slot(g, V.rank), make_uint4(static_cast<uint32_t>(x), e, static_cast<uint32_t>(x >> 32), e));
-        uint64_t sum = 0;
-        for (int32_t g = 0; g < V.G; ++g) {
-            const uint4 v = ld_ll_wait(slot(V.rank, g), e, devstatus);
-            sum += (static_cast<uint64_t>(v.z) << 32) | v.x;
-        }
-        data[j] = static_cast<int64_t>(sum);
-    }
-    __syncthreads();
-    if (j == 0) *ep = e;
+    p2p_allreduce_block(reinterpret_cast<long long*>(data), count, V, devstatus);
 }
 
 __global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams P, const P2PView V) {
@@ -1602,7 +1531,7 @@ extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double*
                 "tsv_verify_accept_update: workspace too small (%llu < %llu bytes)",
                 (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
     TSV_TRY(check_device());
-    UpdateArgs ua;
+    UpdateArgs ua = {};
     ua.alpha = alpha;
     ua.num_accepted = a->num_accepted;
     ua.row_offsets = a->row_offsets;
@@ -1610,6 +1539,36 @@ extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double*
     ua.per_request = per_request;
     ua.B = a->B;
     ua.estimator = estimator;
+    return run_verify<kLazy>(a, make_params(a), static_cast<cudaStream_t>(stream), &ua);
+}
+
+extern "C" tsv_status tsv_verify_accept_update_p2p(const tsv_verify_args* a, double* alpha, int32_t per_request,
+                                                   double decay, int32_t estimator, tsv_p2p* p, void* stream) {
+    TSV_TRY(validate(a));
+    TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
+                "tsv_verify_accept_update_p2p: needs the whole vocabulary (request-sharded mode)");
+    TSV_REQUIRE(alpha != nullptr && p != nullptr, "tsv_verify_accept_update_p2p: NULL argument");
+    TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_verify_accept_update_p2p: decay %g outside [0, 1]", decay);
+    TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED,
+                "tsv_verify_accept_update_p2p: unknown estimator");
+    if (a->B == 0)  // no local requests: this rank still takes part in the exchange (zero sums)
+        return tsv_update_acceptance_p2p(alpha, per_request, a->num_accepted, a->row_offsets, 0, decay, estimator, p,
+                                         a->device_status, stream);
+    TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
+                   "tsv_verify_accept_update_p2p: workspace too small (%llu < %llu bytes)",
+                   (unsigned long long)a->workspace_bytes, (unsigned long long)workspace_bytes(a));
+    TSV_TRY(check_device());
+    UpdateArgs ua = {};
+    ua.alpha = alpha;
+    ua.num_accepted = a->num_accepted;
+    ua.row_offsets = a->row_offsets;
+    ua.decay = decay;
+    ua.per_request = per_request;
+    ua.B = a->B;
+    ua.estimator = estimator;
+    ua.use_p2p = per_request ? 0 : 1;
+    ua.devstatus = a->device_status;
+    ua.p2p = p->view;
     return run_verify<kLazy>(a, make_params(a), static_cast<cudaStream_t>(stream), &ua);
 }
 
@@ -1899,9 +1858,6 @@ extern "C" tsv_status tsv_debug_race_row(const float* w, const uint32_t* words, 
 }
 
 // ------------------------------------------------------------ peer-memory vocab sharding (host)
-struct tsv_p2p {
-    tsv::P2PView view;
-};
 
 extern "C" tsv_status tsv_p2p_buffer_size(int32_t B_max, size_t* bytes) {
     TSV_REQUIRE(bytes != nullptr && B_max >= 1, "tsv_p2p_buffer_size: bad arguments");

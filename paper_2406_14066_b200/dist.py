@@ -91,3 +91,22 @@ def exchange_handles(local: bytes, rank: int, world: int, group=None) -> list:
     assert all(isinstance(b, bytes) and len(b) == len(local) for b in out), "handle exchange failed"
     assert out[rank] == local
     return out
+
+
+def request_slice(p, q, row_offsets, draft_tokens, request_ids, lo: int, hi: int):
+    """Requests [lo, hi) of one ragged verify batch as their own batch (views of the same storage):
+    p rows row_offsets[lo] .. row_offsets[hi]-1, q rows / drafts shifted by the request index
+    (packing row_offsets[i] - i), offsets rebased to 0.  Request ids stay GLOBAL (R6), so a rank's
+    outputs equal the unsharded run's for its requests."""
+    import torch
+    ro = row_offsets.to(torch.int64)
+    r0, r1 = int(ro[lo]), int(ro[hi])
+    q0, q1 = r0 - lo, r1 - hi
+    sub_ro = (row_offsets[lo:hi + 1] - row_offsets[lo]).contiguous()
+    return (p[r0:r1], None if q is None else q[q0:q1], sub_ro, draft_tokens[q0:q1], request_ids[lo:hi])
+
+
+def context_slice(ctx, ctx_offsets, lo: int, hi: int):
+    """Contexts of requests [lo, hi) with offsets rebased to 0 (host or device tensors)."""
+    c0, c1 = int(ctx_offsets[lo]), int(ctx_offsets[hi])
+    return ctx[c0:c1], (ctx_offsets[lo:hi + 1] - ctx_offsets[lo])

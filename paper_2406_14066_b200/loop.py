@@ -30,6 +30,7 @@ class ClosedLoop:
         self.n_min, self.n_max = int(n_min), int(n_max)
         i32 = torch.int32
         self.ctx = [torch.tensor(np.asarray(ctx0, np.int32), device=dev), torch.empty(B * L, dtype=i32, device=dev)]
+        self._init = (self.ctx[0].clone(), torch.tensor(np.asarray(ctx_len0, np.int32), device=dev), float(alpha0))
         self.ctx_offsets = torch.arange(0, (B + 1) * L, L, dtype=i32, device=dev)
         self.ctx_len = torch.tensor(np.asarray(ctx_len0, np.int32), device=dev)
         self.alpha = torch.full((1,), float(alpha0), dtype=torch.float64, device=dev)
@@ -67,7 +68,14 @@ class ClosedLoop:
             a.workspace, a.workspace_bytes = self.workspace.data_ptr(), self.workspace.numel()
         self.graph: Optional[torch.cuda.CUDAGraph] = None
 
-    def step(self, t: int, stream=None):
+    def reset(self, stream=None):
+        """Back to the initial contexts, context lengths and alpha (device copies; graph-capturable)."""
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+            self.ctx[0].copy_(self._init[0])
+            self.ctx_len.copy_(self._init[1])
+            self.alpha.fill_(self._init[2])
+
+    def step(self, t: int, stream=None, log: bool = True):
         """Launch decode step t (reads window t % 2, writes the other)."""
         L_ = tsv.lib()
         st = tsv._stream(stream)
@@ -87,6 +95,8 @@ class ClosedLoop:
                                                tsv.EST_TESTED, st))
         tsv._check(L_.tsv_context_append(cin.data_ptr(), self.L, B, self.out_tokens.data_ptr(),
                                          self.num_accepted.data_ptr(), K, cout.data_ptr(), self.ctx_len.data_ptr(), st))
+        if not log:
+            return
         with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
             self.log_k[t:t + 1].copy_(self.k_star)
             self.log_alpha[t:t + 1].copy_(self.alpha)
@@ -101,16 +111,19 @@ class ClosedLoop:
         for t in range(self.T):
             self.step(t)
 
-    def capture(self):
-        """All T steps as one CUDA graph (replay() runs the whole closed loop)."""
+    def capture(self, log: bool = True, with_reset: bool = False):
+        """All T steps as one CUDA graph (replay() runs the whole closed loop).  with_reset: the graph
+        starts from the initial state, so every replay repeats the same T steps (timing)."""
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             with torch.cuda.graph(g, stream=side):
+                if with_reset:
+                    self.reset(stream=side)
                 for t in range(self.T):
-                    self.step(t, stream=side)
+                    self.step(t, stream=side, log=log)
         self.graph = g
 
     def logs(self):

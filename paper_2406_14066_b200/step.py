@@ -70,9 +70,18 @@ class SpecStep:
     -- 5 kernels chained with PDL (the alpha update is an extra CTA of verify's emit kernel).
     fused=True: tsv_propose_lookup_choose_k (the lookup CTA that finishes last runs choose-k)
     + tsv_verify_accept_update, 4 kernels.  Identical outputs (tests/test_gpu_parity.py);
-    the last-CTA handshake costs more than the kernel boundary it saves on B200."""
+    the last-CTA handshake costs more than the kernel boundary it saves on B200.
 
-    def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0, fused: bool = False):
+    comm (request-sharded): this rank holds a disjoint part of one batch (global
+    request ids) and alpha / k* are global -- one server over the ranks.
+      tsv.P2PComm: tsv_goodput_choose_k_p2p (sums exchanged over NVLink peer memory inside the
+        kernel) and tsv_verify_accept_update_p2p (the update CTA exchanges (sum m, sum t)):
+        still 5 kernels per step, no NCCL launch;
+      tsv.Comm (NCCL): partial -> ncclAllReduce -> finalize for both, 10 launches.
+    k*, every k_i, every emitted token and alpha equal one device holding the whole batch."""
+
+    def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0, fused: bool = False,
+                 comm=None):
         self.inp = inp
         B, K = inp.B, inp.k_max
         dev = torch.device(device)
@@ -87,6 +96,12 @@ class SpecStep:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.counter = tsv.lookup_choose_scratch(dev)  # fused lookup + choose-k
         self.fused = fused
+        self.comm = comm
+        self.p2p = comm is not None and not isinstance(comm, tsv.Comm)
+        if fused and comm is not None:
+            raise ValueError("the fused lookup + choose-k has no request-sharded variant")
+        self.sums_ws = torch.zeros(tsv.gp_sums_len(inp.k_fixed), dtype=torch.int64, device=dev)
+        self.upd_ws = torch.zeros(2, dtype=torch.int64, device=dev)
         self.args = []
         for vb in inp.verify:
             # the batch's row_offsets / drafts / request ids are inputs of the step, never written by
@@ -104,7 +119,35 @@ class SpecStep:
 
     @property
     def launches_per_step(self) -> int:
+        if self.comm is not None and not self.p2p:
+            return 10  # lookup, 3 x choose-k (partial, NCCL, finalize), 3 x verify, 3 x update
         return 4 if self.fused else 5
+
+    def _choose_k(self, s, st):
+        inp, L = self.inp, tsv.lib()
+        args = (self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(), self.proposal_len.data_ptr(), inp.B,
+                inp.k_fixed, tsv.POLICY_PLD, tsv.LatencyModel(*inp.target), tsv.LatencyModel(*inp.draft),
+                float(inp.pld_cost_ms), int(inp.kv_free_slots), self.k_star.data_ptr(), self.goodput.data_ptr(),
+                self.k_req.data_ptr())
+        if self.comm is None:
+            tsv._check(L.tsv_goodput_choose_k(*args, st))
+        elif self.p2p:
+            tsv._check(L.tsv_goodput_choose_k_p2p(*args, self.comm.handle, self.status.data_ptr(), st))
+        else:
+            tsv._check(L.tsv_goodput_choose_k_sharded(*args, self.sums_ws.data_ptr(), self.comm.handle, st))
+
+    def _verify_update(self, a, s, st):
+        L = tsv.lib()
+        if self.comm is None:
+            tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9, tsv.EST_TESTED, st))
+        elif self.p2p:
+            tsv._check(L.tsv_verify_accept_update_p2p(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
+                                                      tsv.EST_TESTED, self.comm.handle, st))
+        else:
+            tsv._check(L.tsv_verify_accept(tsv.ctypes.byref(a), st))
+            tsv._check(L.tsv_update_acceptance_sharded(self.alpha.data_ptr(), self.num_accepted.data_ptr(),
+                                                       self.inp.verify[s].row_offsets.data_ptr(), self.inp.B, 0.9,
+                                                       tsv.EST_TESTED, self.upd_ws.data_ptr(), self.comm.handle, st))
 
     def run(self, step: int, stream=None):
         """Launch one decode step on ``stream`` (default: current)."""
@@ -127,16 +170,10 @@ class SpecStep:
         tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
                                         inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
                                         self.proposal_len.data_ptr(), self.status.data_ptr(), st))
-        tsv._check(L.tsv_goodput_choose_k(self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(),
-                                          self.proposal_len.data_ptr(), inp.B, inp.k_fixed,
-                                          tsv.POLICY_PLD, tsv.LatencyModel(*inp.target),
-                                          tsv.LatencyModel(*inp.draft), float(inp.pld_cost_ms),
-                                          int(inp.kv_free_slots), self.k_star.data_ptr(),
-                                          self.goodput.data_ptr(), self.k_req.data_ptr(), st))
+        self._choose_k(s, st)
         a = self.args[s]
         a.step = step & 0xFFFFFFFF
-        tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
-                                              tsv.EST_TESTED, st))
+        self._verify_update(a, s, st)
 
     def run_component(self, name: str, step: int, stream=None):
         """One launch of a single step component (timing breakdown only)."""
@@ -149,12 +186,7 @@ class SpecStep:
                                             inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
                                             self.proposal_len.data_ptr(), self.status.data_ptr(), st))
         elif name == "choose_k":
-            tsv._check(L.tsv_goodput_choose_k(self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(),
-                                              self.proposal_len.data_ptr(), inp.B, inp.k_fixed,
-                                              tsv.POLICY_PLD, tsv.LatencyModel(*inp.target),
-                                              tsv.LatencyModel(*inp.draft), float(inp.pld_cost_ms),
-                                              int(inp.kv_free_slots), self.k_star.data_ptr(),
-                                              self.goodput.data_ptr(), self.k_req.data_ptr(), st))
+            self._choose_k(s, st)
         elif name == "verify":
             a = self.args[s]
             a.step = step & 0xFFFFFFFF
@@ -162,8 +194,7 @@ class SpecStep:
         elif name == "verify_update":
             a = self.args[s]
             a.step = step & 0xFFFFFFFF
-            tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
-                                                  tsv.EST_TESTED, st))
+            self._verify_update(a, s, st)
         elif name == "update":
             tsv._check(L.tsv_update_acceptance(self.alpha.data_ptr(), 0, self.num_accepted.data_ptr(),
                                                inp.verify[s].row_offsets.data_ptr(), inp.B, 0.9,

@@ -50,6 +50,7 @@ EXPORTED = [
     "tsv_context_append", "tsv_goodput_choose_k_batched", "tsv_debug_race_row",
     "tsv_p2p_buffer_size", "tsv_p2p_alloc", "tsv_p2p_free", "tsv_p2p_open", "tsv_p2p_close", "tsv_p2p_init",
     "tsv_p2p_destroy", "tsv_verify_accept_sharded_p2p", "tsv_verify_shard_p2p_phase", "tsv_allreduce_i64_p2p",
+    "tsv_goodput_choose_k_p2p", "tsv_update_acceptance_p2p", "tsv_verify_accept_update_p2p",
 ]
 
 
@@ -150,6 +151,10 @@ def _load() -> ctypes.CDLL:
         "tsv_verify_accept_sharded_p2p": ([ctypes.POINTER(VerifyArgs), P, P], ctypes.c_int),
         "tsv_verify_shard_p2p_phase": ([ctypes.POINTER(VerifyArgs), P, i32, P], ctypes.c_int),
         "tsv_allreduce_i64_p2p": ([P, i32, P, P, P], ctypes.c_int),
+        "tsv_goodput_choose_k_p2p": ([P, i32, P, P, i32, i32, i32, LatencyModel, LatencyModel, f64, i64,
+                                      P, P, P, P, P, P], ctypes.c_int),
+        "tsv_update_acceptance_p2p": ([P, i32, P, P, i32, f64, i32, P, P, P], ctypes.c_int),
+        "tsv_verify_accept_update_p2p": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -652,6 +657,21 @@ class P2PLoopback:
         self.handles, self.bufs = [], []
 
 
+class P2PLoopbackRank:
+    """Rank g of a P2PLoopback, usable wherever a P2PComm is (tests)."""
+
+    def __init__(self, lb: "P2PLoopback", g: int):
+        self.handle, self.rank, self.world = lb.handles[g], g, lb.world
+
+
+def tsv_verify_accept_update_p2p(args: VerifyArgs, alpha, p2p, decay=0.9, estimator=EST_TESTED, per_request=False,
+                                 stream=None):
+    """Verify/accept + the request-sharded global alpha update, the (sum m, sum t) exchange done by
+    the update CTA beside the race over peer memory (tsv_verify_accept_update_p2p)."""
+    _check(_lib.tsv_verify_accept_update_p2p(ctypes.byref(args), _ptr(alpha), 1 if per_request else 0, float(decay),
+                                             int(estimator), p2p.handle, _stream(stream)))
+
+
 def tsv_verify_accept_sharded_p2p(args: VerifyArgs, p2p, stream=None):
     h = p2p.handle if hasattr(p2p, "handle") else p2p
     _check(_lib.tsv_verify_accept_sharded_p2p(ctypes.byref(args), h, _stream(stream)))
@@ -681,10 +701,10 @@ def tsv_allreduce_i64_p2p(data: torch.Tensor, p2p, device_status=None, stream=No
 def tsv_goodput_choose_k_sharded(alpha, ctx_len, cap, k_max, policy, target, comm,
                                  draft=(0.0, 0.0, 0.0), pld_cost_ms=0.0, kv_free_slots=-1,
                                  alpha_per_request=None, k_out=None, goodput_out=None, k_per_request=None,
-                                 sums_ws=None, stream=None):
+                                 sums_ws=None, device_status=None, stream=None):
     """Request-sharded ArgMaxGoodput: partial -> all-reduce(sum, int64) -> finalize.  comm: a Comm
-    (ncclAllReduce inside tsv_goodput_choose_k_sharded) or a P2PComm (tsv_goodput_partial ->
-    tsv_allreduce_i64_p2p -> tsv_goodput_finalize)."""
+    (ncclAllReduce inside tsv_goodput_choose_k_sharded) or a P2PComm (the single fused kernel
+    tsv_goodput_choose_k_p2p)."""
     B = ctx_len.numel()
     dev = _dev(ctx_len)
     per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
@@ -694,13 +714,11 @@ def tsv_goodput_choose_k_sharded(alpha, ctx_len, cap, k_max, policy, target, com
         goodput_out = torch.empty(k_max + 1, dtype=torch.float64, device=dev)
     if sums_ws is None:
         sums_ws = torch.empty(gp_sums_len(k_max), dtype=torch.int64, device=dev)
-    if isinstance(comm, P2PComm):
-        _check(_lib.tsv_goodput_partial(_ptr(alpha), 1 if per else 0, _ptr(ctx_len), _ptr(cap), B, int(k_max),
-                                        _ptr(sums_ws), _stream(stream)))
-        tsv_allreduce_i64_p2p(sums_ws, comm, stream=stream)
-        _check(_lib.tsv_goodput_finalize(_ptr(sums_ws), int(k_max), int(policy), LatencyModel(*target),
-                                         LatencyModel(*draft), float(pld_cost_ms), int(kv_free_slots), _ptr(cap), B,
-                                         _ptr(k_out), _ptr(goodput_out), _ptr(k_per_request), _stream(stream)))
+    if isinstance(comm, (P2PComm, P2PLoopbackRank)):  # one kernel: partial -> peer-memory sum -> finalize
+        _check(_lib.tsv_goodput_choose_k_p2p(_ptr(alpha), 1 if per else 0, _ptr(ctx_len), _ptr(cap), B, int(k_max),
+                                             int(policy), LatencyModel(*target), LatencyModel(*draft),
+                                             float(pld_cost_ms), int(kv_free_slots), _ptr(k_out), _ptr(goodput_out),
+                                             _ptr(k_per_request), comm.handle, _ptr(device_status), _stream(stream)))
         return k_out, goodput_out, k_per_request
     _check(_lib.tsv_goodput_choose_k_sharded(_ptr(alpha), 1 if per else 0, _ptr(ctx_len), _ptr(cap), B,
                                              int(k_max), int(policy), LatencyModel(*target),
@@ -711,18 +729,16 @@ def tsv_goodput_choose_k_sharded(alpha, ctx_len, cap, k_max, policy, target, com
 
 
 def tsv_update_acceptance_sharded(alpha, num_accepted, row_offsets, comm, decay=0.9,
-                                  estimator=EST_TESTED, sums_ws=None, stream=None):
-    """Request-sharded global alpha update: partial -> all-reduce(sum, int64) -> finalize (NCCL Comm
-    or P2PComm as in tsv_goodput_choose_k_sharded)."""
+                                  estimator=EST_TESTED, sums_ws=None, device_status=None, stream=None):
+    """Request-sharded global alpha update: partial -> all-reduce(sum, int64) -> finalize (NCCL Comm),
+    or with a P2PComm the single kernel tsv_update_acceptance_p2p."""
     B = num_accepted.numel()
+    if isinstance(comm, (P2PComm, P2PLoopbackRank)):
+        _check(_lib.tsv_update_acceptance_p2p(_ptr(alpha), 0, _ptr(num_accepted), _ptr(row_offsets), B, float(decay),
+                                              int(estimator), comm.handle, _ptr(device_status), _stream(stream)))
+        return alpha
     if sums_ws is None:
         sums_ws = torch.empty(2, dtype=torch.int64, device=_dev(num_accepted))
-    if isinstance(comm, P2PComm):
-        _check(_lib.tsv_update_partial(_ptr(num_accepted), _ptr(row_offsets), B, int(estimator), _ptr(sums_ws),
-                                       _stream(stream)))
-        tsv_allreduce_i64_p2p(sums_ws, comm, stream=stream)
-        _check(_lib.tsv_update_finalize(_ptr(alpha), _ptr(sums_ws), float(decay), _stream(stream)))
-        return alpha
     _check(_lib.tsv_update_acceptance_sharded(_ptr(alpha), _ptr(num_accepted), _ptr(row_offsets), B,
                                               float(decay), int(estimator), _ptr(sums_ws), comm.handle,
                                               _stream(stream)))

@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
     config.addinivalue_line("markers", "slow: long-running statistical or full-size case")
+    config.addinivalue_line("markers", "sanitize: compute-sanitizer run over the concurrency-heavy paths")
 
 
 def pytest_collection_modifyitems(config, items):

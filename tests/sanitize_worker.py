@@ -8,7 +8,8 @@ Paths (VERDICT r01 "next round" item 2; SURVEY.md:257 test layer 4):
           config-3-shaped lookup (L=4096, n 1-4); the fused lookup + choose-k (last-CTA arrival
           counter, int64 atomics)
   p2p     peer-memory vocab sharding, G=2 loopback ranks over 3 epochs (LL words, epoch parity),
-          and the p2p int64 all-reduce on two concurrent streams
+          and (one rank) the fused request-sharded choose-k / verify+update exchanges and the int64
+          all-reduce (the sanitizer serialises kernels: no concurrent loopback ranks)
   shard   lazy (flags / race / emit) and dense (partial / combine) vocab sharding in loopback
   greedy  greedy verify (row-slot clear kernel + red.max argmax + emit)
   logits  fused softmax-from-logits verify (statistics pass, logits scan, LOGITS race)
@@ -116,23 +117,39 @@ def path_p2p():
                 assert (_np(na) == ona).all() and (_np(out) == oout).all() and int(stt.item()) == ost
     finally:
         lb.close()
-    # p2p int64 all-reduce, two loopback ranks on two concurrent streams
-    lb = tsv.P2PLoopback(2, 8)
+    # request-sharded global sums over peer memory, one rank (the sanitizer serialises kernels, so a
+    # kernel that pushes and then polls cannot wait for a second loopback rank's kernel): the fused
+    # choose-k, the standalone int64 all-reduce and the update CTA of the verify, 3 calls each
+    comm = tsv.P2PComm(0, 1, B_max=16)
     try:
-        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        ctx_len = torch.tensor(np.full(vb.B, 700, np.int32), device=DEV)
+        cap = torch.tensor(np.arange(vb.B) % 6, dtype=torch.int32, device=DEV)
+        stt = torch.zeros(1, dtype=torch.int32, device=DEV)
         for call in range(3):
-            vals = np.arange(2 * 12, dtype=np.int64).reshape(2, 12) * (call + 3) - 50
-            data = [torch.tensor(vals[r], device=DEV) for r in range(2)]
-            stt = torch.zeros(1, dtype=torch.int32, device=DEV)
+            alpha = torch.tensor([0.3 + 0.2 * call], dtype=torch.float64, device=DEV)
+            k, gp, _ = tsv.tsv_goodput_choose_k_sharded(alpha, ctx_len, cap, 5, tsv.POLICY_PLD, synth.SPEC_DESK_TARGET,
+                                                        comm, synth.SPEC_DESK_DRAFT, 0.05, device_status=stt)
+            data = torch.arange(12, dtype=torch.int64, device=DEV) * (call + 3) - 50
+            want = _np(data)
+            tsv.tsv_allreduce_i64_p2p(data, comm, device_status=stt)
+            na = torch.empty(vb.B, dtype=torch.int32, device=DEV)
+            out = torch.empty((vb.B, vb.k_max + 1), dtype=torch.int32, device=DEV)
+            a = tsv.make_verify_args(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, 21, call, vb.k_max, na,
+                                     out, device_status=stt)
+            ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+            a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+            a2 = torch.tensor([0.7], dtype=torch.float64, device=DEV)
+            tsv.tsv_verify_accept_update_p2p(a, a2, comm, 0.9)
             torch.cuda.synchronize()
-            for r in range(2):
-                tsv._check(tsv.lib().tsv_allreduce_i64_p2p(data[r].data_ptr(), 12, lb.handles[r], stt.data_ptr(),
-                                                           streams[r].cuda_stream))
-            torch.cuda.synchronize()
-            for r in range(2):
-                assert (_np(data[r]) == vals.sum(0)).all() and int(stt.item()) == 0
+            ok, og = oracle.choose_k(0.3 + 0.2 * call, _np(ctx_len), _np(cap), 5, oracle.POLICY_PLD,
+                                     synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT, pld_cost_ms=0.05)
+            ona, oout, _ = _oracle_verify(vb, 21, call)
+            assert int(k.item()) == ok and (_np(gp).view(np.uint64) == og.view(np.uint64)).all()
+            assert (_np(data) == want).all() and int(stt.item()) == 0
+            assert (_np(na) == ona).all() and (_np(out) == oout).all()
+            assert float(a2.item()) == oracle.update(0.7, ona, _np(vb.row_offsets), decay=0.9)
     finally:
-        lb.close()
+        comm.close()
 
 
 def path_shard():

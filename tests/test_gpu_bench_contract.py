@@ -32,3 +32,13 @@ def test_bench_json_line_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "workload" in d["config"] and "l2_defeat" in d["config"]
+    # every other workload as a sub-object, each timed with its own roofline, clocks and device status
+    w = d["workloads"]
+    for name in ("config4", "config4_sharded_p2p", "greedy", "logits", "config5", "loop"):
+        sub = w[name]
+        assert "error" not in sub, (name, sub)
+        assert sub["value"] > 0 and sub["ms_per_step"] > 0, name
+        assert sub["roofline"]["peak"] > 0 and 0 < sub["roofline"]["frac"] < 1.5, name
+        assert "sm_mhz" in sub["clocks"], name
+        assert sub["device_status"] in (0, None), name
+    assert w["config4"]["config"]["vocab"] == 128256

@@ -1,0 +1,28 @@
+"""compute-sanitizer over every concurrency-heavy path (tests/sanitize_worker.py, each path checked
+against the oracle): memcheck, racecheck, synccheck and initcheck must report 0 errors.  Only
+libtsv's kernels are instrumented (--kernel-name kns=tsv), except by initcheck (all kernels).  SURVEY.md:257 test layer 4; the
+logs of the committed run are under profiles/r02/sanitizer/."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.sanitize]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CS = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_sanitizer_clean(tool):
+    extra = {"racecheck": ["--racecheck-report", "all"], "memcheck": ["--check-device-heap", "yes"]}.get(tool, [])
+    # initcheck instruments every kernel: with a kernel filter, memory written by torch's kernels would
+    # look uninitialised to the host copies that read it back
+    filt = [] if tool == "initcheck" else ["--kernel-name", "kns=tsv"]
+    cmd = [CS, "--tool", tool] + extra + filt + ["--print-limit", "50", "--error-exitcode", "99",
+                                                 sys.executable, os.path.join(ROOT, "tests", "sanitize_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count("SANITIZE-OK") == 6, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
