@@ -48,7 +48,12 @@ class StepInputs:
 
     @property
     def B(self) -> int:
-        return int(self.verify[0].row_offsets.numel()) - 1
+        """Largest batch over the rotation sets (buffer sizing; a strong-scaling rank's share of the
+        batch can differ per set)."""
+        return max(self.B_of(s) for s in range(self.sets))
+
+    def B_of(self, s: int) -> int:
+        return int(self.verify[s].row_offsets.numel()) - 1
 
     @property
     def sets(self) -> int:
@@ -125,7 +130,7 @@ class SpecStep:
 
     def _choose_k(self, s, st):
         inp, L = self.inp, tsv.lib()
-        args = (self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(), self.proposal_len.data_ptr(), inp.B,
+        args = (self.alpha.data_ptr(), 0, inp.ctx_len[s].data_ptr(), self.proposal_len.data_ptr(), inp.B_of(s),
                 inp.k_fixed, tsv.POLICY_PLD, tsv.LatencyModel(*inp.target), tsv.LatencyModel(*inp.draft),
                 float(inp.pld_cost_ms), int(inp.kv_free_slots), self.k_star.data_ptr(), self.goodput.data_ptr(),
                 self.k_req.data_ptr())
@@ -146,7 +151,7 @@ class SpecStep:
         else:
             tsv._check(L.tsv_verify_accept(tsv.ctypes.byref(a), st))
             tsv._check(L.tsv_update_acceptance_sharded(self.alpha.data_ptr(), self.num_accepted.data_ptr(),
-                                                       self.inp.verify[s].row_offsets.data_ptr(), self.inp.B, 0.9,
+                                                       self.inp.verify[s].row_offsets.data_ptr(), self.inp.B_of(s), 0.9,
                                                        tsv.EST_TESTED, self.upd_ws.data_ptr(), self.comm.handle, st))
 
     def run(self, step: int, stream=None):
@@ -157,7 +162,7 @@ class SpecStep:
         L = tsv.lib()
         if self.fused:
             tsv._check(L.tsv_propose_lookup_choose_k(
-                inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B, inp.n_min, inp.n_max, inp.k_fixed,
+                inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s), inp.n_min, inp.n_max, inp.k_fixed,
                 self.proposals.data_ptr(), self.proposal_len.data_ptr(), self.alpha.data_ptr(), 0,
                 inp.ctx_len[s].data_ptr(), tsv.LatencyModel(*inp.target), float(inp.pld_cost_ms),
                 int(inp.kv_free_slots), self.k_star.data_ptr(), self.goodput.data_ptr(), self.k_req.data_ptr(),
@@ -167,7 +172,7 @@ class SpecStep:
             tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
                                                   tsv.EST_TESTED, st))
             return
-        tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
+        tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
                                         inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
                                         self.proposal_len.data_ptr(), self.status.data_ptr(), st))
         self._choose_k(s, st)
@@ -182,7 +187,7 @@ class SpecStep:
         st = tsv._stream(stream)
         L = tsv.lib()
         if name == "lookup":
-            tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B,
+            tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
                                             inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
                                             self.proposal_len.data_ptr(), self.status.data_ptr(), st))
         elif name == "choose_k":
@@ -197,7 +202,7 @@ class SpecStep:
             self._verify_update(a, s, st)
         elif name == "update":
             tsv._check(L.tsv_update_acceptance(self.alpha.data_ptr(), 0, self.num_accepted.data_ptr(),
-                                               inp.verify[s].row_offsets.data_ptr(), inp.B, 0.9,
+                                               inp.verify[s].row_offsets.data_ptr(), inp.B_of(s), 0.9,
                                                tsv.EST_TESTED, st))
         else:
             raise ValueError(name)
