@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
+    ap.add_argument("--no-lookup-ready", action="store_true",
+                    help="launch the lookup without TSV_LOOKUP_INPUTS_READY (its loads wait for the preceding kernel)")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
     ap.add_argument("--comm", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 exchange of the request-sharded global sums: NVLink peer memory inside the goodput "
@@ -314,7 +316,7 @@ def step_tokens(st, inp, ks, step_ids, dev, workspace_from=None):
         vb = inp.verify[t % R]
         tsv.tsv_verify_accept(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, inp.seed, t,
                               K_MAX, num_accepted=na, out_tokens=outt, workspace=st.workspace)
-        m = na.cpu().numpy()
+        m = na[:inp.B_of(t % R)].cpu().numpy()
         per_step_tokens[t] = int((m + 1).sum())
         per_step_vbytes[t] = verify_alg_bytes(m, ks[t % R], True, V, K_MAX)
     return per_step_tokens, per_step_vbytes
@@ -358,7 +360,8 @@ def run_ours(args, rank, world, local_rank):
     R = inp.sets
     vbs = inp.verify
     comm = make_comm(args, rank, world, B)
-    st = SpecStep(inp, device=dev, chunk=args.chunk, fused=args.fused and comm is None, comm=comm)
+    st = SpecStep(inp, device=dev, chunk=args.chunk, fused=args.fused and comm is None, comm=comm,
+                  lookup_ready=not args.no_lookup_ready)
     footprint = sum(inp.input_bytes(s) for s in range(R))
     tm = time_step_graphs(args, st, world, local_rank, dev)
     t_max, W, K, gl, stream = tm["t_max"], tm["W"], tm["K"], tm["gl"], tm["stream"]
@@ -486,7 +489,7 @@ def run_ours(args, rank, world, local_rank):
         ne = args.e2e_steps
         hv = synth.VerifyBatch(host[0], host[1], host[2], host[3], host[4], vb.k, V, K_MAX)
         st_h = SpecStep(StepInputs([hv], [hctx[0]], [hctx[1]], [hctx[2]], K_MAX, seed=seed), device=dev,
-                        chunk=args.chunk, comm=comm)
+                        chunk=args.chunk, comm=comm, lookup_ready=not args.no_lookup_ready)
         k_np = ks[0]
         ctx_bytes = hctx[0].numel() * 4 + hctx[1].numel() * 4 + hctx[2].numel() * 4
 
@@ -548,7 +551,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": WORKLOAD, "global_batch": B * world, "vocab": V, "k_max": K_MAX,
                    "ctx_len": L_CTX, "parallelism": par,
                    "l2_defeat": f"{R} rotating input sets, footprint {footprint / 1e6:.0f} MB vs L2 {l2 / 1e6:.0f} MB",
-                   "graph_steps": gl, "fused": bool(args.fused and comm is None)},
+                   "graph_steps": gl, "fused": bool(args.fused and comm is None),
+                   "lookup_inputs_ready": not args.no_lookup_ready},
         "roofline": {"kernel": "verify_race_kernel (the dominant kernel: streams every algorithmic byte of the verify call)",
                      "bound": "hbm", "achieved": race_achieved, "peak": peak,
                      "unit": "GB/s", "frac": race_achieved / peak, "traffic": traffic,
@@ -599,7 +603,7 @@ def run_strong(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     inp, ks, l2 = build_step_inputs("strong", rank, world, dev, args, B)
     comm = make_comm(args, rank, world, B)
-    st = SpecStep(inp, device=dev, chunk=args.chunk, comm=comm)
+    st = SpecStep(inp, device=dev, chunk=args.chunk, comm=comm, lookup_ready=not args.no_lookup_ready)
     tm = time_step_graphs(args, st, world, local_rank, dev)
     consistent = global_state_consistent(st, world, dev)
     per_step_tokens, per_step_vbytes = step_tokens(st, inp, ks, tm["step_ids"], dev)

@@ -113,6 +113,24 @@ TSV_API tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_off
                               int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
                               void* stream);
 
+/* tsv_propose_lookup with flags (tsv_propose_lookup == flags 0).
+ *   TSV_LOOKUP_INPUTS_READY  Contract (as TSV_VERIFY_META_READY): ctx and
+ *     ctx_offsets are COMPLETE before the kernel that immediately precedes
+ *     this call on the stream could start -- no kernel still in flight when
+ *     the lookup launches writes them (e.g. the context buffer is prepared by
+ *     the host / a copy before the step, as a serving engine's input
+ *     preparation does; NOT when the previous step's emit appends to it on the
+ *     device).  The search (loads, compares, reduction, token gather) then runs
+ *     before the grid-dependency wait, overlapping the preceding kernel; only
+ *     the stores of proposals / proposal_len / device_status wait.  Outputs are
+ *     identical to flags 0.
+ * Errors: as tsv_propose_lookup; INVALID_ARG for unknown flags. */
+#define TSV_LOOKUP_INPUTS_READY 1
+TSV_API tsv_status tsv_propose_lookup_ex(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                                 int32_t n_min, int32_t n_max, int32_t k_fixed,
+                                 int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
+                                 int32_t flags, void* stream);
+
 /* --------------------------------------------------------------------------
  * Verify / accept.  PAPER.md:18 [AD] "we utilize rejection sampling to
  * determine which tokens are retained ... (2) a bonus token that either

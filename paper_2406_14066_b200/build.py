@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(OUT_DIR, "libtsv.so")
 SOURCES = ["api.cu", "verify.cu", "lookup.cu", "goodput.cu", "loop.cu"]
-HEADERS = ["common.cuh", "goodput.cuh"]
+HEADERS = ["common.cuh", "goodput.cuh", "p2p.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -163,14 +163,22 @@ __device__ __forceinline__ void fused_choose_k(const ChooseArgs& A, FusedScratch
 
 // FUSED: the CTA that finishes last also runs ArgMaxGoodput (PLD policy, cap_i = the
 // proposal lengths just written) -- GetVerificationLen right after Propose (Listing 1).
-template <bool FUSED>
+//
+// READY (TSV_LOOKUP_INPUTS_READY, tsv_propose_lookup_ex): ctx and ctx_offsets were complete before the
+// preceding kernel on the stream could start, so the whole search -- loads, compares, the block
+// reduction and the gather of the proposed tokens -- runs before the grid-dependency wait, while the
+// preceding kernel drains; only the stores of proposals / proposal_len / device_status wait.  The
+// kernel still triggers its dependents only after its own wait (the PDL chain invariant, tsv.h).
+template <bool FUSED, bool READY = false>
 __global__ void __launch_bounds__(kLookupThreads)
     ngram_lookup_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ ctx_offsets, int32_t B,
                         int32_t n_min, int32_t n_max, int32_t K, int32_t* __restrict__ proposals,
                         int32_t* __restrict__ proposal_len, ChooseArgs ca, uint32_t* counter, int32_t* devstatus) {
     __shared__ uint32_t s_red[kLookupThreads / 32];
-    pdl_wait();
-    pdl_launch_dependents();
+    if (!READY) {
+        pdl_wait();
+        pdl_launch_dependents();
+    }
     const int32_t i = blockIdx.x;
     const int tid = threadIdx.x;
     const int32_t off = __ldg(ctx_offsets + i);
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(kLookupThreads)
     const int64_t L64 = static_cast<int64_t>(end) - off;
     const bool bad_ctx = off < 0 || L64 < 0 || L64 > TSV_MAX_CONTEXT;
     const int32_t L = bad_ctx ? 0 : static_cast<int32_t>(L64);
-    if (bad_ctx && tid == 0 && devstatus) atomicOr(reinterpret_cast<unsigned int*>(devstatus), TSV_DEVSTATUS_BAD_CONTEXT);
+    if (!READY && bad_ctx && tid == 0 && devstatus) atomicOr(reinterpret_cast<unsigned int*>(devstatus), TSV_DEVSTATUS_BAD_CONTEXT);
     const int32_t* c = ctx + off;
     int32_t my_len = 0;  // this request's proposal length (warp 0)
     uint32_t best = 0;
@@ -225,8 +233,19 @@ __global__ void __launch_bounds__(kLookupThreads)
         if (L >= 2 && n_star >= n_min) len = min(K, L - 1 - e_star);
         my_len = len;
         int32_t* out = proposals + static_cast<int64_t>(i) * K;
-        for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? __ldg(c + e_star + 1 + t) : -1;
-        if (tid == 0) proposal_len[i] = len;
+        if (READY) {  // K <= TSV_MAX_K < 32: lane t holds proposed token t; then wait, then store
+            const int32_t tok = (tid < K && tid < len) ? __ldg(c + e_star + 1 + tid) : -1;
+            pdl_wait();
+            pdl_launch_dependents();
+            if (tid < K) out[tid] = tok;
+            if (tid == 0) {
+                proposal_len[i] = len;
+                if (bad_ctx && devstatus) atomicOr(reinterpret_cast<unsigned int*>(devstatus), TSV_DEVSTATUS_BAD_CONTEXT);
+            }
+        } else {
+            for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? __ldg(c + e_star + 1 + t) : -1;
+            if (tid == 0) proposal_len[i] = len;
+        }
     }
     if (FUSED) fused_choose_k(ca, reinterpret_cast<FusedScratch*>(counter), i, my_len);
 }
@@ -239,6 +258,15 @@ extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_
                                          int32_t n_min, int32_t n_max, int32_t k_fixed,
                                          int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
                                          void* stream) {
+    return tsv_propose_lookup_ex(ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, device_status,
+                                 0, stream);
+}
+
+extern "C" tsv_status tsv_propose_lookup_ex(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                                            int32_t n_min, int32_t n_max, int32_t k_fixed,
+                                            int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
+                                            int32_t flags, void* stream) {
+    TSV_REQUIRE((flags & ~TSV_LOOKUP_INPUTS_READY) == 0, "tsv_propose_lookup: unknown flags 0x%x", flags);
     TSV_REQUIRE(B >= 0, "tsv_propose_lookup: B < 0 (%d)", B);
     TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
                 "tsv_propose_lookup: need 1 <= n_min (%d) <= n_max (%d) <= %d", n_min, n_max, TSV_MAX_NGRAM);
@@ -247,7 +275,8 @@ extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_
     TSV_REQUIRE(ctx && ctx_offsets && proposals && proposal_len, "tsv_propose_lookup: a required array is NULL");
     TSV_TRY(check_device());
     ChooseArgs none = {};
-    TSV_CUDA(launch_pdl(ngram_lookup_kernel<false>, dim3(B), dim3(kLookupThreads), 0,
+    auto kern = (flags & TSV_LOOKUP_INPUTS_READY) ? ngram_lookup_kernel<false, true> : ngram_lookup_kernel<false, false>;
+    TSV_CUDA(launch_pdl(kern, dim3(B), dim3(kLookupThreads), 0,
                         static_cast<cudaStream_t>(stream), ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals,
                         proposal_len, none, static_cast<uint32_t*>(nullptr), device_status),
              "ngram_lookup_kernel launch");

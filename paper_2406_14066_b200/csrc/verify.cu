@@ -565,7 +565,10 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
 #endif
         }
         const uint64_t best = warp_max_u64(R.best);
-        if (lane == 0 && best) atomicMax(P.rowkey + key_row, static_cast<unsigned long long>(best));
+        // lazy: the key row (= request i) is recomputed from the item index here rather than kept live
+        // across the streaming loop (which spilled it to the stack at 64 registers)
+        const int32_t key_row_end = (MODE == kLazy && !LOGITS) ? item - (item / P.B) * P.B : key_row;
+        if (lane == 0 && best) atomicMax(P.rowkey + key_row_end, static_cast<unsigned long long>(best));
 #if TSV_TRACE
         if (lane == 0 && item < kTraceMax) {
             g_trace[item][0] = tr0;

@@ -86,8 +86,12 @@ class SpecStep:
     k*, every k_i, every emitted token and alpha equal one device holding the whole batch."""
 
     def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0, fused: bool = False,
-                 comm=None):
+                 comm=None, lookup_ready: bool = True):
         self.inp = inp
+        # the contexts are inputs of the step that no kernel of the step writes (prepared before the step,
+        # like a serving engine's input buffers): TSV_LOOKUP_INPUTS_READY lets the lookup search them
+        # while the previous step's last kernel drains (include/tsv.h states the contract)
+        self.lookup_flags = tsv.LOOKUP_INPUTS_READY if lookup_ready else 0
         B, K = inp.B, inp.k_max
         dev = torch.device(device)
         self.alpha = torch.full((1,), alpha0, dtype=torch.float64, device=dev)
@@ -172,9 +176,9 @@ class SpecStep:
             tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
                                                   tsv.EST_TESTED, st))
             return
-        tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
-                                        inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
-                                        self.proposal_len.data_ptr(), self.status.data_ptr(), st))
+        tsv._check(L.tsv_propose_lookup_ex(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
+                                           inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
+                                           self.proposal_len.data_ptr(), self.status.data_ptr(), self.lookup_flags, st))
         self._choose_k(s, st)
         a = self.args[s]
         a.step = step & 0xFFFFFFFF
@@ -187,9 +191,10 @@ class SpecStep:
         st = tsv._stream(stream)
         L = tsv.lib()
         if name == "lookup":
-            tsv._check(L.tsv_propose_lookup(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
-                                            inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
-                                            self.proposal_len.data_ptr(), self.status.data_ptr(), st))
+            tsv._check(L.tsv_propose_lookup_ex(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
+                                               inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
+                                               self.proposal_len.data_ptr(), self.status.data_ptr(), self.lookup_flags,
+                                               st))
         elif name == "choose_k":
             self._choose_k(s, st)
         elif name == "verify":

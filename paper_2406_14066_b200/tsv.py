@@ -29,6 +29,7 @@ VERIFY_NO_PRUNE = 1
 VERIFY_SHARD_DENSE = 2
 VERIFY_RACE_ONLY = 4  # measurement: the race kernel alone over a previous call's workspace
 VERIFY_META_READY = 8  # row_offsets/drafts/request_ids not written by the preceding kernel on the stream
+LOOKUP_INPUTS_READY = 1  # tsv_propose_lookup_ex: ctx/ctx_offsets not written by any kernel in flight
 LOOKUP_CHOOSE_SCRATCH = 512  # TSV_LOOKUP_CHOOSE_SCRATCH
 POLICY_DRAFT = 0
 POLICY_PLD = 1
@@ -51,6 +52,7 @@ EXPORTED = [
     "tsv_p2p_buffer_size", "tsv_p2p_alloc", "tsv_p2p_free", "tsv_p2p_open", "tsv_p2p_close", "tsv_p2p_init",
     "tsv_p2p_destroy", "tsv_verify_accept_sharded_p2p", "tsv_verify_shard_p2p_phase", "tsv_allreduce_i64_p2p",
     "tsv_goodput_choose_k_p2p", "tsv_update_acceptance_p2p", "tsv_verify_accept_update_p2p",
+    "tsv_propose_lookup_ex",
 ]
 
 
@@ -100,6 +102,7 @@ def _load() -> ctypes.CDLL:
         "tsv_last_error": ([], ctypes.c_char_p),
         "tsv_abi_version": ([], ctypes.c_int),
         "tsv_propose_lookup": ([P, P, i32, i32, i32, i32, P, P, P, P], ctypes.c_int),
+        "tsv_propose_lookup_ex": ([P, P, i32, i32, i32, i32, P, P, P, i32, P], ctypes.c_int),
         "tsv_verify_workspace_size": ([ctypes.POINTER(VerifyArgs), ctypes.POINTER(sz)], ctypes.c_int),
         "tsv_workspace_clear": ([P, sz, P], ctypes.c_int),
         "tsv_verify_accept": ([ctypes.POINTER(VerifyArgs), P], ctypes.c_int),
@@ -216,8 +219,10 @@ def tsv_abi_version() -> int:
 # ----------------------------------------------------------------------------- lookup
 def tsv_propose_lookup(ctx: torch.Tensor, ctx_offsets: torch.Tensor, n_min: int, n_max: int,
                        k_fixed: int, proposals: Optional[torch.Tensor] = None,
-                       proposal_len: Optional[torch.Tensor] = None, device_status=None, stream=None):
-    """Prompt-lookup proposal.  Returns (proposals[B, k], proposal_len[B])."""
+                       proposal_len: Optional[torch.Tensor] = None, device_status=None, stream=None,
+                       flags: int = 0):
+    """Prompt-lookup proposal.  Returns (proposals[B, k], proposal_len[B]).
+    flags: LOOKUP_INPUTS_READY (tsv_propose_lookup_ex; include/tsv.h states the contract)."""
     B = ctx_offsets.numel() - 1
     _want(ctx, torch.int32, None, "ctx")
     _want(ctx_offsets, torch.int32, None, "ctx_offsets")
@@ -227,8 +232,9 @@ def tsv_propose_lookup(ctx: torch.Tensor, ctx_offsets: torch.Tensor, n_min: int,
     if proposal_len is None:
         proposal_len = torch.empty(B, dtype=torch.int32, device=dev)
     ctx_p = _ptr(ctx) if ctx.numel() else _ptr(ctx_offsets)  # any valid pointer when empty
-    _check(_lib.tsv_propose_lookup(ctx_p, _ptr(ctx_offsets), B, n_min, n_max, k_fixed,
-                                   _ptr(proposals), _ptr(proposal_len), _ptr(device_status), _stream(stream)))
+    _check(_lib.tsv_propose_lookup_ex(ctx_p, _ptr(ctx_offsets), B, n_min, n_max, k_fixed,
+                                      _ptr(proposals), _ptr(proposal_len), _ptr(device_status), int(flags),
+                                      _stream(stream)))
     return proposals, proposal_len
 
 

@@ -41,6 +41,7 @@ def test_bench_two_ranks_shared_gpu_json_line():
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["device_status"] == 0
     assert d["config"]["global_batch"] == 512 and "p2p" in d["config"]["parallelism"]
     s = d["workloads"]["strong"]
+    assert "error" not in s, s
     assert s["scaling"] == "strong" and s["config"]["global_batch"] == 256 and s["value"] > 0 and s["device_status"] == 0
     c4 = d["workloads"]["config4"]
     assert c4["n_gpus"] == 2 and c4["config"]["vocab"] == 128256 and c4["value"] > 0 and c4["device_status"] == 0

@@ -114,7 +114,7 @@ def test_step_counts_sharded_flavours(tsv):
                                      vocab_global=4096, step_counts=c_)
             ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
             a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
-            args.append((a, ws, n_))
+            args.append((a, ws, n_, o_))  # keep every output buffer alive while the kernels write it
             scs.append(c_)
         for ph in range(3):
             for s in range(G):

@@ -5,6 +5,8 @@ proposal lengths, k*), bit-exact on the goodput values and the updated alpha
 (same binary64 operation sequence on both sides).  Inputs come
 from synth/ (seeded); expected values come only from oracle/.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -493,6 +495,60 @@ def assert_lookup_parity(tsv, ctx, offs, n_min, n_max, K):
     return opl
 
 
+def test_lookup_inputs_ready_flag_in_pdl_chain(tsv):
+    # TSV_LOOKUP_INPUTS_READY: the search runs before the grid-dependency wait.  Inside a captured graph,
+    # right after a verify call (three PDL kernels) and followed by choose-k, the proposals must equal
+    # the oracle's, on ragged contexts (short, empty, misaligned starts) and on config-3 contexts.
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=5).to(DEV)
+    na = torch.empty(64, dtype=torch.int32, device=DEV)
+    out = torch.empty((64, 9), dtype=torch.int32, device=DEV)
+    a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 7, 0, 8, na, out)
+    ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+    a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    for (B, L, ragged, seed) in ((37, 700, True, 3), (256, 4096, False, 11)):
+        ctx, offs = synth.make_contexts(B=B, L=L, seed=seed, ragged=ragged)
+        opr, opl = oracle.lookup(ctx, offs, 1, 4, 5)
+        c, o = torch.tensor(ctx, device=DEV), torch.tensor(offs, device=DEV)
+        cl = torch.tensor(np.diff(offs).astype(np.int32), device=DEV)
+        pr = torch.full((B, 5), -7, dtype=torch.int32, device=DEV)
+        pl = torch.full((B,), -7, dtype=torch.int32, device=DEV)
+        alpha = torch.full((1,), 0.7, dtype=torch.float64, device=DEV)
+        st = torch.zeros(1, dtype=torch.int32, device=DEV)
+        for mode in ("eager", "graph"):
+            pr.fill_(-7)
+            pl.fill_(-7)
+            g = torch.cuda.CUDAGraph() if mode == "graph" else None
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                ctxm = torch.cuda.graph(g, stream=side) if g is not None else torch.cuda.stream(side)
+                with ctxm:
+                    for rep in range(2):
+                        tsv._check(tsv.lib().tsv_verify_accept(tsv.ctypes.byref(a), tsv._stream(None)))
+                        tsv.tsv_propose_lookup(c, o, 1, 4, 5, proposals=pr, proposal_len=pl, device_status=st,
+                                               flags=tsv.LOOKUP_INPUTS_READY)
+                        tsv.tsv_goodput_choose_k(alpha, cl, pl, 5, tsv.POLICY_PLD, synth.SPEC_DESK_TARGET,
+                                                 synth.SPEC_DESK_DRAFT, 0.05)
+            torch.cuda.current_stream().wait_stream(side)
+            if g is not None:
+                pr.fill_(-7)
+                pl.fill_(-7)
+                g.replay()
+            torch.cuda.synchronize()
+            assert (_np(pl) == opl).all() and (_np(pr) == opr).all(), mode
+            assert int(st.item()) == 0
+
+
+def test_lookup_inputs_ready_bad_context_status(tsv):
+    # the deferred status store: decreasing offsets still flag BAD_CONTEXT with the flag set
+    ctx = torch.arange(64, dtype=torch.int32, device=DEV) % 7
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    pr, pl = tsv.tsv_propose_lookup(ctx, torch.tensor([0, 40, 20, 64], dtype=torch.int32, device=DEV), 1, 3, 4,
+                                    device_status=st, flags=tsv.LOOKUP_INPUTS_READY)
+    torch.cuda.synchronize()
+    assert int(st.item()) == tsv.DEVSTATUS_BAD_CONTEXT and int(pl[1].item()) == 0 and (_np(pr)[1] == -1).all()
+
+
 def test_lookup_config1(tsv):
     ctx, offs = synth.make_contexts(B=4, L=512, seed=1)
     plen = assert_lookup_parity(tsv, ctx, offs, 3, 3, 5)
@@ -800,6 +856,24 @@ def test_step_graph_capture_matches_eager(tsv, fused):
         assert torch.equal(v, eager[k]), k
 
 
+def test_step_lookup_ready_multi_step_graph_matches_eager(tsv):
+    # three consecutive steps in one graph with TSV_LOOKUP_INPUTS_READY (the lookup of step t+1 searches
+    # while step t's emit drains) equal three eager steps without the flag (alpha carried across steps)
+    from paper_2406_14066_b200.step import SpecStep
+    inp = synth.make_step_inputs(B=96, V=32000, L=2048, k_max=8, seed=21, device=DEV, sets=2)
+    st = SpecStep(inp, lookup_ready=False)
+    for t in range(3):
+        st.run(step=t)
+    torch.cuda.synchronize()
+    eager = {k: v.clone() for k, v in st.outputs().items()}
+    st2 = SpecStep(inp, lookup_ready=True)
+    st2.capture(steps=[0, 1, 2])
+    st2.replay()
+    torch.cuda.synchronize()
+    for k, v in st2.outputs().items():
+        assert torch.equal(v, eager[k]), k
+
+
 # ------------------------------------------------------------------- greedy verify (NEXT 2)
 def assert_greedy_parity(tsv, p, ro, drafts, k_max, vocab=None, chunk=0):
     ona, oout, ost = oracle.verify_greedy(p, ro, drafts, k_max, vocab=vocab)
@@ -953,10 +1027,43 @@ def test_verify_logits_parity(tsv, B, V, k_max, tau, dense_q):
     torch.cuda.synchronize()
     gna, gout = _np(gna), _np(gout)
     flips = near_tie_flips(vb, p, q, ona, oout, gna, gout, seed, step)
-    for f in flips:  # every flip is listed; each must be a near tie
-        print("near-tie flip:", f)
+    record_flips(dict(B=B, V=V, k_max=k_max, tau=tau, dense_q=dense_q, seed=seed, step=step), flips)
     assert all(reason is not None for _, reason in flips), flips
     assert len(flips) <= max(1, B // 64)
+
+
+def record_flips(case, flips):
+    """Every near-tie flip is listed (north_star): printed, and appended as one JSON line per case to
+    gpurun_out/logits_flips.jsonl (the GPU run's artifact; the committed copy is under profiles/)."""
+    import json
+    for f in flips:
+        print("near-tie flip:", case, f)
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, "logits_flips.jsonl"), "a") as fh:
+        fh.write(json.dumps({"case": case, "requests": case["B"], "flips": [{"request": i, "near_tie": r}
+                                                                              for i, r in flips]}) + "\n")
+
+
+@pytest.mark.slow
+def test_verify_logits_parity_bench_size(tsv):
+    # the bench's logits workload (B = 256, V = 32000, k in 0..8, tau = 1) at two Philox steps: every token
+    # equal to the oracle's verify on the oracle's probabilities, or a listed near tie
+    vb = synth.make_logits_batch(B=256, V=32000, k_max=8, lam=0.7, seed=240614066, dense_q=True)
+    zp, zq = _np(vb.p), _np(vb.q)
+    p, q = oracle.softmax_rows(zp, 1.0, vocab=32000), oracle.softmax_rows(zq, 1.0, vocab=32000)
+    g = vb.to(DEV)
+    for step in (0, 1):
+        ona, oout, _ = oracle.verify(p, q, _np(vb.row_offsets), _np(vb.draft_tokens),
+                                     _np(vb.request_ids).view(np.uint32), 240614066, step, 8, vocab=32000)
+        gna, gout = tsv.tsv_verify_accept_logits(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, 240614066,
+                                                 step, 8, temperature=1.0, vocab=32000)
+        torch.cuda.synchronize()
+        gna, gout = _np(gna), _np(gout)
+        flips = near_tie_flips(vb, p, q, ona, oout, gna, gout, 240614066, step)
+        record_flips(dict(B=256, V=32000, k_max=8, tau=1.0, dense_q=True, seed=240614066, step=step), flips)
+        assert all(reason is not None for _, reason in flips), flips
+        assert len(flips) <= 4
 
 
 def test_verify_logits_prune_off_identical(tsv):
