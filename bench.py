@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
     ap.add_argument("--no-lookup-ready", action="store_true",
                     help="launch the lookup without TSV_LOOKUP_INPUTS_READY (its loads wait for the preceding kernel)")
+    ap.add_argument("--nvtx", action="store_true",
+                    help="NVTX ranges: TSV_NVTX=1 (every libtsv entry point) plus one range per bench phase / workload")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
     ap.add_argument("--comm", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 exchange of the request-sharded global sums: NVLink peer memory inside the goodput "
@@ -172,8 +174,9 @@ class ClockSampler:
                 pass
             time.sleep(0.0005)
 
-    def __enter__(self):
+    def __enter__(self):  # re-entrant: samples of every `with` block accumulate
         if self.ok:
+            self._stop.clear()
             self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         return self
@@ -260,9 +263,10 @@ def time_step_graphs(args, st, world, local_rank, dev):
         st.capture(list(range(gl, gl + rem)))
         rem_graph = st.graph
     st.reset_state()
-    for _ in range((W + gl - 1) // gl):
-        main_graph.replay()
-    torch.cuda.synchronize()
+    with nvtx_range(args, "warmup"):
+        for _ in range((W + gl - 1) // gl):
+            main_graph.replay()
+        torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -273,7 +277,7 @@ def time_step_graphs(args, st, world, local_rank, dev):
     sampler = ClockSampler(_dev_index(local_rank))
     barrier()
     torch.cuda.synchronize()
-    with sampler:
+    with sampler, nvtx_range(args, "timed"):
         e0.record(stream)
         for _ in range(K // gl):
             main_graph.replay()
@@ -283,22 +287,27 @@ def time_step_graphs(args, st, world, local_rank, dev):
         torch.cuda.synchronize()
     barrier()
     t_max = pdist.max_over_ranks(e0.elapsed_time(e1), dev)
-    # spread: a second pass with an event around every graph replay (kept out of the timed region)
-    n_rep = max(1, min(K // gl, 64))
+    n_timed_samples = len(sampler.samples)
+    # spread: a second pass with an event around every graph replay (kept out of the timed region;
+    # 64 replays whatever K, so a short driver run still gets p10/p90), clocks sampled again
+    n_rep = 64
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(n_rep + 1)]
     barrier()
-    evs[0].record(stream)
-    for r in range(n_rep):
-        main_graph.replay()
-        evs[r + 1].record(stream)
-    torch.cuda.synchronize()
+    with sampler, nvtx_range(args, "spread"):
+        evs[0].record(stream)
+        for r in range(n_rep):
+            main_graph.replay()
+            evs[r + 1].record(stream)
+        torch.cuda.synchronize()
     per_step = sorted(evs[r].elapsed_time(evs[r + 1]) / gl for r in range(n_rep))
     spread = {f"p{q}": per_step[min(n_rep - 1, int(q / 100 * n_rep))] for q in (10, 50, 90)}
     spread["replays"] = n_rep
     spread["steps_per_replay"] = gl
     step_ids = [t for _ in range(K // gl) for t in range(gl)] + [gl + t for t in range(rem)]
+    clocks = sampler.summary()
+    clocks["samples_timed_region"] = n_timed_samples  # the rest were taken during the spread pass
     return {"t_max": t_max, "W": W, "K": K, "gl": gl, "spread": spread, "step_ids": step_ids,
-            "clocks": sampler.summary(), "stream": stream}
+            "clocks": clocks, "stream": stream}
 
 
 def step_tokens(st, inp, ks, step_ids, dev, workspace_from=None):
@@ -1298,6 +1307,24 @@ def run_reference(args, rank, world):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+class nvtx_range:
+    """torch.cuda.nvtx range around a bench phase when --nvtx is given (no-op otherwise)."""
+
+    def __init__(self, args, name):
+        self.on, self.name = bool(getattr(args, "nvtx", False)), name
+
+    def __enter__(self):
+        if self.on:
+            import torch
+            torch.cuda.nvtx.range_push(self.name)
+        return self
+
+    def __exit__(self, *a):
+        if self.on:
+            import torch
+            torch.cuda.nvtx.range_pop()
+
+
 def main():
     # stdout carries only the JSON line: anything native code writes to fd 1 (e.g. NCCL's version
     # banner) is sent to stderr, and the line goes to a private duplicate of the original stdout
@@ -1307,6 +1334,8 @@ def main():
     os.dup2(2, 1)
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
+    if args.nvtx:
+        os.environ["TSV_NVTX"] = "1"  # read once by libtsv at its first entry-point call
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -1334,7 +1363,8 @@ def main():
             dist.barrier()
             dist.destroy_process_group()
         return
-    line = run_ours(args, rank, world, local_rank)
+    with nvtx_range(args, "bench:step"):
+        line = run_ours(args, rank, world, local_rank)
     if not args.no_extras:
         # every other workload of BASELINE.json / SURVEY.md 8(f) as a sub-object of the one JSON line, each
         # timed the same way (its own CUDA events, roofline, clocks and device status)
@@ -1351,7 +1381,8 @@ def main():
                 setattr(a2, k, v)
             t0 = time.perf_counter()
             try:
-                sub = fn(a2, rank, world, local_rank)
+                with nvtx_range(args, f"bench:{name}"):
+                    sub = fn(a2, rank, world, local_rank)
             except Exception as e:  # noqa: BLE001  (a failed sub-workload must not hide the main line)
                 sub = {"error": f"{type(e).__name__}: {e}"[:300]} if rank == 0 else None
             if sub is not None:

@@ -7,6 +7,7 @@
 //                    fixed-point goodput / acceptance counters across ranks;
 //   vocab-sharded:   tsv_verify_accept_sharded = shard partial -> ncclAllGather of
 //                    tsv_shard_tuple rows over NVLink/NVSwitch -> combine.
+#include <stdlib.h>
 #include <dlfcn.h>
 #include <nccl.h>
 #include <stdarg.h>
@@ -31,6 +32,14 @@ void set_error(const char* fmt, ...) {
 tsv_status cuda_status(cudaError_t e, const char* what) {
     set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
     return TSV_ERR_CUDA;
+}
+
+bool nvtx_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("TSV_NVTX");
+        return e && e[0] == '1';
+    }();
+    return on;
 }
 
 tsv_status check_device() {
@@ -113,6 +122,7 @@ extern "C" const char* tsv_last_error(void) { return g_err; }
 extern "C" int tsv_abi_version(void) { return TSV_ABI_VERSION; }
 
 extern "C" tsv_status tsv_comm_get_unique_id(void* unique_id_out) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(unique_id_out != nullptr, "tsv_comm_get_unique_id: out is NULL");
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
     TSV_TRY(nccl_ready());
@@ -123,6 +133,7 @@ extern "C" tsv_status tsv_comm_get_unique_id(void* unique_id_out) {
 }
 
 extern "C" tsv_status tsv_comm_init(tsv_comm** out, const void* unique_id, int32_t rank, int32_t world) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(out && unique_id, "tsv_comm_init: NULL argument");
     TSV_REQUIRE(world >= 1 && rank >= 0 && rank < world, "tsv_comm_init: bad rank %d / world %d", rank, world);
     TSV_TRY(check_device());
@@ -142,6 +153,7 @@ extern "C" tsv_status tsv_comm_init(tsv_comm** out, const void* unique_id, int32
 }
 
 extern "C" tsv_status tsv_comm_destroy(tsv_comm* comm) {
+    TSV_TRACE_CALL();
     if (!comm) return TSV_OK;
     TSV_TRY(nccl_ready());
     tsv_status s = nccl_status(g_nccl.CommDestroy(comm->comm), "ncclCommDestroy");
@@ -151,6 +163,7 @@ extern "C" tsv_status tsv_comm_destroy(tsv_comm* comm) {
 
 // Sharded workspace: [verify slots][dense: tuples local + gathered G x rows_p | lazy: masks B, keys 2B]
 extern "C" tsv_status tsv_verify_sharded_workspace_size(const tsv_verify_args* a, int32_t world, size_t* bytes) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(a && bytes, "tsv_verify_sharded_workspace_size: NULL argument");
     TSV_REQUIRE(world >= 1, "tsv_verify_sharded_workspace_size: world < 1");
     size_t slots = 0;
@@ -164,6 +177,7 @@ extern "C" tsv_status tsv_verify_sharded_workspace_size(const tsv_verify_args* a
 }
 
 extern "C" tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_comm* comm, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(a && comm, "tsv_verify_accept_sharded: NULL argument");
     TSV_TRY(nccl_ready());
     size_t need = 0, slots = 0;
@@ -198,6 +212,7 @@ extern "C" tsv_status tsv_verify_accept_sharded(const tsv_verify_args* a, tsv_co
 }
 
 extern "C" tsv_status tsv_allreduce_i64(int64_t* data, size_t count, tsv_comm* comm, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(data && comm, "tsv_allreduce_i64: NULL argument");
     TSV_TRY(nccl_ready());
     return nccl_status(g_nccl.AllReduce(data, data, count, ncclInt64, ncclSum, comm->comm,
@@ -212,6 +227,7 @@ extern "C" tsv_status tsv_goodput_choose_k_sharded(const double* alpha, int32_t 
                                                    int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
                                                    int32_t* k_per_request, int64_t* sums_ws, tsv_comm* comm,
                                                    void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(comm && sums_ws, "tsv_goodput_choose_k_sharded: NULL argument");
     TSV_TRY(nccl_ready());
     TSV_TRY(tsv_goodput_partial(alpha, alpha_per_request, ctx_len, cap, B, k_max, sums_ws, stream));
@@ -224,6 +240,7 @@ extern "C" tsv_status tsv_update_acceptance_sharded(double* alpha, const int32_t
                                                     const int32_t* row_offsets, int32_t B, double decay,
                                                     int32_t estimator, int64_t* sums_ws, tsv_comm* comm,
                                                     void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(comm && sums_ws && alpha, "tsv_update_acceptance_sharded: NULL argument");
     TSV_TRY(nccl_ready());
     TSV_TRY(tsv_update_partial(num_accepted, row_offsets, B, estimator, sums_ws, stream));
@@ -269,6 +286,7 @@ __global__ void debug_philox_kernel(const uint32_t* ctr, const uint32_t* key, ui
 }  // namespace tsv
 
 extern "C" tsv_status tsv_debug_race_E(uint32_t m_begin, uint32_t n, float* out, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(out != nullptr, "tsv_debug_race_E: out is NULL");
     TSV_REQUIRE(static_cast<uint64_t>(m_begin) + n <= (1ull << 23), "tsv_debug_race_E: range beyond 2^23");
     TSV_TRY(check_device());
@@ -280,6 +298,7 @@ extern "C" tsv_status tsv_debug_race_E(uint32_t m_begin, uint32_t n, float* out,
 
 extern "C" tsv_status tsv_debug_philox(const uint32_t* ctr, const uint32_t* key, uint32_t n, uint32_t* out,
                                        int32_t race_variant, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(ctr && key && out, "tsv_debug_philox: NULL argument");
     TSV_TRY(check_device());
     if (n == 0) return TSV_OK;

@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include "../../include/tsv.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace tsv {
 
@@ -47,6 +48,21 @@ tsv_status cuda_status(cudaError_t e, const char* what);
     } while (0)
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Tracing: with TSV_NVTX=1 in the environment every C-ABI entry point opens an
+// NVTX range named after itself (host side: the call that enqueues the kernels), visible to nsys and to
+// ncu's --nvtx filters.  Off by default; one cached getenv per process.
+bool nvtx_enabled();
+struct NvtxScope {
+    bool on;
+    explicit NvtxScope(const char* name) : on(nvtx_enabled()) {
+        if (on) nvtxRangePushA(name);
+    }
+    ~NvtxScope() {
+        if (on) nvtxRangePop();
+    }
+};
+#define TSV_TRACE_CALL() ::tsv::NvtxScope tsv_nvtx_scope_(__func__)
 
 // ---------------------------------------------------------------- device side
 constexpr uint32_t kPhiloxM0 = 0xD2511F53u;

@@ -172,6 +172,7 @@ extern "C" tsv_status tsv_goodput_choose_k_batched(const double* alpha, const in
                                                    int32_t policy, tsv_latency_model target, tsv_latency_model draft,
                                                    double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
                                                    double* goodput_out, int32_t* k_per_request, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(n_inst >= 0, "tsv_goodput_choose_k_batched: n_inst < 0");
     TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_choose_k_batched: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
     TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_choose_k_batched: unknown policy");
@@ -200,6 +201,7 @@ extern "C" tsv_status tsv_goodput_choose_k_batched(const double* alpha, const in
 extern "C" tsv_status tsv_goodput_partial(const double* alpha, int32_t alpha_per_request, const int32_t* ctx_len,
                                           const int32_t* cap, int32_t B, int32_t k_max, int64_t* sums,
                                           void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 0, "tsv_goodput_partial: B < 0 (%d)", B);
     TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_partial: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
     TSV_REQUIRE(sums != nullptr, "tsv_goodput_partial: sums is NULL");
@@ -228,6 +230,7 @@ extern "C" tsv_status tsv_goodput_finalize(const int64_t* sums, int32_t k_max, i
                                            int64_t kv_free_slots, const int32_t* cap, int32_t B_local,
                                            int32_t* k_out, double* goodput_out, int32_t* k_per_request,
                                            void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_finalize: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
     TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_finalize: unknown policy %d", policy);
     TSV_REQUIRE(sums && k_out, "tsv_goodput_finalize: a required array is NULL");
@@ -254,6 +257,7 @@ extern "C" tsv_status tsv_goodput_finalize(const int64_t* sums, int32_t k_max, i
 
 extern "C" tsv_status tsv_update_partial(const int32_t* num_accepted, const int32_t* row_offsets, int32_t B,
                                          int32_t estimator, int64_t* sums, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 0, "tsv_update_partial: B < 0");
     TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED, "tsv_update_partial: unknown estimator");
     TSV_REQUIRE(sums != nullptr, "tsv_update_partial: sums is NULL");
@@ -275,6 +279,7 @@ extern "C" tsv_status tsv_update_partial(const int32_t* num_accepted, const int3
 }
 
 extern "C" tsv_status tsv_update_finalize(double* alpha, const int64_t* sums, double decay, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(alpha && sums, "tsv_update_finalize: NULL argument");
     TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_update_finalize: decay %g outside [0, 1]", decay);
     TSV_TRY(check_device());
@@ -290,6 +295,7 @@ extern "C" tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_pe
                                            tsv_latency_model draft, double pld_cost_ms,
                                            int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
                                            int32_t* k_per_request, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 1, "tsv_goodput_choose_k: B must be >= 1 (got %d)", B);
     TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_choose_k: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
     TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_choose_k: unknown policy %d", policy);
@@ -318,6 +324,7 @@ extern "C" tsv_status tsv_goodput_choose_k(const double* alpha, int32_t alpha_pe
 extern "C" tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, const int32_t* num_accepted,
                                             const int32_t* row_offsets, int32_t B, double decay,
                                             int32_t estimator, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 0, "tsv_update_acceptance: B < 0");
     TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_update_acceptance: decay %g outside [0, 1]", decay);
     TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED, "tsv_update_acceptance: unknown estimator");
@@ -343,6 +350,7 @@ extern "C" tsv_status tsv_goodput_choose_k_p2p(const double* alpha, int32_t alph
                                                int64_t kv_free_slots, int32_t* k_out, double* goodput_out,
                                                int32_t* k_per_request, tsv_p2p* p, int32_t* device_status,
                                                void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 0, "tsv_goodput_choose_k_p2p: B < 0 (%d)", B);
     TSV_REQUIRE(k_max >= 0 && k_max <= TSV_MAX_K, "tsv_goodput_choose_k_p2p: k_max %d outside [0, %d]", k_max, TSV_MAX_K);
     TSV_REQUIRE(policy == TSV_POLICY_DRAFT || policy == TSV_POLICY_PLD, "tsv_goodput_choose_k_p2p: unknown policy %d",
@@ -374,6 +382,7 @@ extern "C" tsv_status tsv_goodput_choose_k_p2p(const double* alpha, int32_t alph
 extern "C" tsv_status tsv_update_acceptance_p2p(double* alpha, int32_t per_request, const int32_t* num_accepted,
                                                 const int32_t* row_offsets, int32_t B, double decay, int32_t estimator,
                                                 tsv_p2p* p, int32_t* device_status, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 0, "tsv_update_acceptance_p2p: B < 0");
     TSV_REQUIRE(decay >= 0.0 && decay <= 1.0, "tsv_update_acceptance_p2p: decay %g outside [0, 1]", decay);
     TSV_REQUIRE(estimator == TSV_EST_TESTED || estimator == TSV_EST_PROPOSED,
@@ -453,6 +462,7 @@ bool qr_lstsq(const std::vector<double>& X, const std::vector<double>& y, int n,
 
 extern "C" tsv_status tsv_fit_latency_model(const double* ctx_tokens, const double* batched_tokens,
                                             const double* ms, int32_t n, tsv_latency_model* out, double* r2_out) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(n >= 3, "tsv_fit_latency_model: TooFewSamples (n = %d < 3)", n);
     TSV_REQUIRE(ctx_tokens && batched_tokens && ms && out, "tsv_fit_latency_model: NULL argument");
     std::vector<double> X(3 * static_cast<size_t>(n)), y(ms, ms + n);

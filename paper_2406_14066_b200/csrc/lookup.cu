@@ -258,6 +258,7 @@ extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_
                                          int32_t n_min, int32_t n_max, int32_t k_fixed,
                                          int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
                                          void* stream) {
+    TSV_TRACE_CALL();
     return tsv_propose_lookup_ex(ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, device_status,
                                  0, stream);
 }
@@ -266,6 +267,7 @@ extern "C" tsv_status tsv_propose_lookup_ex(const int32_t* ctx, const int32_t* c
                                             int32_t n_min, int32_t n_max, int32_t k_fixed,
                                             int32_t* proposals, int32_t* proposal_len, int32_t* device_status,
                                             int32_t flags, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE((flags & ~TSV_LOOKUP_INPUTS_READY) == 0, "tsv_propose_lookup: unknown flags 0x%x", flags);
     TSV_REQUIRE(B >= 0, "tsv_propose_lookup: B < 0 (%d)", B);
     TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
@@ -291,6 +293,7 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
                                                   double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
                                                   double* goodput_out, int32_t* k_per_request,
                                                   uint32_t* counter, int32_t* device_status, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 1, "tsv_propose_lookup_choose_k: B must be >= 1 (got %d)", B);
     TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
                 "tsv_propose_lookup_choose_k: need 1 <= n_min (%d) <= n_max (%d) <= %d", n_min, n_max, TSV_MAX_NGRAM);

@@ -122,6 +122,7 @@ using namespace tsv;
 extern "C" tsv_status tsv_sim_target(const int32_t* proposals, int32_t K, const int32_t* k_req, int32_t B,
                                      const float* alpha_true, int32_t V, int64_t ld, int32_t rows_cap, float* p_out,
                                      int32_t* row_offsets, int32_t* drafts, int32_t* row_info, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 0 && K >= 1 && K <= TSV_MAX_K, "tsv_sim_target: need B >= 0 and 1 <= K <= %d", TSV_MAX_K);
     TSV_REQUIRE(V >= 1 && ld >= V && ld % 4 == 0, "tsv_sim_target: need 1 <= V <= ld, ld %% 4 == 0");
     TSV_REQUIRE(rows_cap >= B * (K + 1), "tsv_sim_target: rows_cap %d < B (K + 1)", rows_cap);
@@ -145,6 +146,7 @@ extern "C" tsv_status tsv_sim_target(const int32_t* proposals, int32_t K, const 
 extern "C" tsv_status tsv_context_append(const int32_t* ctx_in, int32_t L, int32_t B, const int32_t* out_tokens,
                                          const int32_t* num_accepted, int32_t k_max, int32_t* ctx_out,
                                          int32_t* ctx_len, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(B >= 0 && L >= 1 && k_max >= 0 && k_max <= TSV_MAX_K, "tsv_context_append: bad sizes");
     if (B == 0) return TSV_OK;
     TSV_REQUIRE(ctx_in && out_tokens && num_accepted && ctx_out && ctx_len && ctx_in != ctx_out,

@@ -1495,6 +1495,7 @@ static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_
 using namespace tsv;
 
 extern "C" tsv_status tsv_verify_workspace_size(const tsv_verify_args* a, size_t* bytes) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(bytes != nullptr, "tsv_verify_workspace_size: bytes is NULL");
     TSV_TRY(validate(a));
     *bytes = workspace_bytes(a);
@@ -1502,6 +1503,7 @@ extern "C" tsv_status tsv_verify_workspace_size(const tsv_verify_args* a, size_t
 }
 
 extern "C" tsv_status tsv_workspace_clear(void* workspace, size_t bytes, void* stream) {
+    TSV_TRACE_CALL();
     if (bytes == 0) return TSV_OK;
     TSV_REQUIRE(workspace != nullptr, "tsv_workspace_clear: workspace is NULL");
     TSV_CUDA(cudaMemsetAsync(workspace, 0, bytes, static_cast<cudaStream_t>(stream)), "cudaMemsetAsync");
@@ -1509,6 +1511,7 @@ extern "C" tsv_status tsv_workspace_clear(void* workspace, size_t bytes, void* s
 }
 
 extern "C" tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
                 "tsv_verify_accept: unsharded call needs vocab_offset == 0 and vocab == vocab_global "
@@ -1523,6 +1526,7 @@ extern "C" tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream) 
 
 extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                                double decay, int32_t estimator, void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
                 "tsv_verify_accept_update: unsharded call needs vocab_offset == 0 and vocab == vocab_global");
@@ -1547,6 +1551,7 @@ extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double*
 
 extern "C" tsv_status tsv_verify_accept_update_p2p(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                                    double decay, int32_t estimator, tsv_p2p* p, void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
                 "tsv_verify_accept_update_p2p: needs the whole vocabulary (request-sharded mode)");
@@ -1577,6 +1582,7 @@ extern "C" tsv_status tsv_verify_accept_update_p2p(const tsv_verify_args* a, dou
 
 extern "C" tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_shard_tuple* tuples_out,
                                                void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     if (a->B == 0) return TSV_OK;
     TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
@@ -1591,6 +1597,7 @@ extern "C" tsv_status tsv_verify_shard_partial(const tsv_verify_args* a, tsv_sha
 
 extern "C" tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const tsv_shard_tuple* gathered,
                                                int32_t num_shards, void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     if (a->B == 0) return TSV_OK;
     TSV_TRY(check_device());
@@ -1606,6 +1613,7 @@ extern "C" tsv_status tsv_verify_shard_combine(const tsv_verify_args* a, const t
 }
 
 extern "C" tsv_status tsv_verify_shard_flags(const tsv_verify_args* a, uint64_t* masks_out, void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     if (a->B == 0) return TSV_OK;
     TSV_TRY(check_device());
@@ -1619,6 +1627,7 @@ extern "C" tsv_status tsv_verify_shard_flags(const tsv_verify_args* a, uint64_t*
 
 extern "C" tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint64_t* masks, uint64_t* keys_out,
                                             void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     if (a->B == 0) return TSV_OK;
     TSV_REQUIRE_WS(a->workspace != nullptr && a->workspace_bytes >= workspace_bytes(a),
@@ -1646,6 +1655,7 @@ extern "C" tsv_status tsv_verify_shard_race(const tsv_verify_args* a, const uint
 
 extern "C" tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_t* masks, const uint64_t* keys,
                                             void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     if (a->B == 0) return TSV_OK;
     TSV_TRY(check_device());
@@ -1660,10 +1670,12 @@ extern "C" tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint
 
 #if TSV_TRACE
 extern "C" TSV_API tsv_status tsv_debug_trace(unsigned long long* out, int32_t n) {
+    TSV_TRACE_CALL();
     TSV_CUDA(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 4 * static_cast<size_t>(n)), "trace copy");
     return TSV_OK;
 }
 extern "C" TSV_API tsv_status tsv_debug_trace_clear() {
+    TSV_TRACE_CALL();
     static unsigned long long zeros[kTraceMax][4];
     TSV_CUDA(cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros)), "trace clear");
     return TSV_OK;
@@ -1671,6 +1683,7 @@ extern "C" TSV_API tsv_status tsv_debug_trace_clear() {
 #endif
 
 extern "C" tsv_status tsv_verify_greedy(const tsv_verify_args* a, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(a != nullptr, "tsv_verify_greedy: args is NULL");
     TSV_REQUIRE(a->B >= 0, "tsv_verify_greedy: B < 0 (%d)", a->B);
     TSV_REQUIRE(a->k_max >= 0 && a->k_max <= TSV_MAX_K, "tsv_verify_greedy: k_max %d outside [0, %d]", a->k_max, TSV_MAX_K);
@@ -1750,6 +1763,7 @@ static size_t logits_extra_bytes(const tsv_verify_args* a, int32_t n_chunks) {
 }
 
 extern "C" tsv_status tsv_verify_logits_workspace_size(const tsv_verify_args* a, size_t* bytes) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(bytes != nullptr, "tsv_verify_logits_workspace_size: bytes is NULL");
     TSV_TRY(validate(a));
     const RaceParams P = stats_params(a, make_params(a));
@@ -1758,6 +1772,7 @@ extern "C" tsv_status tsv_verify_logits_workspace_size(const tsv_verify_args* a,
 }
 
 extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float temperature, void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
                 "tsv_verify_accept_logits: vocab sharding is not supported");
@@ -1801,6 +1816,7 @@ extern "C" tsv_status tsv_verify_accept_logits(const tsv_verify_args* a, float t
 
 extern "C" tsv_status tsv_softmax_rows(const float* z, int64_t ld, int32_t vocab, int32_t rows, float temperature,
                                        float* p_out, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(rows >= 0, "tsv_softmax_rows: rows < 0");
     TSV_REQUIRE(vocab >= 1 && vocab <= ld, "tsv_softmax_rows: vocab %d outside [1, ld]", vocab);
     TSV_REQUIRE(temperature > 0.0f && temperature < INFINITY, "tsv_softmax_rows: temperature must be > 0");
@@ -1851,6 +1867,7 @@ __global__ void debug_race_row_kernel(const float* __restrict__ w, const uint32_
 
 extern "C" tsv_status tsv_debug_race_row(const float* w, const uint32_t* words, int32_t V, int32_t prune,
                                          uint64_t* key_out, void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(w && words && key_out && V >= 1, "tsv_debug_race_row: bad arguments");
     TSV_TRY(check_device());
     auto* k = reinterpret_cast<unsigned long long*>(key_out);
@@ -1863,12 +1880,14 @@ extern "C" tsv_status tsv_debug_race_row(const float* w, const uint32_t* words, 
 // ------------------------------------------------------------ peer-memory vocab sharding (host)
 
 extern "C" tsv_status tsv_p2p_buffer_size(int32_t B_max, size_t* bytes) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(bytes != nullptr && B_max >= 1, "tsv_p2p_buffer_size: bad arguments");
     *bytes = tsv::p2p_buffer_bytes(B_max);
     return TSV_OK;
 }
 
 extern "C" tsv_status tsv_p2p_alloc(int32_t B_max, void** buf_out, void* ipc_handle_out) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(buf_out != nullptr && B_max >= 1, "tsv_p2p_alloc: bad arguments");
     TSV_TRY(check_device());
     void* p = nullptr;
@@ -1886,11 +1905,13 @@ extern "C" tsv_status tsv_p2p_alloc(int32_t B_max, void** buf_out, void* ipc_han
 }
 
 extern "C" tsv_status tsv_p2p_free(void* buf) {
+    TSV_TRACE_CALL();
     if (buf) TSV_CUDA(cudaFree(buf), "cudaFree (p2p buffer)");
     return TSV_OK;
 }
 
 extern "C" tsv_status tsv_p2p_open(const void* ipc_handle, void** buf_out) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(ipc_handle && buf_out, "tsv_p2p_open: NULL argument");
     cudaIpcMemHandle_t h;
     memcpy(&h, ipc_handle, sizeof(h));
@@ -1899,11 +1920,13 @@ extern "C" tsv_status tsv_p2p_open(const void* ipc_handle, void** buf_out) {
 }
 
 extern "C" tsv_status tsv_p2p_close(void* buf) {
+    TSV_TRACE_CALL();
     if (buf) TSV_CUDA(cudaIpcCloseMemHandle(buf), "cudaIpcCloseMemHandle");
     return TSV_OK;
 }
 
 extern "C" tsv_status tsv_p2p_init(tsv_p2p** out, int32_t rank, int32_t world, int32_t B_max, void* const* bufs) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(out && bufs, "tsv_p2p_init: NULL argument");
     TSV_REQUIRE(world >= 1 && world <= TSV_P2P_MAX_WORLD && rank >= 0 && rank < world && B_max >= 1,
                 "tsv_p2p_init: rank %d / world %d / B_max %d invalid", rank, world, B_max);
@@ -1921,11 +1944,13 @@ extern "C" tsv_status tsv_p2p_init(tsv_p2p** out, int32_t rank, int32_t world, i
 }
 
 extern "C" tsv_status tsv_p2p_destroy(tsv_p2p* p) {
+    TSV_TRACE_CALL();
     delete p;
     return TSV_OK;
 }
 
 extern "C" tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p2p* p, int32_t phase, void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     TSV_REQUIRE(p != nullptr, "tsv_verify_shard_p2p_phase: p2p handle is NULL");
     TSV_REQUIRE(phase >= 0 && phase <= 2, "tsv_verify_shard_p2p_phase: phase %d", phase);
@@ -1958,12 +1983,14 @@ extern "C" tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p
 }
 
 extern "C" tsv_status tsv_verify_accept_sharded_p2p(const tsv_verify_args* a, tsv_p2p* p, void* stream) {
+    TSV_TRACE_CALL();
     for (int32_t ph = 0; ph < 3; ++ph) TSV_TRY(tsv_verify_shard_p2p_phase(a, p, ph, stream));
     return TSV_OK;
 }
 
 extern "C" tsv_status tsv_allreduce_i64_p2p(int64_t* data, int32_t count, tsv_p2p* p, int32_t* device_status,
                                            void* stream) {
+    TSV_TRACE_CALL();
     TSV_REQUIRE(data && p, "tsv_allreduce_i64_p2p: NULL argument");
     TSV_REQUIRE(count >= 0 && count <= TSV_P2P_MAX_SUMS, "tsv_allreduce_i64_p2p: count %d outside [0, %d]", count,
                 TSV_P2P_MAX_SUMS);
