@@ -114,16 +114,19 @@ TSV_API tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_off
                               void* stream);
 
 /* tsv_propose_lookup with flags (tsv_propose_lookup == flags 0).
- *   TSV_LOOKUP_INPUTS_READY  Contract (as TSV_VERIFY_META_READY): ctx and
- *     ctx_offsets are COMPLETE before the kernel that immediately precedes
- *     this call on the stream could start -- no kernel still in flight when
- *     the lookup launches writes them (e.g. the context buffer is prepared by
- *     the host / a copy before the step, as a serving engine's input
- *     preparation does; NOT when the previous step's emit appends to it on the
- *     device).  The search (loads, compares, reduction, token gather) then runs
- *     before the grid-dependency wait, overlapping the preceding kernel; only
- *     the stores of proposals / proposal_len / device_status wait.  Outputs are
- *     identical to flags 0.
+ *   TSV_LOOKUP_INPUTS_READY  Contract: no kernel that can still be in flight
+ *     when this call's kernel starts writes its inputs (ctx, ctx_offsets) or
+ *     reads its outputs (proposals, proposal_len).  Under programmatic
+ *     dependent launch a kernel may start while its predecessor drains; every
+ *     libtsv kernel triggers its dependents only after its own grid-dependency
+ *     wait, so in a chain of libtsv calls only the IMMEDIATELY preceding kernel
+ *     can be in flight (data written two or more kernels back is complete), and
+ *     a kernel launched without programmatic serialization is complete.  True
+ *     e.g. when the context buffer is prepared before the step (a serving
+ *     engine's input preparation); NOT when the immediately preceding kernel
+ *     appends to it.  The whole lookup then runs before the grid-dependency
+ *     wait, overlapping the preceding kernel; the kernel waits at its end (it
+ *     still completes after its predecessor).  Outputs identical to flags 0.
  * Errors: as tsv_propose_lookup; INVALID_ARG for unknown flags. */
 #define TSV_LOOKUP_INPUTS_READY 1
 TSV_API tsv_status tsv_propose_lookup_ex(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
@@ -407,6 +410,21 @@ TSV_API tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int32_t
                                        double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
                                        double* goodput_out, int32_t* k_per_request,
                                        uint32_t* counter, int32_t* device_status, void* stream);
+/* With flags: TSV_LOOKUP_INPUTS_READY as for tsv_propose_lookup_ex, the inputs
+ * being ctx, ctx_offsets, ctx_len and alpha and the outputs proposals,
+ * proposal_len, k_out, goodput_out and k_per_request: the search, the batch
+ * sums and the last CTA's ArgMaxGoodput all run before the grid-dependency
+ * wait.  In a decode step alpha comes from the previous step's update (two or
+ * more kernels back), so it qualifies. */
+TSV_API tsv_status tsv_propose_lookup_choose_k_ex(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                                          int32_t n_min, int32_t n_max, int32_t k_fixed,
+                                          int32_t* proposals, int32_t* proposal_len,
+                                          const double* alpha, int32_t alpha_per_request,
+                                          const int32_t* ctx_len, tsv_latency_model target,
+                                          double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
+                                          double* goodput_out, int32_t* k_per_request,
+                                          uint32_t* counter, int32_t* device_status, int32_t flags,
+                                          void* stream);
 
 /* --------------------------------------------------------------------------
  * Acceptance-rate update: UpdateGlobalAcceptance (Listing 1 line 19,

@@ -164,11 +164,11 @@ __device__ __forceinline__ void fused_choose_k(const ChooseArgs& A, FusedScratch
 // FUSED: the CTA that finishes last also runs ArgMaxGoodput (PLD policy, cap_i = the
 // proposal lengths just written) -- GetVerificationLen right after Propose (Listing 1).
 //
-// READY (TSV_LOOKUP_INPUTS_READY, tsv_propose_lookup_ex): ctx and ctx_offsets were complete before the
-// preceding kernel on the stream could start, so the whole search -- loads, compares, the block
-// reduction and the gather of the proposed tokens -- runs before the grid-dependency wait, while the
-// preceding kernel drains; only the stores of proposals / proposal_len / device_status wait.  The
-// kernel still triggers its dependents only after its own wait (the PDL chain invariant, tsv.h).
+// READY (TSV_LOOKUP_INPUTS_READY, include/tsv.h): no kernel still in flight writes the inputs or reads
+// the outputs, so the whole kernel -- the search, the stores of the proposals and, when FUSED, the
+// batch sums, the last CTA's ArgMaxGoodput and its stores -- runs before the grid-dependency wait,
+// overlapping the preceding kernel; every thread waits at the very end, so the kernel still completes
+// after its predecessor and triggers its dependents only after its own wait (the PDL chain invariant).
 template <bool FUSED, bool READY = false>
 __global__ void __launch_bounds__(kLookupThreads)
     ngram_lookup_kernel(const int32_t* __restrict__ ctx, const int32_t* __restrict__ ctx_offsets, int32_t B,
@@ -233,21 +233,17 @@ __global__ void __launch_bounds__(kLookupThreads)
         if (L >= 2 && n_star >= n_min) len = min(K, L - 1 - e_star);
         my_len = len;
         int32_t* out = proposals + static_cast<int64_t>(i) * K;
-        if (READY) {  // K <= TSV_MAX_K < 32: lane t holds proposed token t; then wait, then store
-            const int32_t tok = (tid < K && tid < len) ? __ldg(c + e_star + 1 + tid) : -1;
-            pdl_wait();
-            pdl_launch_dependents();
-            if (tid < K) out[tid] = tok;
-            if (tid == 0) {
-                proposal_len[i] = len;
-                if (bad_ctx && devstatus) atomicOr(reinterpret_cast<unsigned int*>(devstatus), TSV_DEVSTATUS_BAD_CONTEXT);
-            }
-        } else {
-            for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? __ldg(c + e_star + 1 + t) : -1;
-            if (tid == 0) proposal_len[i] = len;
+        for (int32_t t = tid; t < K; t += 32) out[t] = t < len ? __ldg(c + e_star + 1 + t) : -1;
+        if (tid == 0) {
+            proposal_len[i] = len;
+            if (READY && bad_ctx && devstatus) atomicOr(reinterpret_cast<unsigned int*>(devstatus), TSV_DEVSTATUS_BAD_CONTEXT);
         }
     }
     if (FUSED) fused_choose_k(ca, reinterpret_cast<FusedScratch*>(counter), i, my_len);
+    if (READY) {
+        pdl_wait();
+        pdl_launch_dependents();
+    }
 }
 
 }  // namespace tsv
@@ -294,6 +290,22 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
                                                   double* goodput_out, int32_t* k_per_request,
                                                   uint32_t* counter, int32_t* device_status, void* stream) {
     TSV_TRACE_CALL();
+    return tsv_propose_lookup_choose_k_ex(ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, alpha,
+                                          alpha_per_request, ctx_len, target, pld_cost_ms, kv_free_slots, k_out,
+                                          goodput_out, k_per_request, counter, device_status, 0, stream);
+}
+
+extern "C" tsv_status tsv_propose_lookup_choose_k_ex(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
+                                                     int32_t n_min, int32_t n_max, int32_t k_fixed,
+                                                     int32_t* proposals, int32_t* proposal_len,
+                                                     const double* alpha, int32_t alpha_per_request,
+                                                     const int32_t* ctx_len, tsv_latency_model target,
+                                                     double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
+                                                     double* goodput_out, int32_t* k_per_request,
+                                                     uint32_t* counter, int32_t* device_status, int32_t flags,
+                                                     void* stream) {
+    TSV_TRACE_CALL();
+    TSV_REQUIRE((flags & ~TSV_LOOKUP_INPUTS_READY) == 0, "tsv_propose_lookup_choose_k: unknown flags 0x%x", flags);
     TSV_REQUIRE(B >= 1, "tsv_propose_lookup_choose_k: B must be >= 1 (got %d)", B);
     TSV_REQUIRE(n_min >= 1 && n_min <= n_max && n_max <= TSV_MAX_NGRAM,
                 "tsv_propose_lookup_choose_k: need 1 <= n_min (%d) <= n_max (%d) <= %d", n_min, n_max, TSV_MAX_NGRAM);
@@ -318,7 +330,8 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
     A.B = B;
     A.k_max = k_fixed;
     A.policy = TSV_POLICY_PLD;
-    TSV_CUDA(launch_pdl(ngram_lookup_kernel<true>, dim3(B), dim3(kLookupThreads), 0,
+    auto kern = (flags & TSV_LOOKUP_INPUTS_READY) ? ngram_lookup_kernel<true, true> : ngram_lookup_kernel<true, false>;
+    TSV_CUDA(launch_pdl(kern, dim3(B), dim3(kLookupThreads), 0,
                         static_cast<cudaStream_t>(stream), ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals,
                         proposal_len, A, counter, device_status),
              "ngram_lookup_kernel launch");

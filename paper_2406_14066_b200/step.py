@@ -165,12 +165,12 @@ class SpecStep:
         st = tsv._stream(stream)
         L = tsv.lib()
         if self.fused:
-            tsv._check(L.tsv_propose_lookup_choose_k(
+            tsv._check(L.tsv_propose_lookup_choose_k_ex(
                 inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s), inp.n_min, inp.n_max, inp.k_fixed,
                 self.proposals.data_ptr(), self.proposal_len.data_ptr(), self.alpha.data_ptr(), 0,
                 inp.ctx_len[s].data_ptr(), tsv.LatencyModel(*inp.target), float(inp.pld_cost_ms),
                 int(inp.kv_free_slots), self.k_star.data_ptr(), self.goodput.data_ptr(), self.k_req.data_ptr(),
-                self.counter.data_ptr(), self.status.data_ptr(), st))
+                self.counter.data_ptr(), self.status.data_ptr(), self.lookup_flags, st))
             a = self.args[s]
             a.step = step & 0xFFFFFFFF
             tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,

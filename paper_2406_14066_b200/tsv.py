@@ -52,7 +52,7 @@ EXPORTED = [
     "tsv_p2p_buffer_size", "tsv_p2p_alloc", "tsv_p2p_free", "tsv_p2p_open", "tsv_p2p_close", "tsv_p2p_init",
     "tsv_p2p_destroy", "tsv_verify_accept_sharded_p2p", "tsv_verify_shard_p2p_phase", "tsv_allreduce_i64_p2p",
     "tsv_goodput_choose_k_p2p", "tsv_update_acceptance_p2p", "tsv_verify_accept_update_p2p",
-    "tsv_propose_lookup_ex",
+    "tsv_propose_lookup_ex", "tsv_propose_lookup_choose_k_ex",
 ]
 
 
@@ -120,6 +120,8 @@ def _load() -> ctypes.CDLL:
         "tsv_allreduce_i64": ([P, sz, P, P], ctypes.c_int),
         "tsv_propose_lookup_choose_k": ([P, P, i32, i32, i32, i32, P, P, P, i32, P, LatencyModel, f64, i64,
                                          P, P, P, P, P, P], ctypes.c_int),
+        "tsv_propose_lookup_choose_k_ex": ([P, P, i32, i32, i32, i32, P, P, P, i32, P, LatencyModel, f64, i64,
+                                            P, P, P, P, P, i32, P], ctypes.c_int),
         "tsv_verify_accept_update": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P], ctypes.c_int),
         "tsv_debug_race_E": ([ctypes.c_uint32, ctypes.c_uint32, P, P], ctypes.c_int),
         "tsv_debug_philox": ([P, P, ctypes.c_uint32, P, i32, P], ctypes.c_int),
@@ -414,9 +416,10 @@ def lookup_choose_scratch(device) -> torch.Tensor:
 def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, ctx_len, target,
                                 pld_cost_ms, counter, kv_free_slots=-1, alpha_per_request=None,
                                 proposals=None, proposal_len=None, k_out=None, goodput_out=None,
-                                k_per_request=None, device_status=None, stream=None):
+                                k_per_request=None, device_status=None, stream=None, flags: int = 0):
     """Fused prompt lookup + PLD goodput selection.  ``counter``: device scratch of
     LOOKUP_CHOOSE_SCRATCH bytes (e.g. lookup_choose_scratch()), zeroed once.
+    flags: LOOKUP_INPUTS_READY (tsv_propose_lookup_choose_k_ex; include/tsv.h states the contract).
     Returns (proposals, proposal_len, k_out, goodput_out)."""
     B = ctx_offsets.numel() - 1
     dev = _dev(ctx_offsets)
@@ -432,12 +435,12 @@ def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, 
         goodput_out = torch.empty(k_fixed + 1, dtype=torch.float64, device=dev)
     per = (alpha.numel() == B and B > 1) if alpha_per_request is None else bool(alpha_per_request)
     ctx_p = _ptr(ctx) if ctx.numel() else _ptr(ctx_offsets)
-    _check(_lib.tsv_propose_lookup_choose_k(ctx_p, _ptr(ctx_offsets), B, n_min, n_max, k_fixed,
-                                            _ptr(proposals), _ptr(proposal_len), _ptr(alpha),
-                                            1 if per else 0, _ptr(ctx_len), LatencyModel(*target),
-                                            float(pld_cost_ms), int(kv_free_slots), _ptr(k_out),
-                                            _ptr(goodput_out), _ptr(k_per_request), _ptr(counter),
-                                            _ptr(device_status), _stream(stream)))
+    _check(_lib.tsv_propose_lookup_choose_k_ex(ctx_p, _ptr(ctx_offsets), B, n_min, n_max, k_fixed,
+                                               _ptr(proposals), _ptr(proposal_len), _ptr(alpha),
+                                               1 if per else 0, _ptr(ctx_len), LatencyModel(*target),
+                                               float(pld_cost_ms), int(kv_free_slots), _ptr(k_out),
+                                               _ptr(goodput_out), _ptr(k_per_request), _ptr(counter),
+                                               _ptr(device_status), int(flags), _stream(stream)))
     return proposals, proposal_len, k_out, goodput_out
 
 

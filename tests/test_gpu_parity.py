@@ -856,9 +856,11 @@ def test_step_graph_capture_matches_eager(tsv, fused):
         assert torch.equal(v, eager[k]), k
 
 
-def test_step_lookup_ready_multi_step_graph_matches_eager(tsv):
-    # three consecutive steps in one graph with TSV_LOOKUP_INPUTS_READY (the lookup of step t+1 searches
-    # while step t's emit drains) equal three eager steps without the flag (alpha carried across steps)
+@pytest.mark.parametrize("fused", [False, True])
+def test_step_lookup_ready_multi_step_graph_matches_eager(tsv, fused):
+    # three consecutive steps in one graph with TSV_LOOKUP_INPUTS_READY (the lookup of step t+1 -- and,
+    # fused, its ArgMaxGoodput over alpha from step t's update -- runs while step t's emit drains) equal
+    # three eager steps of the separate calls without the flag (alpha carried across steps)
     from paper_2406_14066_b200.step import SpecStep
     inp = synth.make_step_inputs(B=96, V=32000, L=2048, k_max=8, seed=21, device=DEV, sets=2)
     st = SpecStep(inp, lookup_ready=False)
@@ -866,7 +868,7 @@ def test_step_lookup_ready_multi_step_graph_matches_eager(tsv):
         st.run(step=t)
     torch.cuda.synchronize()
     eager = {k: v.clone() for k, v in st.outputs().items()}
-    st2 = SpecStep(inp, lookup_ready=True)
+    st2 = SpecStep(inp, lookup_ready=True, fused=fused)
     st2.capture(steps=[0, 1, 2])
     st2.replay()
     torch.cuda.synchronize()
