@@ -1347,21 +1347,9 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* z, int64
 static int sm_count();
 // Default work-item size: about one item per resident warp of the race kernel
 // (148 SMs x 4 CTAs x 8 warps), in whole 128-column iterations.  Never changes results.
-// Waves of race CTAs (experiments: env TSV_RACE_WAVES, default 1): > 1 sizes the items for that many
-// waves of resident warps, and the grid covers every item with one item per warp, so the hardware CTA
-// scheduler hands the later items to the SMs whose CTAs finish first.
-static double race_waves() {
-    static const double w = [] {
-        const char* e = getenv("TSV_RACE_WAVES");
-        const double v = e ? atof(e) : 1.0;
-        return v >= 1.0 && v <= 16.0 ? v : 1.0;
-    }();
-    return w;
-}
-
 static int32_t auto_chunk(const tsv_verify_args* a) {
     if (a->chunk > 0) return a->chunk;
-    const int64_t warps = static_cast<int64_t>(sm_count() * 32 * race_waves());  // resident warps x waves
+    const int64_t warps = static_cast<int64_t>(sm_count()) * 32;  // resident warps of the race kernel
     // chunks per row so that B * chunks <= warps (one wave), then the chunk covering V in that many
     const int64_t per_row = std::max<int64_t>(1, warps / std::max<int32_t>(a->B, 1));
     int64_t c = (a->vocab + per_row - 1) / per_row;
@@ -1468,7 +1456,7 @@ static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
     const int64_t n_items = static_cast<int64_t>(P.B) * per_req;
     TSV_REQUIRE(n_items < (1ll << 31), "verify: too many work items");
     const int64_t want = (n_items + kRaceWarps - 1) / kRaceWarps;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(sm_count() * occ * race_waves()))) +
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * occ)) +
                          ((MODE == kLazy && P.race_update) ? 1 : 0);
     TSV_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kRaceThreads), 0, st, P), "verify_race_kernel launch");
     return TSV_OK;
