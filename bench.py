@@ -75,7 +75,7 @@ def parse():
                          "temperature-0 verify (NEXT 2) on the config-2 batch (weak scaling); logits: the fused "
                          "softmax-from-logits verify (NEXT 1) on the config-2 batch given as logits; config5: the "
                          "goodput sweep (B 1-512 x alpha 0.3-0.9, K = 8) as one batched choose-k launch")
-    ap.add_argument("--shard-mode", default="auto", choices=["auto", "none", "lazy", "dense", "p2p"],
+    ap.add_argument("--shard-mode", default="auto", choices=["auto", "none", "lazy", "dense", "p2p", "p2p_fused"],
                     help="config4 sharding mode: lazy two rounds over NCCL all-reduces, one-round dense over an "
                          "NCCL all-gather, or the lazy two rounds over NVLink peer memory (no NCCL); none = the "
                          "unsharded tsv_verify_accept (N = 1 only); auto = p2p for N > 1, none for N = 1")
@@ -195,6 +195,17 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------- our arm
+def committed_traffic(workload):
+    """DRAM bytes (read + write) per call of a workload's kernels from the committed ncu capture
+    (profiles/r02/traffic.json, scripts/traffic.sh: cold caches, per-launch means summed over the call's
+    kernels); None when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "traffic.json")) as f:
+            return json.load(f)[workload]["dram_bytes_per_call"]
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def _sets_for(args, bytes_per_set, l2):
     """Rotating input sets: at least --sets, and enough that R x footprint >= 3 x L2."""
     need = int(np.ceil(3.0 * l2 / max(1, bytes_per_set)))
@@ -675,10 +686,12 @@ def run_config4(args, rank, world, local_rank):
         args.shard_mode = "p2p" if world > 1 else "none"
     if args.shard_mode == "none" and world > 1:
         raise SystemExit("--shard-mode none is the one-GPU (unsharded) call")
-    p2p = args.shard_mode == "p2p"
+    p2p = args.shard_mode in ("p2p", "p2p_fused")
     unsharded = args.shard_mode == "none"
     comm = None if unsharded else (tsv.P2PComm(rank, world, B_max=B) if p2p else tsv.Comm(rank, world))
     flags = tsv.VERIFY_SHARD_DENSE if args.shard_mode == "dense" else 0
+    if args.shard_mode == "p2p_fused":  # the race items push their chunk keys (no keys kernel)
+        flags = tsv.VERIFY_P2P_FUSED
     if unsharded:  # the batch's offsets / drafts / ids are inputs, not written by the preceding kernel
         flags = tsv.VERIFY_META_READY
     entry = tsv.lib().tsv_verify_accept_sharded_p2p if p2p else tsv.lib().tsv_verify_accept_sharded
@@ -781,7 +794,8 @@ def run_config4(args, rank, world, local_rank):
         "roofline": {"kernel": "tsv_verify_accept (unsharded, one GPU)" if unsharded else
                      f"tsv_verify_accept_sharded{'_p2p' if p2p else ''} (per rank)", "bound": "hbm",
                      "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": committed_traffic("config4") if unsharded else None,
                      "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),
         "gpu_launches": (3 if (args.shard_mode == "dense" or unsharded) else 5) * steps,
@@ -887,7 +901,7 @@ def run_greedy(args, rank, world, local_rank):
                    "k_max": K_MAX, "parallelism": f"request-sharded x{world}",
                    "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank", "graph_steps": gl},
         "roofline": {"kernel": "tsv_verify_greedy (argmax + emit)", "bound": "hbm", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": committed_traffic("greedy"),
                      "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),
         "gpu_launches": 2 * steps,
@@ -988,7 +1002,8 @@ def run_logits(args, rank, world, local_rank):
                    "global_batch": B * world, "vocab": V, "k_max": K_MAX, "parallelism": f"request-sharded x{world}",
                    "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank", "graph_steps": gl},
         "roofline": {"kernel": "tsv_verify_accept_logits (stats + scan + race + emit)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": committed_traffic("logits"),
                      "alg_bytes_per_launch": vbytes, "launch_us": ms_step * 1e3, "peak_source": peak_src},
         "clocks": sampler.summary(),
         "gpu_launches": 4 * steps,
@@ -1081,7 +1096,7 @@ def run_config5(args, rank, world, local_rank):
                    "parallelism": f"instance-sharded x{world}", "graph_steps": gl,
                    "l2_defeat": "none: latency/ALU-bound, 7.4 MB of inputs stay L2-resident (stated, not hidden)"},
         "roofline": {"kernel": "goodput_choose_k_batched_kernel", "bound": "latency", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": committed_traffic("config5"),
                      "alg_bytes_per_launch": bytes_step, "launch_us": ms_step * 1e3, "peak_source": peak_src,
                      "note": "one CTA per instance (3 waves of 8 CTAs/SM), each a dependent chain: loads, fp64 "
                              "Horner, int64 reductions, argmax, stores; the HBM fraction is reported, not targeted"},

@@ -64,6 +64,8 @@ struct RaceParams {
     int32_t meta_ready;         // TSV_VERIFY_META_READY: the scan reads row_offsets/drafts/rids before its wait
     int32_t race_update;        // lazy race: one extra CTA runs the alpha update (ua) beside the race
     UpdateArgs ua;
+    int32_t push;               // TSV_VERIFY_P2P_FUSED: each race item pushes its chunk key to every rank (pv)
+    P2PView pv;
 };
 
 enum Mode { kLazy = 0, kShard = 1 };
@@ -455,26 +457,32 @@ __device__ __forceinline__ uint32_t smid() {
 }
 #endif
 
-template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false>
+__device__ __forceinline__ uint32_t nctaid_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(r));
+    return r;
+}
+
+template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false, bool PUSH = false>
 __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kernel(const RaceParams P) {
     pdl_wait();  // the scan kernel's ReqMeta / rowT / rowkey are complete and visible
     pdl_launch_dependents();
-    // the update CTA (if any) is CTA 0: launched first, it runs beside the race whatever the number
-    // of waves of race CTAs
+    // the update CTA (if any) is CTA 0, the first launched: it runs beside the race
     const int32_t upd = (MODE == kLazy && P.race_update) ? 1 : 0;
-    const int32_t race_ctas = gridDim.x - upd;
     if (upd && blockIdx.x == 0) {
         update_cta(P.ua);  // the accepted counts are final after the scan; runs beside the race
         return;
     }
     const int lane = threadIdx.x & 31;
     const int32_t warp_id = (blockIdx.x - upd) * kRaceWarps + (threadIdx.x >> 5);
-    const int32_t n_warps = race_ctas * kRaceWarps;
     const int32_t per_req = (MODE == kLazy) ? P.n_chunks : (P.k_max + 1) * P.n_chunks;
     const int32_t n_items = P.B * per_req;
     const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
+    const uint32_t push_e = PUSH ? p2p_load_epoch(P.pv) : 0u;  // this call's epoch (fused push)
 
-    for (int32_t item = warp_id; item < n_items; item += n_warps) {
+    // the stride is re-read from %nctaid at the increment (volatile asm): kept live across the streaming
+    // loop it was spilled to the stack at 64 registers
+    for (int32_t item = warp_id; item < n_items; item += (static_cast<int32_t>(nctaid_x()) - upd) * kRaceWarps) {
         // request-minor order: neighbouring warps (same CTA / SM) race different requests
         const int32_t i = item % P.B;
         const int32_t rem = item / P.B;
@@ -571,7 +579,15 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
         // lazy: the key row (= request i) is recomputed from the item index here rather than kept live
         // across the streaming loop (which spilled it to the stack at 64 registers)
         const int32_t key_row_end = (MODE == kLazy && !LOGITS) ? item - (item / P.B) * P.B : key_row;
-        if (lane == 0 && best) atomicMax(P.rowkey + key_row_end, static_cast<unsigned long long>(best));
+        if (PUSH) {  // fused push: this chunk's key into slot [rank][c][i] of every rank
+            if (lane < P.pv.G) {
+                const int32_t cc = (item / P.B) % P.n_chunks;
+                st_ll(p2p_ckeys(P.pv, push_e, lane, P.pv.rank, cc) + key_row_end,
+                      make_uint4(static_cast<uint32_t>(best), push_e, static_cast<uint32_t>(best >> 32), push_e));
+            }
+        } else if (lane == 0 && best) {
+            atomicMax(P.rowkey + key_row_end, static_cast<unsigned long long>(best));
+        }
 #if TSV_TRACE
         if (lane == 0 && item < kTraceMax) {
             g_trace[item][0] = tr0;
@@ -879,7 +895,9 @@ __global__ void __launch_bounds__(64) p2p_allreduce_i64_kernel(int64_t* data, in
     p2p_allreduce_block(reinterpret_cast<long long*>(data), count, V, devstatus);
 }
 
-__global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams P, const P2PView V) {
+// NC > 0 (fused push): this rank races P.n_chunks <= NC chunks per row; the slots of chunks
+// P.n_chunks .. NC-1 (uneven shards) get an empty key here, so every rank's emit polls NC slots per rank.
+__global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams P, const P2PView V, int32_t NC) {
     pdl_wait();
     pdl_launch_dependents();
     zero_step_counts(P.step_counts);
@@ -891,6 +909,8 @@ __global__ void __launch_bounds__(256) verify_p2p_flags_kernel(const RaceParams 
     if (lane < V.G)  // lane g stores into rank g's buffer
         st_ll(p2p_masks(V, e, lane, V.rank) + i,
               make_uint4(static_cast<uint32_t>(mask), e, static_cast<uint32_t>(mask >> 32), e));
+    for (int32_t idx = lane; idx < V.G * (NC - P.n_chunks); idx += 32)
+        st_ll(p2p_ckeys(V, e, idx % V.G, V.rank, P.n_chunks + idx / V.G) + i, make_uint4(0u, e, 0u, e));
 }
 
 __global__ void __launch_bounds__(256) verify_p2p_meta_kernel(const RaceParams P, const P2PView V) {
@@ -968,6 +988,61 @@ __global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P
             if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
         } else {
             if (key == 0 && rm.m < rm.k) key = fb;
+            emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
+            if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
+            mk = make_int2(rm.m, rm.k);
+        }
+    }
+    if (P.step_counts) add_step_counts(P.step_counts, (threadIdx.x & 31) == 0, mk.x, mk.y);
+    // advance the device epoch once every CTA of this kernel has read it (last CTA, GPU scope)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p2p_counter(V), 1u) == gridDim.x - 1) {
+            atomicExch(p2p_counter(V), 0u);
+            atomicExch(p2p_epoch(V), e);
+        }
+    }
+}
+
+// Fused-push emit (TSV_VERIFY_P2P_FUSED): the race items pushed their chunk keys as LL lines, so
+// request i's warp polls the G x NC lines of its own buffer (lane-strided), takes the max and emits;
+// no keys kernel.  A zero max with m < k means the residual is zero on every rank (R5): every rank's
+// warp for i takes this path together, races max(0, p_m) over its columns, pushes that fallback key
+// as one more LL line and takes the max of the G fallback keys.
+template <bool PRUNE>
+__global__ void __launch_bounds__(256) verify_p2p_emit_push_kernel(const RaceParams P, const P2PView V, int32_t NC) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const uint32_t e = p2p_load_epoch(V);
+    const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    int2 mk = make_int2(-1, 0);
+    if (i < P.B) {
+        const int lane = threadIdx.x & 31;
+        const ReqMeta rm = P.meta[i];  // same m_i on every rank
+        if (rm.ok != 1) {
+            emit(P, i, 0, -1, -1);
+            if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
+        } else {
+            uint64_t key = 0;
+            for (int32_t idx = lane; idx < V.G * NC; idx += 32) {
+                const uint4 v = ld_ll_wait(p2p_ckeys(V, e, V.rank, idx / NC, idx % NC) + i, e, P.devstatus);
+                const uint64_t k = (static_cast<uint64_t>(v.z) << 32) | v.x;
+                key = k > key ? k : key;
+            }
+            key = warp_max_u64(key);
+            if (key == 0 && rm.m < rm.k) {  // R5 on every rank: the fallback race, exchanged as one LL line
+                const uint64_t fb = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
+                if (lane < V.G)
+                    st_ll(p2p_fbkeys(V, e, lane, V.rank) + i,
+                          make_uint4(static_cast<uint32_t>(fb), e, static_cast<uint32_t>(fb >> 32), e));
+                uint64_t f = 0;
+                if (lane < V.G) {
+                    const uint4 v = ld_ll_wait(p2p_fbkeys(V, e, V.rank, lane) + i, e, P.devstatus);
+                    f = (static_cast<uint64_t>(v.z) << 32) | v.x;
+                }
+                key = warp_max_u64(f);
+            }
             emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
             if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
             mk = make_int2(rm.m, rm.k);
@@ -1359,6 +1434,34 @@ static int32_t auto_chunk(const tsv_verify_args* a) {
     return static_cast<int32_t>(c);
 }
 
+// Fused push (TSV_VERIFY_P2P_FUSED): every rank must agree on NC, the number of chunk slots per row
+// and rank, from what all ranks know (vocab_global, the world size, B, the SM count): chunks sized as
+// auto_chunk would for the largest shard ceil4(vocab_global / G), at most kP2PMaxChunks of them.
+// This rank races ceil(vocab / chunk) <= NC chunks (its shard may be smaller).
+static tsv_status p2p_push_chunks(const tsv_verify_args* a, int32_t G, int32_t* chunk, int32_t* NC, int32_t* n_chunks) {
+    const int64_t v_max = ((static_cast<int64_t>(a->vocab_global) + G - 1) / G + 3) / 4 * 4;
+    int64_t c;
+    if (a->chunk > 0) {
+        c = a->chunk;
+    } else {
+        const int64_t warps = static_cast<int64_t>(sm_count()) * 32;
+        const int64_t per_row = std::max<int64_t>(1, warps / std::max<int32_t>(a->B, 1));
+        c = (v_max + per_row - 1) / per_row;
+        c = std::max<int64_t>(512, (c + 127) / 128 * 128);
+    }
+    if ((v_max + c - 1) / c > kP2PMaxChunks) c = ((v_max + kP2PMaxChunks - 1) / kP2PMaxChunks + 127) / 128 * 128;
+    TSV_REQUIRE(c <= kMaxChunk, "tsv_verify p2p fused: chunk %lld > %d", (long long)c, kMaxChunk);
+    const int64_t nc = (v_max + c - 1) / c, mine = (static_cast<int64_t>(a->vocab) + c - 1) / c;
+    TSV_REQUIRE(nc <= kP2PMaxChunks, "tsv_verify p2p fused: %lld chunks per row > %d (use a larger chunk)",
+                (long long)nc, kP2PMaxChunks);
+    TSV_REQUIRE(mine <= nc, "tsv_verify p2p fused: shard of %d columns larger than ceil4(vocab_global / world) = %lld",
+                a->vocab, (long long)v_max);
+    *chunk = static_cast<int32_t>(c);
+    *NC = static_cast<int32_t>(nc);
+    *n_chunks = static_cast<int32_t>(mine);
+    return TSV_OK;
+}
+
 static tsv_status validate(const tsv_verify_args* a) {
     TSV_REQUIRE(a != nullptr, "tsv_verify: args is NULL");
     TSV_REQUIRE(a->B >= 0, "tsv_verify: B < 0 (%d)", a->B);
@@ -1419,6 +1522,8 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.n_chunks = (a->vocab + chunk - 1) / chunk;
     P.race_update = 0;
     P.ua = UpdateArgs{};
+    P.push = 0;
+    P.pv = P2PView{};
     P.meta_ready = (a->flags & TSV_VERIFY_META_READY) ? 1 : 0;
     P.rows_p = a->rows_p;
     const size_t n_chunks = static_cast<size_t>(P.n_chunks);
@@ -1443,9 +1548,9 @@ static int sm_count() {
     return n[dev] > 0 ? n[dev] : 148;
 }
 
-template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false>
+template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false, bool PUSH = false>
 static tsv_status launch_race(const RaceParams& P, cudaStream_t st) {
-    auto kern = verify_race_kernel<MODE, DENSE_Q, PRUNE, LOGITS>;
+    auto kern = verify_race_kernel<MODE, DENSE_Q, PRUNE, LOGITS, PUSH>;
     static int occ = 0;  // resident CTAs per SM
     if (!occ) {
         int b = 0;
@@ -1968,17 +2073,32 @@ extern "C" tsv_status tsv_verify_shard_p2p_phase(const tsv_verify_args* a, tsv_p
     const dim3 grid(static_cast<unsigned>((a->B + 7) / 8));
     const P2PView V = p->view;
     const bool prune = !(a->flags & TSV_VERIFY_NO_PRUNE);
+    const bool fused = (a->flags & TSV_VERIFY_P2P_FUSED) != 0;
+    int32_t NC = 0;  // fused: chunks per row polled per rank, identical on every rank
+    if (fused) TSV_TRY(p2p_push_chunks(a, V.G, &P.chunk, &NC, &P.n_chunks));
     if (phase == 0) {
-        TSV_CUDA(launch_pdl(verify_p2p_flags_kernel, grid, dim3(256), 0, st, P, V), "verify_p2p_flags_kernel launch");
+        TSV_CUDA(launch_pdl(verify_p2p_flags_kernel, grid, dim3(256), 0, st, P, V, NC), "verify_p2p_flags_kernel launch");
     } else if (phase == 1) {
         TSV_CUDA(launch_pdl(verify_p2p_meta_kernel, grid, dim3(256), 0, st, P, V), "verify_p2p_meta_kernel launch");
         tsv_status rs;
-        if (a->q) rs = prune ? launch_race<kLazy, true, true>(P, st) : launch_race<kLazy, true, false>(P, st);
-        else rs = prune ? launch_race<kLazy, false, true>(P, st) : launch_race<kLazy, false, false>(P, st);
+        if (fused) {
+            P.push = 1;
+            P.pv = V;
+            if (a->q) rs = prune ? launch_race<kLazy, true, true, false, true>(P, st) : launch_race<kLazy, true, false, false, true>(P, st);
+            else rs = prune ? launch_race<kLazy, false, true, false, true>(P, st) : launch_race<kLazy, false, false, false, true>(P, st);
+        } else {
+            if (a->q) rs = prune ? launch_race<kLazy, true, true>(P, st) : launch_race<kLazy, true, false>(P, st);
+            else rs = prune ? launch_race<kLazy, false, true>(P, st) : launch_race<kLazy, false, false>(P, st);
+        }
         TSV_TRY(rs);
-        TSV_CUDA(prune ? launch_pdl(verify_p2p_keys_kernel<true>, grid, dim3(256), 0, st, P, V)
-                       : launch_pdl(verify_p2p_keys_kernel<false>, grid, dim3(256), 0, st, P, V),
-                 "verify_p2p_keys_kernel launch");
+        if (!fused)
+            TSV_CUDA(prune ? launch_pdl(verify_p2p_keys_kernel<true>, grid, dim3(256), 0, st, P, V)
+                           : launch_pdl(verify_p2p_keys_kernel<false>, grid, dim3(256), 0, st, P, V),
+                     "verify_p2p_keys_kernel launch");
+    } else if (fused) {
+        TSV_CUDA(prune ? launch_pdl(verify_p2p_emit_push_kernel<true>, grid, dim3(256), 0, st, P, V, NC)
+                       : launch_pdl(verify_p2p_emit_push_kernel<false>, grid, dim3(256), 0, st, P, V, NC),
+                 "verify_p2p_emit_push_kernel launch");
     } else {
         TSV_CUDA(launch_pdl(verify_p2p_emit_kernel, grid, dim3(256), 0, st, P, V), "verify_p2p_emit_kernel launch");
     }

@@ -38,9 +38,10 @@ def main():
     out = torch.empty((B, vb.k_max + 1), dtype=torch.int32, device=dev)
     st = torch.zeros(1, dtype=torch.int32, device=dev)
     ok = True
-    for step in range(4):
+    for step in range(8):  # steps 0-3: LL keys kernel; steps 4-7: keys pushed by the race items (P2P_FUSED)
+        fl = tsv.VERIFY_P2P_FUSED if step >= 4 else 0
         a = tsv.make_verify_args(p, q, g.row_offsets, g.draft_tokens, g.request_ids, 31, step, vb.k_max, na, out,
-                                 device_status=st, vocab=Vs, vocab_offset=lo, vocab_global=V)
+                                 device_status=st, vocab=Vs, vocab_offset=lo, vocab_global=V, flags=fl)
         ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), dev)
         a.workspace = ws.data_ptr()
         a.workspace_bytes = ws.numel()

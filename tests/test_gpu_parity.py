@@ -297,27 +297,30 @@ def test_lazy_vocab_shard_one_hot_and_adversarial(tsv):
         assert (na == ona).all() and (out == oout).all()
 
 
-def p2p_shard_loopback(tsv, vb, G, seed, steps, chunk=0, B_max=None):
+def p2p_shard_loopback(tsv, vb, G, seed, steps, chunk=0, B_max=None, flags=0, bounds=None):
     """Lazy two rounds over peer memory (tsv_verify_shard_p2p_phase), G virtual ranks on one device:
-    all ranks phase 0, then phase 1, then phase 2, for each step; every rank's outputs are returned."""
+    all ranks phase 0, then phase 1, then phase 2, for each step; every rank's outputs are returned.
+    flags: e.g. VERIFY_P2P_FUSED (the race items push their chunk keys; no keys kernel).
+    bounds: explicit shard column boundaries [0, ..., V] (default: G equal shards)."""
     g = vb.to(DEV)
     B, V = vb.B, vb.vocab
-    assert V % (4 * G) == 0
-    Vs = V // G
+    if bounds is None:
+        assert V % (4 * G) == 0
+        bounds = [s * (V // G) for s in range(G)] + [V]
     lb = tsv.P2PLoopback(G, B_max or max(B, 1))
     res = []
     try:
         for step in steps:
             outs, args = [], []
             for s in range(G):
-                lo = s * Vs
+                lo, Vs = bounds[s], bounds[s + 1] - bounds[s]
                 na = torch.full((B,), -7, dtype=torch.int32, device=DEV)
                 out = torch.full((B, vb.k_max + 1), -7, dtype=torch.int32, device=DEV)
                 st = torch.zeros(1, dtype=torch.int32, device=DEV)
                 a = tsv.make_verify_args(g.p[:, lo:lo + Vs], None if g.q is None else g.q[:, lo:lo + Vs],
                                          g.row_offsets, g.draft_tokens, g.request_ids, seed, step, vb.k_max,
                                          na, out, device_status=st, vocab=Vs, vocab_offset=lo, vocab_global=V,
-                                         chunk=chunk)
+                                         chunk=chunk, flags=flags)
                 ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
                 a.workspace = ws.data_ptr()
                 a.workspace_bytes = ws.numel()
@@ -333,39 +336,57 @@ def p2p_shard_loopback(tsv, vb, G, seed, steps, chunk=0, B_max=None):
     return res
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-def test_p2p_vocab_shard_loopback_equals_oracle(tsv, G):
+def test_p2p_vocab_shard_loopback_equals_oracle(tsv, G, fused):
     # three consecutive calls: both slot parities and advancing epochs
     vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=26)
-    res = p2p_shard_loopback(tsv, vb, G, 21, [3, 4, 5], B_max=80)
+    res = p2p_shard_loopback(tsv, vb, G, 21, [3, 4, 5], B_max=80, flags=tsv.VERIFY_P2P_FUSED if fused else 0)
     for step, ranks in zip([3, 4, 5], res):
         ona, oout, ost = oracle_verify(vb, 21, step)
         for na, out, st in ranks:
             assert (na == ona).all() and (out == oout).all() and st == ost
 
 
-def test_p2p_vocab_shard_one_hot_adversarial_llama3(tsv):
+@pytest.mark.parametrize("fused", [False, True])
+def test_p2p_vocab_shard_one_hot_adversarial_llama3(tsv, fused):
+    fl = tsv.VERIFY_P2P_FUSED if fused else 0
     vb = synth.make_verify_batch(B=40, V=4096, k_max=6, lam=0.7, seed=27, dense_q=False)
     ona, oout, _ = oracle_verify(vb, 2, 2)
     for G in (2, 4):
-        for na, out, st in p2p_shard_loopback(tsv, vb, G, 2, [2], chunk=1024)[0]:
+        for na, out, st in p2p_shard_loopback(tsv, vb, G, 2, [2], chunk=1024, flags=fl)[0]:
             assert (na == ona).all() and (out == oout).all()
-    adv = _adversarial_batch()
+    adv = _adversarial_batch()  # includes p == q rows: a residual zero on every rank (R5 fallback path)
     adv.vocab = 256
     adv.p = adv.p[:, :256].contiguous(); adv.q = adv.q[:, :256].contiguous()
     adv.draft_tokens = adv.draft_tokens.clamp(max=255)
-    res = p2p_shard_loopback(tsv, adv, 4, 4, [0, 1, 2, 3])
+    res = p2p_shard_loopback(tsv, adv, 4, 4, [0, 1, 2, 3], flags=fl)
     for step, ranks in enumerate(res):
         ona, oout, ost = oracle_verify(adv, 4, step)
         for na, out, st in ranks:
             assert (na == ona).all() and (out == oout).all() and st == ost
     vb3 = synth.make_verify_batch(B=24, V=128256, k_max=8, lam=0.7, seed=28)  # Llama-3 vocabulary, G = 8
     ona, oout, _ = oracle_verify(vb3, 9, 1)
-    for na, out, st in p2p_shard_loopback(tsv, vb3, 8, 9, [1])[0]:
+    for na, out, st in p2p_shard_loopback(tsv, vb3, 8, 9, [1], flags=fl)[0]:
         assert (na == ona).all() and (out == oout).all()
 
 
-def test_p2p_graph_replay_advances_epochs(tsv):
+def test_p2p_fused_uneven_shards(tsv):
+    # fused push with shards of 2052 and 2048 columns (V = 4100), chunk 512: every rank polls
+    # NC = 5 chunk slots per rank; rank 1 races only 4 chunks and its flags kernel fills the fifth slot
+    vb = synth.make_verify_batch(B=30, V=4100, k_max=8, lam=0.6, seed=33)
+    res = p2p_shard_loopback(tsv, vb, 2, 5, [0, 1, 2], chunk=512, flags=tsv.VERIFY_P2P_FUSED, bounds=[0, 2052, 4100])
+    for step, ranks in enumerate(res):
+        ona, oout, ost = oracle_verify(vb, 5, step)
+        for na, out, st in ranks:
+            assert (na == ona).all() and (out == oout).all() and st == ost
+    # a shard larger than ceil4(vocab_global / world) is refused on the host
+    with pytest.raises(RuntimeError):
+        p2p_shard_loopback(tsv, vb, 2, 5, [0], chunk=512, flags=tsv.VERIFY_P2P_FUSED, bounds=[0, 2100, 4100])
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_p2p_graph_replay_advances_epochs(tsv, fused):
     # the call epoch lives on the device: a captured graph of 3 calls replayed twice stays correct
     vb = synth.make_verify_batch(B=32, V=8192, k_max=8, lam=0.7, seed=30)
     g = vb.to(DEV)
@@ -377,7 +398,8 @@ def test_p2p_graph_replay_advances_epochs(tsv):
             na = torch.empty(vb.B, dtype=torch.int32, device=DEV)
             out = torch.full((vb.B, vb.k_max + 1), -7, dtype=torch.int32, device=DEV)
             a = tsv.make_verify_args(g.p, g.q, g.row_offsets, g.draft_tokens, g.request_ids, 8, step, vb.k_max,
-                                     na, out, vocab=vb.vocab, vocab_global=vb.vocab)
+                                     na, out, vocab=vb.vocab, vocab_global=vb.vocab,
+                                     flags=tsv.VERIFY_P2P_FUSED if fused else 0)
             ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
             a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
             args.append((a, ws))
