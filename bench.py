@@ -1387,7 +1387,8 @@ def main():
         plan = [("strong", run_strong, {})] if world > 1 else []
         plan += [("config4", run_config4, {"shard_mode": "auto"})]
         if world == 1:
-            plan += [("config4_sharded_p2p", run_config4, {"shard_mode": "p2p"})]
+            plan += [("config4_sharded_p2p", run_config4, {"shard_mode": "p2p"}),
+                     ("config4_sharded_p2p_fused", run_config4, {"shard_mode": "p2p_fused"})]
         plan += [("greedy", run_greedy, {}), ("logits", run_logits, {}), ("config5", run_config5, {}),
                  ("loop", run_loop, {})]
         for name, fn, over in plan:

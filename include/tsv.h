@@ -203,8 +203,9 @@ typedef struct tsv_verify_args {
 #define TSV_VERIFY_P2P_FUSED 16   /* tsv_verify_accept_sharded_p2p / _phase: the race */
                                   /* kernel's work items push their chunk keys to     */
                                   /* every rank themselves (LL lines, no keys kernel);*/
-                                  /* every rank must pass it; needs each shard <=     */
-                                  /* ceil4(vocab_global / world) columns              */
+                                  /* every rank must pass it; each shard must fit the */
+                                  /* NC chunk slots sized for ceil4(vocab_global /    */
+                                  /* world) columns (INVALID_ARG otherwise)           */
 #define TSV_VERIFY_META_READY 8   /* Contract: row_offsets, draft_tokens and          */
                                   /* request_ids are COMPLETE before the kernel that  */
                                   /* immediately precedes this call on the stream     */

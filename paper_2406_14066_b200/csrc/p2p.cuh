@@ -33,13 +33,12 @@ __host__ __device__ constexpr size_t p2p_masks_bytes(int32_t B_max) {
 constexpr size_t kP2PSumsBytes = 2ull * TSV_P2P_MAX_WORLD * TSV_P2P_MAX_SUMS * 16ull;  // [2][W][n] LL lines
 // Fused push (TSV_VERIFY_P2P_FUSED): every race work item (request i, chunk c) of rank `from` pushes its
 // chunk key as one LL line into slot [from][c][i] of every peer; [2][W][kP2PMaxChunks][B_max] lines.
-// Then the rare R5 fallback keys: [2][W][B_max] lines.
 constexpr int32_t kP2PMaxChunks = 32;
 __host__ __device__ constexpr size_t p2p_ckeys_bytes(int32_t B_max) {
     return 2ull * TSV_P2P_MAX_WORLD * kP2PMaxChunks * static_cast<size_t>(B_max) * 16ull;
 }
 __host__ __device__ constexpr size_t p2p_buffer_bytes(int32_t B_max) {
-    return kP2PHdr + 3ull * p2p_masks_bytes(B_max) + kP2PSumsBytes + p2p_ckeys_bytes(B_max) + p2p_masks_bytes(B_max);
+    return kP2PHdr + 3ull * p2p_masks_bytes(B_max) + kP2PSumsBytes + p2p_ckeys_bytes(B_max);
 }
 __device__ __forceinline__ uint32_t* p2p_epoch(const P2PView& V) {
     return reinterpret_cast<uint32_t*>(V.buf[V.rank]);
@@ -68,11 +67,6 @@ __device__ __forceinline__ uint4* p2p_sums(const P2PView& V, uint32_t e, int32_t
 __device__ __forceinline__ uint4* p2p_ckeys(const P2PView& V, uint32_t e, int32_t owner, int32_t from, int32_t c) {
     return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr + 3ull * p2p_masks_bytes(V.B_max) + kP2PSumsBytes) +
            ((static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + from) * kP2PMaxChunks + c) * V.B_max;
-}
-__device__ __forceinline__ uint4* p2p_fbkeys(const P2PView& V, uint32_t e, int32_t owner, int32_t from) {
-    return reinterpret_cast<uint4*>(V.buf[owner] + kP2PHdr + 3ull * p2p_masks_bytes(V.B_max) + kP2PSumsBytes +
-                                    p2p_ckeys_bytes(V.B_max)) +
-           (static_cast<size_t>(e & 1u) * TSV_P2P_MAX_WORLD + from) * V.B_max;
 }
 __device__ __forceinline__ void st_ll(uint4* p, uint4 v) {
     asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)

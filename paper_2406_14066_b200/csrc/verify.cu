@@ -38,7 +38,7 @@ namespace tsv {
 struct ReqMeta {           // 32 bytes, written by the scan kernel
     int32_t r0, k, qbase, m;
     int32_t xm, ok;        // ok: 1 valid, 0 bad k, 2 bad draft token
-    uint32_t rid, pad;
+    uint32_t rid, pad;     // pad: the call's epoch in the p2p modes (0 otherwise)
 };
 
 struct RaceParams {
@@ -416,6 +416,37 @@ __device__ __forceinline__ void update_cta(const UpdateArgs& A) {
     }
 }
 
+// One warp races max(0, p) over local columns [c0, c1) of the row at prow (c0 % 4 == 0): the R5
+// fallback (emit kernels; the fused-push race epilogue for its chunk).  Returns the packed key (0: no
+// positive weight).
+template <bool PRUNE, bool LOGITS = false>
+__device__ __forceinline__ uint64_t warp_race_cols(const RaceParams& P, const float* prow, int32_t c0, int32_t c1,
+                                                int32_t sel, uint32_t rid, float M = 0.f, float inv_S = 0.f) {
+    const RaceCtr rc = race_ctr((kPurposeRace << 16) | static_cast<uint32_t>(sel), rid, P.step, P.k0, P.k1);
+    const int lane = threadIdx.x & 31;
+    const float4* p4 = reinterpret_cast<const float4*>(prow);
+    const int32_t q1 = (c1 + 3) >> 2;
+    const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
+    Race F;
+    F.init();
+    for (int32_t f0 = c0 >> 2; f0 < q1; f0 += 32) {
+        const int32_t f = f0 + lane;
+        const int32_t col = 4 * f;
+        float w[4] = {0.f, 0.f, 0.f, 0.f};
+        uint4 r = make_uint4(0, 0, 0, 0);
+        if (f < q1) {
+            float4 a = p4[f];
+            if (LOGITS) a = to_prob4(a, M, inv_S, P.inv_tau);
+            quad_weights<true>(w, a, a, false, col, c1, -1);
+            r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(f), P);
+        }
+        F.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
+        if (PRUNE) F.sync_T();
+    }
+    F.finish<PRUNE>(F.T);
+    return warp_max_u64(F.best);
+}
+
 // ------------------------------------------------------------------ 2. the race
 // Warp-independent: every warp races work items -- (request [, position], chunk of P.chunk
 // columns) -- interleaved over all warps of the grid so residual (p and q) and bonus (p
@@ -478,7 +509,6 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
     const int32_t per_req = (MODE == kLazy) ? P.n_chunks : (P.k_max + 1) * P.n_chunks;
     const int32_t n_items = P.B * per_req;
     const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
-    const uint32_t push_e = PUSH ? p2p_load_epoch(P.pv) : 0u;  // this call's epoch (fused push)
 
     // the stride is re-read from %nctaid at the increment (volatile asm): kept live across the streaming
     // loop it was spilled to the stack at 64 registers
@@ -580,10 +610,25 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
         // across the streaming loop (which spilled it to the stack at 64 registers)
         const int32_t key_row_end = (MODE == kLazy && !LOGITS) ? item - (item / P.B) * P.B : key_row;
         if (PUSH) {  // fused push: this chunk's key into slot [rank][c][i] of every rank
+            uint64_t push = best;
+            const int32_t cc = (item / P.B) % P.n_chunks;
+            if (best == 0) {  // (rare; warp-uniform) the request's meta is reloaded, nothing kept live
+                const ReqMeta r2 = P.meta[key_row_end];
+                if (r2.m < r2.k) {
+                    // no positive residual in this chunk: push its share of the R5 fallback instead (max(0,
+                    // p_m) over the chunk), flagged in bit 63 (never set in a race key: scores are >= 0)
+                    const int32_t cb = cc * P.chunk;
+                    const uint64_t fb = warp_race_cols<PRUNE>(P, P.p + static_cast<int64_t>(r2.r0 + r2.m) * P.ld, cb,
+                                                              min(P.vocab, cb + P.chunk), r2.m, r2.rid);
+                    push = fb ? (fb | (1ull << 63)) : 0ull;
+                }
+            }
             if (lane < P.pv.G) {
-                const int32_t cc = (item / P.B) % P.n_chunks;
+                // this call's epoch (written into the request's meta by the p2p meta kernel), reloaded here
+                // rather than kept live across the streaming loop
+                const uint32_t push_e = __ldg(&P.meta[key_row_end].pad);
                 st_ll(p2p_ckeys(P.pv, push_e, lane, P.pv.rank, cc) + key_row_end,
-                      make_uint4(static_cast<uint32_t>(best), push_e, static_cast<uint32_t>(best >> 32), push_e));
+                      make_uint4(static_cast<uint32_t>(push), push_e, static_cast<uint32_t>(push >> 32), push_e));
             }
         } else if (lane == 0 && best) {
             atomicMax(P.rowkey + key_row_end, static_cast<unsigned long long>(best));
@@ -608,29 +653,7 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
 template <bool PRUNE, bool LOGITS = false>
 __device__ uint64_t warp_race_row(const RaceParams& P, const float* prow, int32_t sel, uint32_t rid,
                                   float M = 0.f, float inv_S = 0.f) {
-    const RaceCtr rc = race_ctr((kPurposeRace << 16) | static_cast<uint32_t>(sel), rid, P.step, P.k0, P.k1);
-    const int lane = threadIdx.x & 31;
-    const float4* p4 = reinterpret_cast<const float4*>(prow);
-    const int32_t nq = (P.vocab + 3) >> 2;
-    const uint32_t vbase = static_cast<uint32_t>(P.vocab_offset);
-    Race F;
-    F.init();
-    for (int32_t f0 = 0; f0 < nq; f0 += 32) {
-        const int32_t f = f0 + lane;
-        const int32_t col = 4 * f;
-        float w[4] = {0.f, 0.f, 0.f, 0.f};
-        uint4 r = make_uint4(0, 0, 0, 0);
-        if (f < nq) {
-            float4 a = p4[f];
-            if (LOGITS) a = to_prob4(a, M, inv_S, P.inv_tau);
-            quad_weights<true>(w, a, a, false, col, P.vocab, -1);
-            r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(f), P);
-        }
-        F.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
-        if (PRUNE) F.sync_T();
-    }
-    F.finish<PRUNE>(F.T);
-    return warp_max_u64(F.best);
+    return warp_race_cols<PRUNE, LOGITS>(P, prow, 0, P.vocab, sel, rid, M, inv_S);
 }
 
 template <int MODE, bool PRUNE, bool LOGITS = false>
@@ -928,7 +951,8 @@ __global__ void __launch_bounds__(256) verify_p2p_meta_kernel(const RaceParams P
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) mask += __shfl_xor_sync(0xFFFFFFFFu, mask, o);  // lanes 0..7
     mask = __shfl_sync(0xFFFFFFFFu, mask, 0);
-    const ReqMeta rm = shard_meta_from_masks(P, i, mask);
+    ReqMeta rm = shard_meta_from_masks(P, i, mask);
+    rm.pad = e;  // the call's epoch, for the fused-push race items (no epoch load in the race kernel)
     if (lane == 0) {
         P.meta[i] = rm;
         P.rowT[i] = 0u;
@@ -1007,9 +1031,9 @@ __global__ void __launch_bounds__(256) verify_p2p_emit_kernel(const RaceParams P
 
 // Fused-push emit (TSV_VERIFY_P2P_FUSED): the race items pushed their chunk keys as LL lines, so
 // request i's warp polls the G x NC lines of its own buffer (lane-strided), takes the max and emits;
-// no keys kernel.  A zero max with m < k means the residual is zero on every rank (R5): every rank's
-// warp for i takes this path together, races max(0, p_m) over its columns, pushes that fallback key
-// as one more LL line and takes the max of the G fallback keys.
+// no keys kernel.  A race item whose chunk has no positive residual pushed its chunk's share of the R5
+// fallback instead, flagged in bit 63: the max of the flagged keys is used only when every chunk of
+// every rank had a zero residual (R5), exactly the fallback of the unsharded verify.
 template <bool PRUNE>
 __global__ void __launch_bounds__(256) verify_p2p_emit_push_kernel(const RaceParams P, const P2PView V, int32_t NC) {
     pdl_wait();
@@ -1024,25 +1048,20 @@ __global__ void __launch_bounds__(256) verify_p2p_emit_push_kernel(const RacePar
             emit(P, i, 0, -1, -1);
             if (lane == 0) report(P.devstatus, rm.ok == 2 ? TSV_DEVSTATUS_BAD_TOKEN : TSV_DEVSTATUS_BAD_K);
         } else {
-            uint64_t key = 0;
+            uint64_t key = 0, fb = 0;  // max race key; max flagged chunk fallback key (bit 63)
             for (int32_t idx = lane; idx < V.G * NC; idx += 32) {
                 const uint4 v = ld_ll_wait(p2p_ckeys(V, e, V.rank, idx / NC, idx % NC) + i, e, P.devstatus);
                 const uint64_t k = (static_cast<uint64_t>(v.z) << 32) | v.x;
-                key = k > key ? k : key;
+                if (k >> 63) {
+                    const uint64_t f = k & ~(1ull << 63);
+                    fb = f > fb ? f : fb;
+                } else {
+                    key = k > key ? k : key;
+                }
             }
             key = warp_max_u64(key);
-            if (key == 0 && rm.m < rm.k) {  // R5 on every rank: the fallback race, exchanged as one LL line
-                const uint64_t fb = warp_race_row<PRUNE>(P, P.p + static_cast<int64_t>(rm.r0 + rm.m) * P.ld, rm.m, rm.rid);
-                if (lane < V.G)
-                    st_ll(p2p_fbkeys(V, e, lane, V.rank) + i,
-                          make_uint4(static_cast<uint32_t>(fb), e, static_cast<uint32_t>(fb >> 32), e));
-                uint64_t f = 0;
-                if (lane < V.G) {
-                    const uint4 v = ld_ll_wait(p2p_fbkeys(V, e, V.rank, lane) + i, e, P.devstatus);
-                    f = (static_cast<uint64_t>(v.z) << 32) | v.x;
-                }
-                key = warp_max_u64(f);
-            }
+            fb = warp_max_u64(fb);
+            if (key == 0 && rm.m < rm.k) key = fb;  // R5: the residual is zero on every rank
             emit(P, i, rm.qbase, rm.m, key ? key_index(key) : -1);
             if (lane == 0 && !key) report(P.devstatus, TSV_DEVSTATUS_NO_WEIGHT);
             mk = make_int2(rm.m, rm.k);
@@ -1454,8 +1473,9 @@ static tsv_status p2p_push_chunks(const tsv_verify_args* a, int32_t G, int32_t* 
     const int64_t nc = (v_max + c - 1) / c, mine = (static_cast<int64_t>(a->vocab) + c - 1) / c;
     TSV_REQUIRE(nc <= kP2PMaxChunks, "tsv_verify p2p fused: %lld chunks per row > %d (use a larger chunk)",
                 (long long)nc, kP2PMaxChunks);
-    TSV_REQUIRE(mine <= nc, "tsv_verify p2p fused: shard of %d columns larger than ceil4(vocab_global / world) = %lld",
-                a->vocab, (long long)v_max);
+    TSV_REQUIRE(mine <= nc, "tsv_verify p2p fused: shard of %d columns needs %lld chunks of %lld > NC = %lld "
+                "(shards up to about ceil4(vocab_global / world) = %lld columns)", a->vocab, (long long)mine,
+                (long long)c, (long long)nc, (long long)v_max);
     *chunk = static_cast<int32_t>(c);
     *NC = static_cast<int32_t>(nc);
     *n_chunks = static_cast<int32_t>(mine);

@@ -380,9 +380,9 @@ def test_p2p_fused_uneven_shards(tsv):
         ona, oout, ost = oracle_verify(vb, 5, step)
         for na, out, st in ranks:
             assert (na == ona).all() and (out == oout).all() and st == ost
-    # a shard larger than ceil4(vocab_global / world) is refused on the host
+    # a shard needing more chunks than NC = ceil(ceil4(vocab_global / world) / chunk) is refused on the host
     with pytest.raises(RuntimeError):
-        p2p_shard_loopback(tsv, vb, 2, 5, [0], chunk=512, flags=tsv.VERIFY_P2P_FUSED, bounds=[0, 2100, 4100])
+        p2p_shard_loopback(tsv, vb, 2, 5, [0], chunk=512, flags=tsv.VERIFY_P2P_FUSED, bounds=[0, 2600, 4100])
 
 
 @pytest.mark.parametrize("fused", [False, True])
