@@ -361,7 +361,13 @@ def make_comm(args, rank, world, B_max):
     from paper_2406_14066_b200 import tsv
     if args.comm == "nccl" and not SHARED_GPU:
         return tsv.Comm(rank, world)
-    return tsv.P2PComm(rank, world, B_max=B_max)
+    try:
+        return tsv.P2PComm(rank, world, B_max=B_max)
+    except tsv.TsvError as e:  # every rank raises together (P2PComm agrees on the outcome)
+        if SHARED_GPU:
+            raise
+        print(f"[bench] peer-memory exchange unavailable ({e}); using NCCL", file=sys.stderr)
+        return tsv.Comm(rank, world)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -688,7 +694,18 @@ def run_config4(args, rank, world, local_rank):
         raise SystemExit("--shard-mode none is the one-GPU (unsharded) call")
     p2p = args.shard_mode in ("p2p", "p2p_fused")
     unsharded = args.shard_mode == "none"
-    comm = None if unsharded else (tsv.P2PComm(rank, world, B_max=B) if p2p else tsv.Comm(rank, world))
+    comm = None
+    if not unsharded and p2p:
+        try:
+            comm = tsv.P2PComm(rank, world, B_max=B)
+        except tsv.TsvError as e:  # every rank raises together: fall back to the NCCL lazy mode
+            if SHARED_GPU:
+                raise
+            print(f"[bench] peer-memory exchange unavailable ({e}); config 4 uses the NCCL lazy mode", file=sys.stderr)
+            p2p = False
+            args.shard_mode = "lazy"
+    if not unsharded and not p2p:
+        comm = tsv.Comm(rank, world)
     flags = tsv.VERIFY_SHARD_DENSE if args.shard_mode == "dense" else 0
     if args.shard_mode == "p2p_fused":  # the race items push their chunk keys (no keys kernel)
         flags = tsv.VERIFY_P2P_FUSED

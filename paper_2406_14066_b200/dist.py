@@ -60,6 +60,16 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def min_over_ranks(value: float, device=None, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return float(t.item())
+
+
 def sum_over_ranks(value: float, device=None) -> float:
     import torch
     import torch.distributed as dist

@@ -612,22 +612,35 @@ class P2PComm:
         from . import dist as pdist
         handles = pdist.exchange_handles(bytes(hnd), self.rank, self.world, group)
         self.opened = []
+        self.handle = None
         bufs = (ctypes.c_void_p * self.world)()
-        for g, h in enumerate(handles):
-            if g == self.rank:
-                bufs[g] = own.value
-                continue
-            raw = (ctypes.c_uint8 * 64).from_buffer_copy(h)
-            ptr = ctypes.c_void_p()
-            _check(_lib.tsv_p2p_open(ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(ptr)))
-            self.opened.append(ptr)
-            bufs[g] = ptr.value
-        h = ctypes.c_void_p()
-        _check(_lib.tsv_p2p_init(ctypes.byref(h), self.rank, self.world, self.B_max,
-                                 ctypes.cast(bufs, ctypes.c_void_p)))
-        self.handle = h
-        if dist.is_initialized() and self.world > 1:
-            dist.barrier(group=group)  # every peer mapped before anyone's first store
+        err = None
+        try:
+            for g, h in enumerate(handles):
+                if g == self.rank:
+                    bufs[g] = own.value
+                    continue
+                raw = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+                ptr = ctypes.c_void_p()
+                _check(_lib.tsv_p2p_open(ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(ptr)))
+                self.opened.append(ptr)
+                bufs[g] = ptr.value
+            h = ctypes.c_void_p()
+            _check(_lib.tsv_p2p_init(ctypes.byref(h), self.rank, self.world, self.B_max,
+                                     ctypes.cast(bufs, ctypes.c_void_p)))
+            self.handle = h
+        except TsvError as e:  # e.g. no peer access between these GPUs
+            err = e
+        # every rank learns whether every rank mapped its peers (this all-reduce also orders every
+        # mapping before anyone's first store), so all ranks fail -- or proceed -- together
+        if self.world > 1 and dist.is_initialized():
+            dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else None
+            ok = pdist.min_over_ranks(0.0 if err else 1.0, device=dev, group=group)
+        else:
+            ok = 0.0 if err else 1.0
+        if ok < 1.0:
+            self.close()
+            raise TsvError(2, f"P2PComm: peer mapping failed on some rank ({err or 'another rank'})")
 
     def close(self):
         if self.handle:
