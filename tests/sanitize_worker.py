@@ -62,7 +62,15 @@ def path_step():
     assert (_np(st.num_accepted) == ona).all() and (_np(st.out_tokens) == oout).all()
     want = oracle.update(0.7, ona, _np(vb.row_offsets), decay=0.9)
     assert float(st.alpha.item()) == want
-    # the same step as a CUDA graph (PDL edges inside the graph)
+    # the same step as a CUDA graph (PDL edges inside the graph; the fused lookup + choose-k with
+    # TSV_LOOKUP_INPUTS_READY in a second step object)
+    stf = SpecStep(inp, device=DEV, fused=True)
+    stf.capture([6, 7])
+    stf.reset_state()
+    stf.replay()
+    torch.cuda.synchronize()
+    ona7, oout7, _ = _oracle_verify(vb, synth.DEFAULT_SEED, 7)
+    assert (_np(stf.num_accepted) == ona7).all() and (_np(stf.out_tokens) == oout7).all()
     st.capture([6, 7])
     st.reset_state()
     st.replay()
@@ -78,9 +86,10 @@ def path_step():
     counter = tsv.lookup_choose_scratch(DEV)
     ctx_len = torch.tensor(np.diff(o3).astype(np.int32), device=DEV)
     alpha = torch.tensor([0.7], dtype=torch.float64, device=DEV)
-    for _ in range(2):
+    for rep in range(4):  # reps 2-3: TSV_LOOKUP_INPUTS_READY (everything before the grid-dependency wait)
         _, pl2, k2, _ = tsv.tsv_propose_lookup_choose_k(torch.tensor(c3, device=DEV), torch.tensor(o3, device=DEV),
-                                                        1, 4, 5, alpha, ctx_len, synth.SPEC_DESK_TARGET, 0.05, counter)
+                                                        1, 4, 5, alpha, ctx_len, synth.SPEC_DESK_TARGET, 0.05, counter,
+                                                        flags=tsv.LOOKUP_INPUTS_READY if rep >= 2 else 0)
         torch.cuda.synchronize()
         ok3, _ = oracle.choose_k(0.7, np.diff(o3).astype(np.int32), opl3, 5, oracle.POLICY_PLD,
                                  synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT, pld_cost_ms=0.05)
@@ -94,7 +103,8 @@ def path_p2p():
     G, Vs = 2, 2048
     lb = tsv.P2PLoopback(G, 16)
     try:
-        for step in (3, 4, 5):  # both slot parities, advancing epochs
+        for step in (3, 4, 5, 6, 7):  # both slot parities, advancing epochs; steps 6-7: keys pushed by the race
+            fl = tsv.VERIFY_P2P_FUSED if step >= 6 else 0
             outs, args = [], []
             for s in range(G):
                 lo = s * Vs
@@ -103,7 +113,7 @@ def path_p2p():
                 stt = torch.zeros(1, dtype=torch.int32, device=DEV)
                 a = tsv.make_verify_args(g.p[:, lo:lo + Vs], g.q[:, lo:lo + Vs], g.row_offsets, g.draft_tokens,
                                          g.request_ids, 21, step, vb.k_max, na, out, device_status=stt, vocab=Vs,
-                                         vocab_offset=lo, vocab_global=vb.vocab)
+                                         vocab_offset=lo, vocab_global=vb.vocab, flags=fl)
                 ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
                 a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
                 args.append((a, ws))

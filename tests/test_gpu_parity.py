@@ -371,6 +371,18 @@ def test_p2p_vocab_shard_one_hot_adversarial_llama3(tsv, fused):
         assert (na == ona).all() and (out == oout).all()
 
 
+@pytest.mark.slow
+def test_config4_full_size_unsharded_and_p2p_g8(tsv):
+    # BASELINE config 4 at its full size (B = 256, k in 0..8, V = 128256): the unsharded call (with
+    # TSV_VERIFY_META_READY, as the bench times it) and eight loopback vocab shards over peer memory,
+    # LL keys kernel and fused push, every request equal to the oracle
+    vb = synth.make_verify_batch(B=256, V=128256, k_max=8, lam=0.7, seed=240614066)
+    ona, oout = assert_verify_parity(tsv, vb, 240614066, 0, flags=tsv.VERIFY_META_READY)
+    for fl in (0, tsv.VERIFY_P2P_FUSED):
+        for na, out, st in p2p_shard_loopback(tsv, vb, 8, 240614066, [0], flags=fl)[0]:
+            assert (na == ona).all() and (out == oout).all() and st == 0
+
+
 def test_p2p_fused_uneven_shards(tsv):
     # fused push with shards of 2052 and 2048 columns (V = 4100), chunk 512: every rank polls
     # NC = 5 chunk slots per rank; rank 1 races only 4 chunks and its flags kernel fills the fifth slot
