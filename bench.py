@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
     ap.add_argument("--no-lookup-ready", action="store_true",
                     help="launch the lookup without TSV_LOOKUP_INPUTS_READY (its loads wait for the preceding kernel)")
+    ap.add_argument("--ld", type=int, default=0,
+                    help="row stride (elements) of the step's p / q buffers (default: vocab); layout experiments")
     ap.add_argument("--nvtx", action="store_true",
                     help="NVTX ranges: TSV_NVTX=1 (every libtsv entry point) plus one range per bench phase / workload")
     ap.add_argument("--breakdown", action="store_true", help="also time each step component alone (in graphs)")
@@ -230,7 +232,7 @@ def build_step_inputs(mode, rank, world, dev, args, B_total):
     while s < R:
         if mode == "weak":
             vb = synth.make_verify_batch(B=B_total, V=V, k_max=K_MAX, lam=0.7, seed=seed + 7919 * s + rank,
-                                         device=dev, request_id_base=rank * B_total)
+                                         device=dev, request_id_base=rank * B_total, ld=args.ld or None)
             c, o = synth.make_contexts(B=B_total, L=L_CTX, V=V, seed=seed + 7919 * s + rank)
             k = vb.k
         else:
