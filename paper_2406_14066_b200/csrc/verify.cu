@@ -98,6 +98,12 @@ __device__ __forceinline__ float prune_scale(float T) {
 }
 
 struct Race;
+#ifndef TSV_COUNT_EXACT
+#define TSV_COUNT_EXACT 0
+#endif
+#if TSV_COUNT_EXACT  // diagnostic builds only: exact evaluations / candidates / quads raced
+__device__ unsigned long long g_exact_count[4];
+#endif
 
 // Per-thread race state.  T is warp-uniform: a lower bound on (or an exact value of) a
 // score achieved by an element of this row.  Prune test: skipping element
@@ -129,6 +135,9 @@ struct Race {
     }
 
     __device__ __forceinline__ void eval_exact(float w, uint32_t x, uint32_t vg) {
+#if TSV_COUNT_EXACT
+        atomicAdd(&g_exact_count[0], 1ull);
+#endif
         const uint64_t key = exact_race_key(w, x, vg);
         best = key > best ? key : best;
         Tloc = fmaxf(Tloc, __uint_as_float(static_cast<uint32_t>(best >> 32)));
@@ -157,6 +166,10 @@ struct Race {
             bool cand[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) cand[e] = __fmaf_rn(Tc, race_F(rw[e]), -w[e]) < Th;
+#if TSV_COUNT_EXACT
+            atomicAdd(&g_exact_count[2], 1ull);
+            atomicAdd(&g_exact_count[1], static_cast<unsigned long long>(cand[0] + cand[1] + cand[2] + cand[3]));
+#endif
             if (cand[0] | cand[1] | cand[2] | cand[3]) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -1618,6 +1631,13 @@ static tsv_status run_verify(const tsv_verify_args* a, RaceParams P, cudaStream_
     return TSV_OK;
 }
 
+#if TSV_COUNT_EXACT
+extern "C" TSV_API void tsv_debug_exact_count(unsigned long long* out) {  // diagnostic builds only
+    cudaMemcpyFromSymbol(out, g_exact_count, sizeof(g_exact_count));
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_exact_count, z, sizeof(z));
+}
+#endif
 }  // namespace tsv
 
 using namespace tsv;
