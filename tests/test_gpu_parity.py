@@ -890,6 +890,39 @@ def test_step_graph_capture_matches_eager(tsv, fused):
         assert torch.equal(v, eager[k]), k
 
 
+@pytest.mark.slow
+def test_bench_step_full_size_equals_oracle(tsv):
+    # the bench's step at its full size and in the launch configuration bench.py times (B = 256,
+    # V = 32000, k in 0..8, L = 4096, n 1-4, K = 5; two rotation sets; four consecutive steps in one
+    # CUDA graph, TSV_LOOKUP_INPUTS_READY and TSV_VERIFY_META_READY set, alpha carried from step to
+    # step) against the oracle's composition of Listing 1: lookup -> choose-k -> verify -> update
+    from paper_2406_14066_b200.step import SpecStep
+    inp = synth.make_step_inputs(B=256, V=32000, L=4096, k_max=8, seed=240614066, device=DEV, sets=2)
+    st = SpecStep(inp)
+    steps = [0, 1, 2, 3]
+    st.capture(steps)
+    st.reset_state()
+    st.replay()
+    torch.cuda.synchronize()
+    alpha = 0.7
+    for t in steps:
+        s = t % inp.sets
+        ctx, offs = _np(inp.ctx[s]), _np(inp.ctx_offsets[s])
+        opr, opl = oracle.lookup(ctx, offs, 1, 4, 5)
+        ok, og = oracle.choose_k(alpha, np.diff(offs).astype(np.int32), opl, 5, oracle.POLICY_PLD,
+                                 synth.SPEC_DESK_TARGET, synth.SPEC_DESK_DRAFT, pld_cost_ms=0.05)
+        vb = inp.verify[s]
+        ona, oout, _ = oracle.verify(_np(vb.p), _np(vb.q), _np(vb.row_offsets), _np(vb.draft_tokens),
+                                     _np(vb.request_ids).view(np.uint32), inp.seed, t, 8, vocab=32000)
+        alpha = oracle.update(alpha, ona, _np(vb.row_offsets), decay=0.9)
+    # the graph's buffers hold the last step's outputs (and alpha after all four updates)
+    assert (_np(st.proposal_len) == opl).all() and (_np(st.proposals) == opr).all()
+    assert int(st.k_star.item()) == ok
+    assert (_np(st.goodput).view(np.uint64) == og.view(np.uint64)).all()
+    assert (_np(st.num_accepted) == ona).all() and (_np(st.out_tokens) == oout).all()
+    assert float(st.alpha.item()) == alpha and int(st.status.item()) == 0
+
+
 @pytest.mark.parametrize("fused", [False, True])
 def test_step_lookup_ready_multi_step_graph_matches_eager(tsv, fused):
     # three consecutive steps in one graph with TSV_LOOKUP_INPUTS_READY (the lookup of step t+1 -- and,
