@@ -90,6 +90,14 @@ def test_host_validation_without_gpu(tsv):
     assert L.tsv_propose_lookup(None, None, -1, 1, 2, 5, None, None, None, None) == 1
     # B = 0 is a no-op
     assert L.tsv_propose_lookup(None, None, 0, 1, 2, 5, None, None, None, None) == 0
+    # the flagged entry points: unknown flag bits are rejected before any device work
+    assert L.tsv_propose_lookup_ex(None, None, 0, 1, 2, 5, None, None, None, tsv.LOOKUP_INPUTS_READY, None) == 0
+    assert L.tsv_propose_lookup_ex(None, None, 4, 1, 2, 5, None, None, None, 2, None) == 1
+    assert b"flags" in L.tsv_last_error()
+    m0 = tsv.LatencyModel(0.001, 0.05, 2.0)
+    assert L.tsv_propose_lookup_choose_k_ex(None, None, 4, 1, 4, 5, None, None, None, 0, None, m0, 0.05, -1, None,
+                                            None, None, None, None, 6, None) == 1
+    assert b"flags" in L.tsv_last_error()
     a = tsv.VerifyArgs()
     a.B, a.k_max = 4, 16
     assert L.tsv_verify_accept(ctypes.byref(a), None) == 1
