@@ -190,11 +190,10 @@ class SpecStep:
         s = step % inp.sets
         st = tsv._stream(stream)
         L = tsv.lib()
-        if name == "lookup":
+        if name == "lookup":  # flags 0: back-to-back READY lookups would overlap each other entirely
             tsv._check(L.tsv_propose_lookup_ex(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
                                                inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
-                                               self.proposal_len.data_ptr(), self.status.data_ptr(), self.lookup_flags,
-                                               st))
+                                               self.proposal_len.data_ptr(), self.status.data_ptr(), 0, st))
         elif name == "choose_k":
             self._choose_k(s, st)
         elif name == "verify":
