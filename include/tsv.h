@@ -327,7 +327,14 @@ TSV_API tsv_status tsv_verify_shard_emit(const tsv_verify_args* a, const uint64_
  *    workspace (tsv_verify_workspace_size).
  *  tsv_verify_shard_p2p_phase: phase 0 (flags + push), 1 (wait, meta, race, keys +
  *    push), 2 (wait, emit) separately: lets one process drive G loopback ranks on
- *    one device (all phase 0, then all 1, then all 2). */
+ *    one device (all phase 0, then all 1, then all 2).
+ *  flags & TSV_VERIFY_P2P_FUSED (every rank): no keys kernel -- each race work item
+ *    (request i, chunk c) pushes its chunk key as one LL line into slot [rank][c][i]
+ *    of every rank's buffer and the emit takes the max over the G x NC lines (NC:
+ *    chunk slots per rank, the same on every rank, from vocab_global, world, B and
+ *    the SM count); an item whose chunk has no positive residual pushes its share of
+ *    the R5 fallback instead (flagged in bit 63).  Four kernels per call; outputs
+ *    identical to the LL keys kernel. */
 #define TSV_P2P_MAX_WORLD 8
 #define TSV_P2P_MAX_SUMS 64
 typedef struct tsv_p2p tsv_p2p;
