@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--fused", action="store_true", help="fused lookup+choose-k call (verify+update is always one call)")
+    ap.add_argument("--no-early-trigger", action="store_true",
+                    help="verify without TSV_VERIFY_EARLY_TRIGGER (the next step's lookup launches after the emit)")
     ap.add_argument("--no-lookup-ready", action="store_true",
                     help="launch the lookup without TSV_LOOKUP_INPUTS_READY (its loads wait for the preceding kernel)")
     ap.add_argument("--ld", type=int, default=0,
@@ -406,7 +408,7 @@ def run_ours(args, rank, world, local_rank):
     vbs = inp.verify
     comm = make_comm(args, rank, world, B)
     st = SpecStep(inp, device=dev, chunk=args.chunk, fused=args.fused and comm is None, comm=comm,
-                  lookup_ready=not args.no_lookup_ready)
+                  lookup_ready=not args.no_lookup_ready, early_trigger=not args.no_early_trigger)
     footprint = sum(inp.input_bytes(s) for s in range(R))
     tm = time_step_graphs(args, st, world, local_rank, dev)
     t_max, W, K, gl, stream = tm["t_max"], tm["W"], tm["K"], tm["gl"], tm["stream"]
@@ -537,7 +539,8 @@ def run_ours(args, rank, world, local_rank):
         ne = args.e2e_steps
         hv = synth.VerifyBatch(host[0], host[1], host[2], host[3], host[4], vb.k, V, K_MAX)
         st_h = SpecStep(StepInputs([hv], [hctx[0]], [hctx[1]], [hctx[2]], K_MAX, seed=seed), device=dev,
-                        chunk=args.chunk, comm=comm, lookup_ready=not args.no_lookup_ready)
+                        chunk=args.chunk, comm=comm, lookup_ready=not args.no_lookup_ready,
+                        early_trigger=not args.no_early_trigger)
         k_np = ks[0]
         ctx_bytes = hctx[0].numel() * 4 + hctx[1].numel() * 4 + hctx[2].numel() * 4
 
@@ -600,7 +603,8 @@ def run_ours(args, rank, world, local_rank):
                    "ctx_len": L_CTX, "parallelism": par,
                    "l2_defeat": f"{R} rotating input sets, footprint {footprint / 1e6:.0f} MB vs L2 {l2 / 1e6:.0f} MB",
                    "graph_steps": gl, "fused": bool(args.fused and comm is None),
-                   "lookup_inputs_ready": not args.no_lookup_ready},
+                   "lookup_inputs_ready": not args.no_lookup_ready,
+                   "verify_early_trigger": not (args.no_early_trigger or args.no_lookup_ready)},
         "roofline": {"kernel": "verify_race_kernel (the dominant kernel: streams every algorithmic byte of the verify call)",
                      "bound": "hbm", "achieved": race_achieved, "peak": peak,
                      "unit": "GB/s", "frac": race_achieved / peak, "traffic": traffic,
@@ -651,7 +655,8 @@ def run_strong(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     inp, ks, l2 = build_step_inputs("strong", rank, world, dev, args, B)
     comm = make_comm(args, rank, world, B)
-    st = SpecStep(inp, device=dev, chunk=args.chunk, comm=comm, lookup_ready=not args.no_lookup_ready)
+    st = SpecStep(inp, device=dev, chunk=args.chunk, comm=comm, lookup_ready=not args.no_lookup_ready,
+                  early_trigger=not args.no_early_trigger)
     tm = time_step_graphs(args, st, world, local_rank, dev)
     consistent = global_state_consistent(st, world, dev)
     per_step_tokens, per_step_vbytes = step_tokens(st, inp, ks, tm["step_ids"], dev)

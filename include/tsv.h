@@ -206,6 +206,20 @@ typedef struct tsv_verify_args {
                                   /* every rank must pass it; each shard must fit the */
                                   /* NC chunk slots sized for ceil4(vocab_global /    */
                                   /* world) columns (INVALID_ARG otherwise)           */
+#define TSV_VERIFY_EARLY_TRIGGER 32 /* tsv_verify_accept / _update: the emit kernel  */
+                                  /* lets the kernel after the call launch (PDL)      */
+                                  /* before the race completes, so that kernel's CTAs */
+                                  /* run in the SM slots the race's tail frees.       */
+                                  /* Contract: the kernel after the call reads        */
+                                  /* nothing the call writes (num_accepted,           */
+                                  /* out_tokens, alpha, step_counts, device_status,   */
+                                  /* the workspace) before its own grid-dependency    */
+                                  /* wait -- true of every libtsv kernel without a    */
+                                  /* *_READY flag, and of a TSV_LOOKUP_INPUTS_READY   */
+                                  /* lookup whose contexts this call does not write.  */
+                                  /* With it, two kernels of this call (race, emit)   */
+                                  /* can be in flight when the next kernel starts.    */
+                                  /* Outputs are unchanged.                           */
 #define TSV_VERIFY_META_READY 8   /* Contract: row_offsets, draft_tokens and          */
                                   /* request_ids are COMPLETE before the kernel that  */
                                   /* immediately precedes this call on the stream     */

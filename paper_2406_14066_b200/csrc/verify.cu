@@ -62,6 +62,7 @@ struct RaceParams {
     int32_t B, k_max, vocab, vocab_offset, vocab_global, chunk, n_chunks, rows_p;
     uint32_t ks0[10], ks1[10];  // Philox key schedule k + r W (constant bank)
     int32_t meta_ready;         // TSV_VERIFY_META_READY: the scan reads row_offsets/drafts/rids before its wait
+    int32_t early_trigger;      // TSV_VERIFY_EARLY_TRIGGER: the emit kernel triggers its dependents before its wait
     int32_t race_update;        // lazy race: one extra CTA runs the alpha update (ua) beside the race
     UpdateArgs ua;
     int32_t push;               // TSV_VERIFY_P2P_FUSED: each race item pushes its chunk key to every rank (pv)
@@ -710,8 +711,12 @@ __device__ __forceinline__ int2 emit_unit(const RaceParams& P, int32_t unit) {  
 // kernels back), so no inter-CTA handshake is needed.
 template <int MODE, bool PRUNE, bool UPDATE, bool LOGITS = false>
 __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P, UpdateArgs ua) {
+    // TSV_VERIFY_EARLY_TRIGGER: the kernel after the call may launch while the race still runs (its
+    // CTAs take the SM slots the race's tail frees); it must read nothing this call writes before its
+    // own grid-dependency wait (tsv.h)
+    if (P.early_trigger) pdl_launch_dependents();
     pdl_wait();
-    pdl_launch_dependents();
+    if (!P.early_trigger) pdl_launch_dependents();
     if (UPDATE && blockIdx.x == gridDim.x - 1) {
         update_block(ua);
         return;
@@ -1558,6 +1563,7 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.push = 0;
     P.pv = P2PView{};
     P.meta_ready = (a->flags & TSV_VERIFY_META_READY) ? 1 : 0;
+    P.early_trigger = (a->flags & TSV_VERIFY_EARLY_TRIGGER) ? 1 : 0;
     P.rows_p = a->rows_p;
     const size_t n_chunks = static_cast<size_t>(P.n_chunks);
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);

@@ -86,7 +86,7 @@ class SpecStep:
     k*, every k_i, every emitted token and alpha equal one device holding the whole batch."""
 
     def __init__(self, inp: StepInputs, device="cuda", alpha0: float = 0.7, chunk: int = 0, fused: bool = False,
-                 comm=None, lookup_ready: bool = True):
+                 comm=None, lookup_ready: bool = True, early_trigger: bool = True):
         self.inp = inp
         # the contexts are inputs of the step that no kernel of the step writes (prepared before the step,
         # like a serving engine's input buffers): TSV_LOOKUP_INPUTS_READY lets the lookup search them
@@ -115,9 +115,16 @@ class SpecStep:
         for vb in inp.verify:
             # the batch's row_offsets / drafts / request ids are inputs of the step, never written by
             # the step's own kernels (the proposer's output goes through the target forward first)
+            # the next kernel after the verify call is the next step's lookup: with INPUTS_READY it
+            # reads only the contexts (never written by a step kernel) before its wait, so the emit
+            # may let it launch early (TSV_VERIFY_EARLY_TRIGGER): it searches in the race's tail
+            # (not with the fused lookup + choose-k: it reads alpha, which this call's update CTA writes,
+            # before its wait)
+            early = lookup_ready and early_trigger and not fused
+            flags = tsv.VERIFY_META_READY | (tsv.VERIFY_EARLY_TRIGGER if early else 0)
             a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids,
                                      inp.seed, 0, K, self.num_accepted, self.out_tokens, self.status,
-                                     chunk=chunk, flags=tsv.VERIFY_META_READY)
+                                     chunk=chunk, flags=flags)
             self.args.append(a)
         ws_bytes = max(tsv.tsv_verify_workspace_size(a) for a in self.args)
         self.workspace = tsv.alloc_workspace(ws_bytes, dev)

@@ -30,6 +30,7 @@ VERIFY_SHARD_DENSE = 2
 VERIFY_RACE_ONLY = 4  # measurement: the race kernel alone over a previous call's workspace
 VERIFY_META_READY = 8  # row_offsets/drafts/request_ids not written by the preceding kernel on the stream
 VERIFY_P2P_FUSED = 16  # peer-memory vocab sharding: race items push their chunk keys (no keys kernel)
+VERIFY_EARLY_TRIGGER = 32  # the emit kernel lets the next kernel launch before the race completes (tsv.h)
 LOOKUP_INPUTS_READY = 1  # tsv_propose_lookup_ex: ctx/ctx_offsets not written by any kernel in flight
 LOOKUP_CHOOSE_SCRATCH = 512  # TSV_LOOKUP_CHOOSE_SCRATCH
 POLICY_DRAFT = 0

@@ -851,6 +851,45 @@ def test_meta_ready_flag_same_outputs(tsv):
         assert (na == ona).all() and (out == oout).all() and st == 0
 
 
+def test_early_trigger_followed_by_dependent_kernels(tsv):
+    # TSV_VERIFY_EARLY_TRIGGER: the kernel after the call may launch while the race runs; kernels that
+    # read the call's outputs only after their own grid-dependency wait (the alpha update, the next
+    # verify's scan for p / q and its workspace writes) still see them complete.  Three verify calls with
+    # the flag, each followed by the standalone update, in one graph: every output equals the oracle
+    vb = synth.make_verify_batch(B=200, V=32000, k_max=8, lam=0.6, seed=41).to(DEV)
+    na = torch.empty(200, dtype=torch.int32, device=DEV)
+    out = torch.empty((200, 9), dtype=torch.int32, device=DEV)
+    alpha = torch.full((1,), 0.7, dtype=torch.float64, device=DEV)
+    args = [tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 9, t, 8, na, out,
+                                 flags=tsv.VERIFY_EARLY_TRIGGER | tsv.VERIFY_META_READY) for t in range(3)]
+    ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(args[0]), DEV)
+    for a in args:
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    outs = [torch.empty_like(out) for _ in range(3)]
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        tsv._check(tsv.lib().tsv_verify_accept(tsv.ctypes.byref(args[0]), tsv._stream(side)))  # warm-up
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            for t, a in enumerate(args):
+                tsv._check(tsv.lib().tsv_verify_accept(tsv.ctypes.byref(a), tsv._stream(side)))
+                tsv.tsv_update_acceptance(alpha, na, vb.row_offsets, 0.9, stream=side)
+                outs[t].copy_(out)
+    torch.cuda.current_stream().wait_stream(side)
+    alpha.fill_(0.7)
+    g.replay()
+    torch.cuda.synchronize()
+    h = synth.make_verify_batch(B=200, V=32000, k_max=8, lam=0.6, seed=41)
+    a_ref = 0.7
+    for t in range(3):
+        ona, oout, _ = oracle_verify(h, 9, t)
+        assert (_np(outs[t]) == oout).all(), t
+        a_ref = oracle.update(a_ref, ona, _np(h.row_offsets), decay=0.9)
+    assert float(alpha.item()) == a_ref
+
+
 @pytest.mark.parametrize("est", [0, 1])  # TESTED (default), PROPOSED
 def test_fused_verify_update_equals_separate(tsv, est):
     # the fused update runs as an extra CTA of the race kernel: same alpha bits as the separate call
