@@ -76,6 +76,8 @@ typedef enum {
 #define TSV_DEVSTATUS_NO_WEIGHT 4u  /* selected p row has no positive entry        */
 #define TSV_DEVSTATUS_P2P_TIMEOUT 8u /* a peer-memory exchange wait gave up (a peer
                                         never arrived); outputs are not valid      */
+#define TSV_DEVSTATUS_WAIT_TIMEOUT 32u /* a bounded wait for alpha_ready gave up (its
+                                           producer never ran: a contract violation) */
 #define TSV_DEVSTATUS_BAD_CONTEXT 16u /* lookup: ctx_offsets negative or decreasing,
                                           or L_i > TSV_MAX_CONTEXT                 */
 
@@ -441,8 +443,15 @@ TSV_API tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int32_t
  * being ctx, ctx_offsets, ctx_len and alpha and the outputs proposals,
  * proposal_len, k_out, goodput_out and k_per_request: the search, the batch
  * sums and the last CTA's ArgMaxGoodput all run before the grid-dependency
- * wait.  In a decode step alpha comes from the previous step's update (two or
- * more kernels back), so it qualifies. */
+ * wait.
+ *   alpha_ready  nullable device word: before reading alpha the kernel waits
+ *                (acquire, bounded: TSV_DEVSTATUS_WAIT_TIMEOUT) until it is 1.
+ *                With the previous step's tsv_verify_accept_update_ex (which
+ *                resets the word in its first kernel and sets it once alpha is
+ *                written) and TSV_VERIFY_EARLY_TRIGGER, this lookup + choose-k
+ *                runs in the previous race's tail and still reads that step's
+ *                alpha.  NULL: alpha must qualify as an input (written two or
+ *                more kernels back). */
 TSV_API tsv_status tsv_propose_lookup_choose_k_ex(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                                           int32_t n_min, int32_t n_max, int32_t k_fixed,
                                           int32_t* proposals, int32_t* proposal_len,
@@ -450,8 +459,8 @@ TSV_API tsv_status tsv_propose_lookup_choose_k_ex(const int32_t* ctx, const int3
                                           const int32_t* ctx_len, tsv_latency_model target,
                                           double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
                                           double* goodput_out, int32_t* k_per_request,
-                                          uint32_t* counter, int32_t* device_status, int32_t flags,
-                                          void* stream);
+                                          uint32_t* counter, int32_t* device_status,
+                                          const uint32_t* alpha_ready, int32_t flags, void* stream);
 
 /* --------------------------------------------------------------------------
  * Acceptance-rate update: UpdateGlobalAcceptance (Listing 1 line 19,
@@ -472,11 +481,19 @@ TSV_API tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, con
 /* Fused Accept + UpdateGlobalAcceptance (Listing 1 lines 18-19): tsv_verify_accept
  * followed by tsv_update_acceptance(alpha, per_request, a->num_accepted,
  * a->row_offsets, a->B, decay, estimator), with the update run by one extra CTA
- * of verify's final (emit) kernel -- the accepted counts are final after the
- * acceptance scan, so it needs no handshake.  Outputs identical to the two
+ * of verify's race kernel (beside the race) -- the accepted counts are final after
+ * the acceptance scan, so it needs no handshake.  Outputs identical to the two
  * separate calls; same workspace as tsv_verify_accept. */
 TSV_API tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                     double decay, int32_t estimator, void* stream);
+/* ... with alpha_ready (nullable device word): the call's first kernel sets it to 0
+ * (after its grid-dependency wait) and the update sets it to 1 (release) once
+ * alpha is written -- the signal a following kernel that may start before this
+ * call completes (TSV_VERIFY_EARLY_TRIGGER) waits on before reading alpha, e.g.
+ * tsv_propose_lookup_choose_k_ex(..., alpha_ready, TSV_LOOKUP_INPUTS_READY).
+ * Initialise the word to 1 (alpha valid) before the first call. */
+TSV_API tsv_status tsv_verify_accept_update_ex(const tsv_verify_args* a, double* alpha, int32_t per_request,
+                                       double decay, int32_t estimator, uint32_t* alpha_ready, void* stream);
 
 /* --------------------------------------------------------------------------
  * Request-sharded step over NVLink peer memory (the exchange fused into

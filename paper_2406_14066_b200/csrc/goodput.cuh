@@ -42,6 +42,8 @@ struct ChooseArgs {
     double pld_cost_ms;
     long long kv_free;
     int32_t alpha_per_request, B, k_max, policy;
+    const uint32_t* alpha_ready;  // nullable: wait for *alpha_ready == 1 before reading alpha (fused lookup)
+    int32_t* devstatus;           // TSV_DEVSTATUS_WAIT_TIMEOUT (nullable)
 };
 
 struct UpdateArgs {
@@ -55,7 +57,36 @@ struct UpdateArgs {
     int32_t use_p2p;
     int32_t* devstatus;  // TSV_DEVSTATUS_P2P_TIMEOUT (nullable)
     P2PView p2p;
+    // nullable (tsv_verify_accept_update_ex): set to 1 with release semantics once alpha is written, so
+    // a kernel that starts before this call completes (TSV_VERIFY_EARLY_TRIGGER) can wait for alpha
+    uint32_t* alpha_ready;
 };
+
+// alpha is written (by this thread, or by this CTA before a __syncthreads): publish it
+__device__ __forceinline__ void signal_alpha_ready(uint32_t* flag) {
+    if (flag) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+    }
+}
+
+// Wait (bounded, %globaltimer) until *flag == 1 with acquire semantics; TSV_DEVSTATUS_WAIT_TIMEOUT if it
+// never comes (the producer is not running: a contract violation), instead of hanging.
+__device__ __forceinline__ void wait_alpha_ready(const uint32_t* flag, int32_t* devstatus) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v == 1u) return;
+    const unsigned long long t0 = global_ns();
+    uint32_t n = 0;
+    while (v != 1u) {
+        __nanosleep(64);
+        if ((++n & 255u) == 0 && global_ns() - t0 > TSV_P2P_TIMEOUT_NS) {
+            report(devstatus, TSV_DEVSTATUS_WAIT_TIMEOUT);
+            return;
+        }
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    }
+}
 
 // Batch sums of ArgMaxGoodput, exact int64 (fixed point 2^-32 for the token sums):
 //   L[k] = sum_i rint(2^32 l(alpha_i, min(k, cap_i))),  N[k] = sum_i min(k, cap_i),
@@ -247,7 +278,13 @@ __device__ __forceinline__ void update_block(const UpdateArgs& A, long long* sum
             stt += t;
         }
     }
-    if (A.per_request) return;
+    if (A.per_request) {
+        if (A.alpha_ready) {  // every thread wrote its alpha_i: publish them together
+            __syncthreads();
+            if (threadIdx.x == 0) signal_alpha_ready(A.alpha_ready);
+        }
+        return;
+    }
     sm = warp_sum_i64(sm);
     stt = warp_sum_i64(stt);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -269,6 +306,7 @@ __device__ __forceinline__ void update_block(const UpdateArgs& A, long long* sum
             sums_out[1] = b;
         } else if (!A.use_p2p) {
             ewma_apply(A.alpha, a, b, A.decay);
+            signal_alpha_ready(A.alpha_ready);
         }
         s_ab[0] = a;
         s_ab[1] = b;
@@ -276,7 +314,10 @@ __device__ __forceinline__ void update_block(const UpdateArgs& A, long long* sum
     if (A.use_p2p && !sums_out) {  // the ranks' pairs summed over peer memory, then the same EWMA everywhere
         __syncthreads();
         p2p_allreduce_block(s_ab, 2, A.p2p, A.devstatus);
-        if (threadIdx.x == 0) ewma_apply(A.alpha, s_ab[0], s_ab[1], A.decay);
+        if (threadIdx.x == 0) {
+            ewma_apply(A.alpha, s_ab[0], s_ab[1], A.decay);
+            signal_alpha_ready(A.alpha_ready);
+        }
     }
 }
 

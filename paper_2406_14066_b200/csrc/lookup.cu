@@ -110,6 +110,7 @@ __device__ __forceinline__ void fused_choose_k(const ChooseArgs& A, FusedScratch
     __shared__ int s_last, s_best;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {  // ci: request i's proposal length (valid in warp 0)
+        if (A.alpha_ready) wait_alpha_ready(A.alpha_ready, A.devstatus);  // alpha may be written by a kernel in flight
         const double a = __ldcg(A.alpha + (A.alpha_per_request ? i : 0));
         const int32_t k = lane;
         if (k <= A.k_max) {
@@ -292,7 +293,7 @@ extern "C" tsv_status tsv_propose_lookup_choose_k(const int32_t* ctx, const int3
     TSV_TRACE_CALL();
     return tsv_propose_lookup_choose_k_ex(ctx, ctx_offsets, B, n_min, n_max, k_fixed, proposals, proposal_len, alpha,
                                           alpha_per_request, ctx_len, target, pld_cost_ms, kv_free_slots, k_out,
-                                          goodput_out, k_per_request, counter, device_status, 0, stream);
+                                          goodput_out, k_per_request, counter, device_status, nullptr, 0, stream);
 }
 
 extern "C" tsv_status tsv_propose_lookup_choose_k_ex(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
@@ -302,8 +303,8 @@ extern "C" tsv_status tsv_propose_lookup_choose_k_ex(const int32_t* ctx, const i
                                                      const int32_t* ctx_len, tsv_latency_model target,
                                                      double pld_cost_ms, int64_t kv_free_slots, int32_t* k_out,
                                                      double* goodput_out, int32_t* k_per_request,
-                                                     uint32_t* counter, int32_t* device_status, int32_t flags,
-                                                     void* stream) {
+                                                     uint32_t* counter, int32_t* device_status,
+                                                     const uint32_t* alpha_ready, int32_t flags, void* stream) {
     TSV_TRACE_CALL();
     TSV_REQUIRE((flags & ~TSV_LOOKUP_INPUTS_READY) == 0, "tsv_propose_lookup_choose_k: unknown flags 0x%x", flags);
     TSV_REQUIRE(B >= 1, "tsv_propose_lookup_choose_k: B must be >= 1 (got %d)", B);
@@ -326,6 +327,8 @@ extern "C" tsv_status tsv_propose_lookup_choose_k_ex(const int32_t* ctx, const i
     A.draft = target;
     A.pld_cost_ms = pld_cost_ms;
     A.kv_free = static_cast<long long>(kv_free_slots);
+    A.alpha_ready = alpha_ready;
+    A.devstatus = device_status;
     A.alpha_per_request = alpha_per_request;
     A.B = B;
     A.k_max = k_fixed;

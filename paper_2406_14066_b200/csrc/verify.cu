@@ -63,6 +63,7 @@ struct RaceParams {
     uint32_t ks0[10], ks1[10];  // Philox key schedule k + r W (constant bank)
     int32_t meta_ready;         // TSV_VERIFY_META_READY: the scan reads row_offsets/drafts/rids before its wait
     int32_t early_trigger;      // TSV_VERIFY_EARLY_TRIGGER: the emit kernel triggers its dependents before its wait
+    uint32_t* alpha_ready;      // nullable (tsv_verify_accept_update_ex): reset to 0 by the scan, set by the update
     int32_t race_update;        // lazy race: one extra CTA runs the alpha update (ua) beside the race
     UpdateArgs ua;
     int32_t push;               // TSV_VERIFY_P2P_FUSED: each race item pushes its chunk key to every rank (pv)
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
         pdl_launch_dependents();
     }
     zero_step_counts(P.step_counts);
+    if (P.alpha_ready && blockIdx.x == 0 && threadIdx.x == 0) *P.alpha_ready = 0u;  // alpha of this call: pending
     if (ok && lane < k) {
         bad = x < 0 || x >= P.vocab_global;
         const int32_t xl = x - P.vocab_offset;
@@ -403,7 +405,13 @@ __device__ __forceinline__ void update_cta(const UpdateArgs& A) {
             stt += t;
         }
     }
-    if (A.per_request) return;
+    if (A.per_request) {
+        if (A.alpha_ready) {  // every thread wrote its alpha_i: publish them together
+            __syncthreads();
+            if (threadIdx.x == 0) signal_alpha_ready(A.alpha_ready);
+        }
+        return;
+    }
     sm = warp_sum_i64(sm);
     stt = warp_sum_i64(stt);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -419,14 +427,20 @@ __device__ __forceinline__ void update_cta(const UpdateArgs& A) {
             a += red2[w][0];
             b += red2[w][1];
         }
-        if (!A.use_p2p) ewma_apply(A.alpha, a, b, A.decay);
+        if (!A.use_p2p) {
+            ewma_apply(A.alpha, a, b, A.decay);
+            signal_alpha_ready(A.alpha_ready);
+        }
         s_ab[0] = a;
         s_ab[1] = b;
     }
     if (A.use_p2p) {  // request-sharded global alpha: sum the pair over the ranks (p2p.cuh), same EWMA everywhere
         __syncthreads();
         p2p_allreduce_block(s_ab, 2, A.p2p, A.devstatus);
-        if (threadIdx.x == 0) ewma_apply(A.alpha, s_ab[0], s_ab[1], A.decay);
+        if (threadIdx.x == 0) {
+            ewma_apply(A.alpha, s_ab[0], s_ab[1], A.decay);
+            signal_alpha_ready(A.alpha_ready);
+        }
     }
 }
 
@@ -1564,6 +1578,7 @@ static RaceParams make_params(const tsv_verify_args* a) {
     P.pv = P2PView{};
     P.meta_ready = (a->flags & TSV_VERIFY_META_READY) ? 1 : 0;
     P.early_trigger = (a->flags & TSV_VERIFY_EARLY_TRIGGER) ? 1 : 0;
+    P.alpha_ready = nullptr;
     P.rows_p = a->rows_p;
     const size_t n_chunks = static_cast<size_t>(P.n_chunks);
     const size_t rows = static_cast<size_t>(a->rows_p > a->B ? a->rows_p : a->B);
@@ -1681,6 +1696,13 @@ extern "C" tsv_status tsv_verify_accept(const tsv_verify_args* a, void* stream) 
 extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                                double decay, int32_t estimator, void* stream) {
     TSV_TRACE_CALL();
+    return tsv_verify_accept_update_ex(a, alpha, per_request, decay, estimator, nullptr, stream);
+}
+
+extern "C" tsv_status tsv_verify_accept_update_ex(const tsv_verify_args* a, double* alpha, int32_t per_request,
+                                                  double decay, int32_t estimator, uint32_t* alpha_ready,
+                                                  void* stream) {
+    TSV_TRACE_CALL();
     TSV_TRY(validate(a));
     TSV_REQUIRE(a->vocab_offset == 0 && a->vocab == a->vocab_global,
                 "tsv_verify_accept_update: unsharded call needs vocab_offset == 0 and vocab == vocab_global");
@@ -1700,7 +1722,10 @@ extern "C" tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double*
     ua.per_request = per_request;
     ua.B = a->B;
     ua.estimator = estimator;
-    return run_verify<kLazy>(a, make_params(a), static_cast<cudaStream_t>(stream), &ua);
+    ua.alpha_ready = alpha_ready;
+    RaceParams P = make_params(a);
+    P.alpha_ready = alpha_ready;
+    return run_verify<kLazy>(a, P, static_cast<cudaStream_t>(stream), &ua);
 }
 
 extern "C" tsv_status tsv_verify_accept_update_p2p(const tsv_verify_args* a, double* alpha, int32_t per_request,

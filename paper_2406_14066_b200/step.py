@@ -104,6 +104,9 @@ class SpecStep:
         self.out_tokens = torch.empty((B, K + 1), dtype=torch.int32, device=dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.counter = tsv.lookup_choose_scratch(dev)  # fused lookup + choose-k
+        # 1: alpha is final.  The verify + update call resets it and sets it once alpha is written; the
+        # fused lookup + choose-k of the next step waits for it (it may start in the race's tail)
+        self.alpha_ready = torch.ones(1, dtype=torch.int32, device=dev)
         self.fused = fused
         self.comm = comm
         self.p2p = comm is not None and not isinstance(comm, tsv.Comm)
@@ -118,9 +121,9 @@ class SpecStep:
             # the next kernel after the verify call is the next step's lookup: with INPUTS_READY it
             # reads only the contexts (never written by a step kernel) before its wait, so the emit
             # may let it launch early (TSV_VERIFY_EARLY_TRIGGER): it searches in the race's tail
-            # (not with the fused lookup + choose-k: it reads alpha, which this call's update CTA writes,
-            # before its wait)
-            early = lookup_ready and early_trigger and not fused
+            # (the fused lookup + choose-k reads alpha, which this call's update CTA writes, before its
+            # wait: it waits for the alpha_ready word the update sets, tsv_verify_accept_update_ex)
+            early = lookup_ready and early_trigger
             flags = tsv.VERIFY_META_READY | (tsv.VERIFY_EARLY_TRIGGER if early else 0)
             a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids,
                                      inp.seed, 0, K, self.num_accepted, self.out_tokens, self.status,
@@ -177,11 +180,12 @@ class SpecStep:
                 self.proposals.data_ptr(), self.proposal_len.data_ptr(), self.alpha.data_ptr(), 0,
                 inp.ctx_len[s].data_ptr(), tsv.LatencyModel(*inp.target), float(inp.pld_cost_ms),
                 int(inp.kv_free_slots), self.k_star.data_ptr(), self.goodput.data_ptr(), self.k_req.data_ptr(),
-                self.counter.data_ptr(), self.status.data_ptr(), self.lookup_flags, st))
+                self.counter.data_ptr(), self.status.data_ptr(),
+                self.alpha_ready.data_ptr() if self.lookup_flags else None, self.lookup_flags, st))
             a = self.args[s]
             a.step = step & 0xFFFFFFFF
-            tsv._check(L.tsv_verify_accept_update(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
-                                                  tsv.EST_TESTED, st))
+            tsv._check(L.tsv_verify_accept_update_ex(tsv.ctypes.byref(a), self.alpha.data_ptr(), 0, 0.9,
+                                                     tsv.EST_TESTED, self.alpha_ready.data_ptr(), st))
             return
         tsv._check(L.tsv_propose_lookup_ex(inp.ctx[s].data_ptr(), inp.ctx_offsets[s].data_ptr(), inp.B_of(s),
                                            inp.n_min, inp.n_max, inp.k_fixed, self.proposals.data_ptr(),
@@ -240,6 +244,7 @@ class SpecStep:
 
     def reset_state(self, alpha0: float = 0.7):
         self.alpha.fill_(alpha0)
+        self.alpha_ready.fill_(1)
         self.status.zero_()
 
     def outputs(self):

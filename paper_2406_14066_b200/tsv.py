@@ -25,6 +25,7 @@ DEVSTATUS_BAD_K = 2
 DEVSTATUS_NO_WEIGHT = 4
 DEVSTATUS_P2P_TIMEOUT = 8
 DEVSTATUS_BAD_CONTEXT = 16
+DEVSTATUS_WAIT_TIMEOUT = 32
 VERIFY_NO_PRUNE = 1
 VERIFY_SHARD_DENSE = 2
 VERIFY_RACE_ONLY = 4  # measurement: the race kernel alone over a previous call's workspace
@@ -54,7 +55,7 @@ EXPORTED = [
     "tsv_p2p_buffer_size", "tsv_p2p_alloc", "tsv_p2p_free", "tsv_p2p_open", "tsv_p2p_close", "tsv_p2p_init",
     "tsv_p2p_destroy", "tsv_verify_accept_sharded_p2p", "tsv_verify_shard_p2p_phase", "tsv_allreduce_i64_p2p",
     "tsv_goodput_choose_k_p2p", "tsv_update_acceptance_p2p", "tsv_verify_accept_update_p2p",
-    "tsv_propose_lookup_ex", "tsv_propose_lookup_choose_k_ex",
+    "tsv_propose_lookup_ex", "tsv_propose_lookup_choose_k_ex", "tsv_verify_accept_update_ex",
 ]
 
 
@@ -123,7 +124,8 @@ def _load() -> ctypes.CDLL:
         "tsv_propose_lookup_choose_k": ([P, P, i32, i32, i32, i32, P, P, P, i32, P, LatencyModel, f64, i64,
                                          P, P, P, P, P, P], ctypes.c_int),
         "tsv_propose_lookup_choose_k_ex": ([P, P, i32, i32, i32, i32, P, P, P, i32, P, LatencyModel, f64, i64,
-                                            P, P, P, P, P, i32, P], ctypes.c_int),
+                                            P, P, P, P, P, P, i32, P], ctypes.c_int),
+        "tsv_verify_accept_update_ex": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P, P], ctypes.c_int),
         "tsv_verify_accept_update": ([ctypes.POINTER(VerifyArgs), P, i32, f64, i32, P], ctypes.c_int),
         "tsv_debug_race_E": ([ctypes.c_uint32, ctypes.c_uint32, P, P], ctypes.c_int),
         "tsv_debug_philox": ([P, P, ctypes.c_uint32, P, i32, P], ctypes.c_int),
@@ -418,7 +420,8 @@ def lookup_choose_scratch(device) -> torch.Tensor:
 def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, ctx_len, target,
                                 pld_cost_ms, counter, kv_free_slots=-1, alpha_per_request=None,
                                 proposals=None, proposal_len=None, k_out=None, goodput_out=None,
-                                k_per_request=None, device_status=None, stream=None, flags: int = 0):
+                                k_per_request=None, device_status=None, stream=None, flags: int = 0,
+                                alpha_ready=None):
     """Fused prompt lookup + PLD goodput selection.  ``counter``: device scratch of
     LOOKUP_CHOOSE_SCRATCH bytes (e.g. lookup_choose_scratch()), zeroed once.
     flags: LOOKUP_INPUTS_READY (tsv_propose_lookup_choose_k_ex; include/tsv.h states the contract).
@@ -442,7 +445,7 @@ def tsv_propose_lookup_choose_k(ctx, ctx_offsets, n_min, n_max, k_fixed, alpha, 
                                                1 if per else 0, _ptr(ctx_len), LatencyModel(*target),
                                                float(pld_cost_ms), int(kv_free_slots), _ptr(k_out),
                                                _ptr(goodput_out), _ptr(k_per_request), _ptr(counter),
-                                               _ptr(device_status), int(flags), _stream(stream)))
+                                               _ptr(device_status), _ptr(alpha_ready), int(flags), _stream(stream)))
     return proposals, proposal_len, k_out, goodput_out
 
 

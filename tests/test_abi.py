@@ -96,7 +96,7 @@ def test_host_validation_without_gpu(tsv):
     assert b"flags" in L.tsv_last_error()
     m0 = tsv.LatencyModel(0.001, 0.05, 2.0)
     assert L.tsv_propose_lookup_choose_k_ex(None, None, 4, 1, 4, 5, None, None, None, 0, None, m0, 0.05, -1, None,
-                                            None, None, None, None, 6, None) == 1
+                                            None, None, None, None, None, 6, None) == 1
     assert b"flags" in L.tsv_last_error()
     a = tsv.VerifyArgs()
     a.B, a.k_max = 4, 16
@@ -173,4 +173,4 @@ def test_devstatus_bits_match_header(tsv):
     bits = dict((n, int(v)) for n, v in re.findall(r"#define TSV_DEVSTATUS_(\w+) (\d+)u", txt))
     assert bits == {"BAD_TOKEN": tsv.DEVSTATUS_BAD_TOKEN, "BAD_K": tsv.DEVSTATUS_BAD_K,
                     "NO_WEIGHT": tsv.DEVSTATUS_NO_WEIGHT, "P2P_TIMEOUT": tsv.DEVSTATUS_P2P_TIMEOUT,
-                    "BAD_CONTEXT": tsv.DEVSTATUS_BAD_CONTEXT}
+                    "BAD_CONTEXT": tsv.DEVSTATUS_BAD_CONTEXT, "WAIT_TIMEOUT": tsv.DEVSTATUS_WAIT_TIMEOUT}
