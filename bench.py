@@ -1438,6 +1438,10 @@ def main():
         if world == 1:
             plan += [("config4_sharded_p2p", run_config4, {"shard_mode": "p2p"}),
                      ("config4_sharded_p2p_fused", run_config4, {"shard_mode": "p2p_fused"})]
+        else:  # the other exchanges of config 4 over the N ranks (the "config4" line is the LL exchange)
+            plan += [("config4_p2p_fused", run_config4, {"shard_mode": "p2p_fused"})]
+            if not SHARED_GPU:  # NCCL cannot put two ranks on one GPU
+                plan += [("config4_nccl_lazy", run_config4, {"shard_mode": "lazy"})]
         plan += [("greedy", run_greedy, {}), ("logits", run_logits, {}), ("config5", run_config5, {}),
                  ("loop", run_loop, {})]
         for name, fn, over in plan:
