@@ -833,7 +833,7 @@ def run_config4(args, rank, world, local_rank):
         "config": {"workload": f"config4 Llama-3 verify (B={B}, k~U{{0..{K_MAX}}}, V={V4}, fp32 p+q, lambda=0.7), "
                                + ("one GPU, unsharded" if unsharded else f"vocab-sharded x{world} ({args.shard_mode})"),
                    "global_batch": B, "vocab": V4, "k_max": K_MAX,
-                   "parallelism": "unsharded x1" if unsharded else f"vocab-sharded x{world}",
+                   "parallelism": "unsharded x1" if unsharded else f"vocab-sharded x{world} ({args.shard_mode})",
                    "l2_defeat": f"{R} rotating input sets, {footprint / 1e6:.0f} MB per rank",
                    "graph_steps": gl},
         "roofline": {"kernel": "tsv_verify_accept (unsharded, one GPU)" if unsharded else
