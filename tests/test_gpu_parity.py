@@ -890,6 +890,48 @@ def test_early_trigger_followed_by_dependent_kernels(tsv):
     assert float(alpha.item()) == a_ref
 
 
+def test_alpha_ready_word_protocol(tsv):
+    # tsv_verify_accept_update_ex: the word is reset by the call's first kernel and set to 1 once alpha is
+    # written (global and per-request alpha); the fused lookup + choose-k waiting on it reads that alpha
+    vb = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=43).to(DEV)
+    h = synth.make_verify_batch(B=64, V=32000, k_max=8, lam=0.7, seed=43)
+    ona, _, _ = oracle_verify(h, 3, 1)
+    for per in (False, True):
+        na = torch.empty(64, dtype=torch.int32, device=DEV)
+        out = torch.empty((64, 9), dtype=torch.int32, device=DEV)
+        a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 3, 1, 8, na, out)
+        ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+        alpha = torch.full((64 if per else 1,), 0.7, dtype=torch.float64, device=DEV)
+        ready = torch.full((1,), 7, dtype=torch.int32, device=DEV)
+        tsv._check(tsv.lib().tsv_verify_accept_update_ex(tsv.ctypes.byref(a), alpha.data_ptr(), 1 if per else 0, 0.9,
+                                                         tsv.EST_TESTED, ready.data_ptr(), tsv._stream(None)))
+        torch.cuda.synchronize()
+        assert int(ready.item()) == 1
+        want = oracle.update(np.full(64, 0.7) if per else 0.7, ona, _np(h.row_offsets), decay=0.9)
+        assert np.array_equal(_np(alpha), np.atleast_1d(want))
+
+
+def test_alpha_ready_wait_times_out_without_producer(tsv):
+    # a fused lookup + choose-k told to wait for alpha_ready that nobody sets gives up after the bounded
+    # wait (TSV_DEVSTATUS_WAIT_TIMEOUT) instead of hanging; its outputs still follow the alpha it then reads
+    ctx, offs = synth.make_contexts(B=8, L=256, seed=9)
+    c, o = torch.tensor(ctx, device=DEV), torch.tensor(offs, device=DEV)
+    cl = torch.tensor(np.diff(offs).astype(np.int32), device=DEV)
+    alpha = torch.full((1,), 0.6, dtype=torch.float64, device=DEV)
+    ready = torch.zeros(1, dtype=torch.int32, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    counter = tsv.lookup_choose_scratch(DEV)
+    pr, pl, k, g = tsv.tsv_propose_lookup_choose_k(c, o, 1, 4, 5, alpha, cl, synth.SPEC_DESK_TARGET, 0.05, counter,
+                                                   device_status=st, flags=tsv.LOOKUP_INPUTS_READY, alpha_ready=ready)
+    torch.cuda.synchronize()
+    assert int(st.item()) & tsv.DEVSTATUS_WAIT_TIMEOUT
+    opr, opl = oracle.lookup(ctx, offs, 1, 4, 5)
+    ok, _ = oracle.choose_k(0.6, np.diff(offs).astype(np.int32), opl, 5, oracle.POLICY_PLD, synth.SPEC_DESK_TARGET,
+                            synth.SPEC_DESK_DRAFT, pld_cost_ms=0.05)
+    assert (_np(pl) == opl).all() and int(k.item()) == ok
+
+
 @pytest.mark.parametrize("est", [0, 1])  # TESTED (default), PROPOSED
 def test_fused_verify_update_equals_separate(tsv, est):
     # the fused update runs as an extra CTA of the race kernel: same alpha bits as the separate call
