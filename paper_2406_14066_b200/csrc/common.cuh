@@ -257,6 +257,61 @@ __device__ __forceinline__ void report(int32_t* devstatus, uint32_t bits) {
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Step timeline (diagnostic builds only, -DTSV_STEP_TRACE=1; scripts/diag_step_trace.py): thread 0 of
+// every CTA of the step's kernels records (kernel id, CTA, entry, after the grid-dependency wait, exit)
+// from %globaltimer into its translation unit's buffer (read by tsv_debug_step_trace_*).
+#ifndef TSV_STEP_TRACE
+#define TSV_STEP_TRACE 0
+#endif
+#if TSV_STEP_TRACE
+constexpr unsigned kStepTraceMax = 1u << 16;
+static __device__ unsigned long long g_step_tr[kStepTraceMax][4];
+static __device__ unsigned int g_step_tr_n;
+__device__ __forceinline__ unsigned long long step_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+struct StepTrace {
+    unsigned long long t0, t1;
+    int id;
+    __device__ explicit StepTrace(int i) : t0(step_ns()), t1(0), id(i) {}
+    __device__ void waited() { t1 = step_ns(); }
+    __device__ ~StepTrace() {
+        if (threadIdx.x == 0) {
+            const unsigned k = atomicAdd(&g_step_tr_n, 1u);
+            if (k < kStepTraceMax) {
+                g_step_tr[k][0] = (static_cast<unsigned long long>(blockIdx.x) << 8) | static_cast<unsigned>(id);
+                g_step_tr[k][1] = t0;
+                g_step_tr[k][2] = t1;
+                g_step_tr[k][3] = step_ns();
+            }
+        }
+    }
+};
+#define TSV_STEP_SPAN(id) ::tsv::StepTrace tsv_step_span_(id)
+#define TSV_STEP_WAITED() tsv_step_span_.waited()
+#define TSV_STEP_TRACE_READER(name)                                                                   \
+    extern "C" TSV_API unsigned tsv_debug_step_trace_##name(unsigned long long* out, unsigned max_n) { \
+        unsigned n = 0;                                                                               \
+        cudaMemcpyFromSymbol(&n, ::tsv::g_step_tr_n, sizeof(n));                                      \
+        n = n < max_n ? n : max_n;                                                                    \
+        if (n > ::tsv::kStepTraceMax) n = ::tsv::kStepTraceMax;                                       \
+        cudaMemcpyFromSymbol(out, ::tsv::g_step_tr, n * 4 * sizeof(unsigned long long));              \
+        unsigned z = 0;                                                                               \
+        cudaMemcpyToSymbol(::tsv::g_step_tr_n, &z, sizeof(z));                                        \
+        return n;                                                                                     \
+    }
+#else
+#define TSV_STEP_SPAN(id) \
+    do {                  \
+    } while (0)
+#define TSV_STEP_WAITED() \
+    do {                  \
+    } while (0)
+#define TSV_STEP_TRACE_READER(name)
+#endif
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>

@@ -24,7 +24,9 @@ namespace tsv {
 #endif
 constexpr int kGpChooseThreads = TSV_GP_CHOOSE_THREADS;  // B = 256 step: 256 threads 2.84 us; 128: 3.12; 64: 3.86; 32: 6.10
 __global__ void __launch_bounds__(kGpChooseThreads) goodput_choose_k_kernel(const ChooseArgs A) {
+    TSV_STEP_SPAN(1);
     pdl_wait();
+    TSV_STEP_WAITED();
     pdl_launch_dependents();
     choose_k_block<kGpChooseThreads>(A);
 }
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(kGpBatchThreads) goodput_choose_k_batched_kern
 }  // namespace tsv
 
 using namespace tsv;
+TSV_STEP_TRACE_READER(goodput)
 
 extern "C" tsv_status tsv_goodput_choose_k_batched(const double* alpha, const int32_t* ctx_len, const int32_t* cap,
                                                    const int32_t* inst_offsets, int32_t n_inst, int32_t k_max,

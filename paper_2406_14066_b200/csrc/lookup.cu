@@ -176,8 +176,10 @@ __global__ void __launch_bounds__(kLookupThreads)
                         int32_t n_min, int32_t n_max, int32_t K, int32_t* __restrict__ proposals,
                         int32_t* __restrict__ proposal_len, ChooseArgs ca, uint32_t* counter, int32_t* devstatus) {
     __shared__ uint32_t s_red[kLookupThreads / 32];
+    TSV_STEP_SPAN(0);
     if (!READY) {
         pdl_wait();
+        TSV_STEP_WAITED();
         pdl_launch_dependents();
     }
     const int32_t i = blockIdx.x;
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(kLookupThreads)
     if (FUSED) fused_choose_k(ca, reinterpret_cast<FusedScratch*>(counter), i, my_len);
     if (READY) {
         pdl_wait();
+        TSV_STEP_WAITED();
         pdl_launch_dependents();
     }
 }
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(kLookupThreads)
 }  // namespace tsv
 
 using namespace tsv;
+TSV_STEP_TRACE_READER(lookup)
 
 extern "C" tsv_status tsv_propose_lookup(const int32_t* ctx, const int32_t* ctx_offsets, int32_t B,
                                          int32_t n_min, int32_t n_max, int32_t k_fixed,

@@ -305,10 +305,12 @@ __device__ __forceinline__ void emit_prefix(const RaceParams& P, int32_t i, int3
 // Shard: writes the accept / owner flags of every p row of the request into its tuple.
 template <int MODE>
 __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
+    TSV_STEP_SPAN(2);
     // TSV_VERIFY_META_READY: row_offsets / draft_tokens / request_ids were not written by the
     // preceding kernel, so they are read while it drains; p and q only after the wait.
     if (!P.meta_ready) {
         pdl_wait();               // inputs of this step are complete
+        TSV_STEP_WAITED();
         pdl_launch_dependents();  // let the race kernel launch and set up while we scan
     }
     const int32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     if (ok && lane < k) x = P.drafts[qbase + lane];
     if (P.meta_ready) {
         pdl_wait();
+        TSV_STEP_WAITED();
         pdl_launch_dependents();
     }
     zero_step_counts(P.step_counts);
@@ -524,7 +527,9 @@ __device__ __forceinline__ uint32_t nctaid_x() {
 
 template <int MODE, bool DENSE_Q, bool PRUNE, bool LOGITS = false, bool PUSH = false>
 __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kernel(const RaceParams P) {
+    TSV_STEP_SPAN(3);
     pdl_wait();  // the scan kernel's ReqMeta / rowT / rowkey are complete and visible
+    TSV_STEP_WAITED();
     pdl_launch_dependents();
     // the update CTA (if any) is CTA 0, the first launched: it runs beside the race
     const int32_t upd = (MODE == kLazy && P.race_update) ? 1 : 0;
@@ -728,8 +733,10 @@ __global__ void __launch_bounds__(256) verify_emit_kernel(const RaceParams P, Up
     // TSV_VERIFY_EARLY_TRIGGER: the kernel after the call may launch while the race still runs (its
     // CTAs take the SM slots the race's tail frees); it must read nothing this call writes before its
     // own grid-dependency wait (tsv.h)
+    TSV_STEP_SPAN(4);
     if (P.early_trigger) pdl_launch_dependents();
     pdl_wait();
+    TSV_STEP_WAITED();
     if (!P.early_trigger) pdl_launch_dependents();
     if (UPDATE && blockIdx.x == gridDim.x - 1) {
         update_block(ua);
@@ -1662,6 +1669,7 @@ extern "C" TSV_API void tsv_debug_exact_count(unsigned long long* out) {  // dia
 }  // namespace tsv
 
 using namespace tsv;
+TSV_STEP_TRACE_READER(verify)
 
 extern "C" tsv_status tsv_verify_workspace_size(const tsv_verify_args* a, size_t* bytes) {
     TSV_TRACE_CALL();
