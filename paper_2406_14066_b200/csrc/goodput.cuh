@@ -102,8 +102,91 @@ struct GpTotals {  // per lane k of warp 0: L[k], N[k]; every lane: c[0..3]
 // l(a, j+1) = fma(a, l(a, j), 1) advanced once each time min(k, cap_i) grows, op-for-op a
 // fresh evaluation); warp sums are exact redux.sync limb sums, then one shared-memory step.
 constexpr int kGpCapCache = 4;  // caps kept in registers for k_i = min(k*, cap_i) (B <= 4 NT)
+// Global alpha: every request's term depends only on j_i = clamp(cap_i, 0, k_max), so the batch sums
+// follow from the histogram n_j of the j_i:  L[k] = sum_j n_j rint(2^32 l(alpha, min(k, j))) and
+// N[k] = sum_j n_j min(k, j) -- the same exact int64 values as summing the requests' terms one by one
+// (integer addition is exact and order-free; each term is the same function of (alpha, min(k, j_i))).
+// l(alpha, j) is evaluated once per j by warp 0 with the same Horner recurrence.  The histogram needs
+// one redux per bin instead of a Horner chain and 64-bit conversions per request.
+#ifndef TSV_GP_HISTOGRAM
+#define TSV_GP_HISTOGRAM 1
+#endif
+template <int NT>
+__device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int32_t* cap_cache) {
+    constexpr int NW = NT / 32;
+    __shared__ uint32_t sH[NW][kGpMaxK];
+    __shared__ long long sC[NW][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t B = A.B, k_max = A.k_max;
+    uint32_t cnt[kGpMaxK];
+#pragma unroll
+    for (int j = 0; j < kGpMaxK; ++j) cnt[j] = 0;
+    long long n_ctx = 0, n_ctx_spec = 0;
+    const double a = warp == 0 ? __ldcg(A.alpha) : 0.0;  // issued with the caps: one round trip for both
+    int slot = 0;
+    for (int32_t i = threadIdx.x; i < B; i += NT, ++slot) {
+        const int32_t ci = __ldcg(A.cap + i);
+        if (cap_cache && slot < kGpCapCache) cap_cache[slot] = ci;
+        const int32_t cl = __ldcg(A.ctx_len + i);
+        n_ctx += cl;
+        if (ci > 0) n_ctx_spec += cl;
+        const int32_t j = ci < 0 ? 0 : (ci > k_max ? k_max : ci);
+#pragma unroll
+        for (int b = 0; b < kGpMaxK; ++b) cnt[b] += (b == j) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int b = 0; b < kGpMaxK; ++b) {
+        if (b <= k_max) {
+            const uint32_t h = __reduce_add_sync(0xFFFFFFFFu, cnt[b]);
+            if (lane == 0) sH[warp][b] = h;
+        }
+    }
+    n_ctx = warp_sum_i64(n_ctx);
+    n_ctx_spec = warp_sum_i64(n_ctx_spec);
+    if (lane == 0) {
+        sC[warp][0] = n_ctx;
+        sC[warp][1] = n_ctx_spec;
+    }
+    __syncthreads();
+    GpTotals t = {0, 0, 0, 0, 0, static_cast<long long>(B)};
+    if (warp == 0) {
+        long long nj = 0;  // lane j: n_j
+        if (lane <= k_max)
+#pragma unroll
+            for (int w = 0; w < NW; ++w) nj += sH[w][lane];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            t.c0 += sC[w][0];
+            t.c1 += sC[w][1];
+        }
+        // lane j: fix_j = rint(2^32 l(alpha, j)), l by the Horner recurrence from 1.0, j steps
+        double l = 1.0;
+        for (int s = 0; s < lane && s < k_max; ++s) l = __fma_rn(a, l, 1.0);
+        const long long fix_j = __double2ll_rn(l * 0x1p32);
+        // lane k: L[k] = sum_{j<k} n_j fix_j + (sum_{j>=k} n_j) fix_k;  N[k] = sum_j n_j min(k, j)
+        long long Lk = 0, Nk = 0, tail = 0;
+        for (int j = 0; j <= k_max; ++j) {
+            const long long n_ = __shfl_sync(0xFFFFFFFFu, nj, j);
+            const long long f_ = __shfl_sync(0xFFFFFFFFu, fix_j, j);
+            if (j < lane) {
+                Lk += n_ * f_;
+                Nk += n_ * j;
+            } else {
+                tail += n_;
+            }
+        }
+        if (lane <= k_max) {
+            t.L = Lk + tail * fix_j;
+            t.N = Nk + tail * lane;
+        }
+        t.c2 = B - __shfl_sync(0xFFFFFFFFu, nj, 0);  // #{cap_i > 0}
+    }
+    return t;
+}
+
 template <int NT = kGpThreads>
 __device__ __forceinline__ GpTotals gp_sums_block(const ChooseArgs& A, int32_t* cap_cache = nullptr) {
+    if (TSV_GP_HISTOGRAM && !A.alpha_per_request) return gp_sums_block_hist<NT>(A, cap_cache);
     constexpr int NW = NT / 32;
     __shared__ long long sL[NW][kGpMaxK];
     __shared__ long long sN[NW][kGpMaxK];
