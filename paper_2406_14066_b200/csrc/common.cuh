@@ -266,7 +266,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 #endif
 #if TSV_STEP_TRACE
 constexpr unsigned kStepTraceMax = 1u << 16;
-static __device__ unsigned long long g_step_tr[kStepTraceMax][4];
+static __device__ unsigned long long g_step_tr[kStepTraceMax][6];
 static __device__ unsigned int g_step_tr_n;
 __device__ __forceinline__ unsigned long long step_ns() {
     unsigned long long t;
@@ -274,10 +274,11 @@ __device__ __forceinline__ unsigned long long step_ns() {
     return t;
 }
 struct StepTrace {
-    unsigned long long t0, t1;
+    unsigned long long t0, t1, m1, m2;
     int id;
-    __device__ explicit StepTrace(int i) : t0(step_ns()), t1(0), id(i) {}
+    __device__ explicit StepTrace(int i) : t0(step_ns()), t1(0), m1(0), m2(0), id(i) {}
     __device__ void waited() { t1 = step_ns(); }
+    __device__ void mark(int n) { (n == 1 ? m1 : m2) = step_ns(); }
     __device__ ~StepTrace() {
         if (threadIdx.x == 0) {
             const unsigned k = atomicAdd(&g_step_tr_n, 1u);
@@ -286,19 +287,22 @@ struct StepTrace {
                 g_step_tr[k][1] = t0;
                 g_step_tr[k][2] = t1;
                 g_step_tr[k][3] = step_ns();
+                g_step_tr[k][4] = m1;
+                g_step_tr[k][5] = m2;
             }
         }
     }
 };
 #define TSV_STEP_SPAN(id) ::tsv::StepTrace tsv_step_span_(id)
 #define TSV_STEP_WAITED() tsv_step_span_.waited()
+#define TSV_STEP_MARK(n) tsv_step_span_.mark(n)
 #define TSV_STEP_TRACE_READER(name)                                                                   \
     extern "C" TSV_API unsigned tsv_debug_step_trace_##name(unsigned long long* out, unsigned max_n) { \
         unsigned n = 0;                                                                               \
         cudaMemcpyFromSymbol(&n, ::tsv::g_step_tr_n, sizeof(n));                                      \
         n = n < max_n ? n : max_n;                                                                    \
         if (n > ::tsv::kStepTraceMax) n = ::tsv::kStepTraceMax;                                       \
-        cudaMemcpyFromSymbol(out, ::tsv::g_step_tr, n * 4 * sizeof(unsigned long long));              \
+        cudaMemcpyFromSymbol(out, ::tsv::g_step_tr, n * 6 * sizeof(unsigned long long));              \
         unsigned z = 0;                                                                               \
         cudaMemcpyToSymbol(::tsv::g_step_tr_n, &z, sizeof(z));                                        \
         return n;                                                                                     \
@@ -309,6 +313,9 @@ struct StepTrace {
     } while (0)
 #define TSV_STEP_WAITED() \
     do {                  \
+    } while (0)
+#define TSV_STEP_MARK(n) \
+    do {                 \
     } while (0)
 #define TSV_STEP_TRACE_READER(name)
 #endif

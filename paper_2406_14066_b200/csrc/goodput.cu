@@ -28,7 +28,25 @@ __global__ void __launch_bounds__(kGpChooseThreads) goodput_choose_k_kernel(cons
     pdl_wait();
     TSV_STEP_WAITED();
     pdl_launch_dependents();
+#if TSV_STEP_TRACE
+    {  // choose_k_block with marks: m1 after the batch sums, m2 after Listing 2's argmax
+        __shared__ int s_best;
+        int32_t caps[kGpCapCache];
+        const GpTotals t = gp_sums_block<kGpChooseThreads>(A, caps);
+        TSV_STEP_MARK(1);
+        if ((threadIdx.x >> 5) == 0) {
+            const int kb = gp_argmax_warp(A, t);
+            if (threadIdx.x == 0) s_best = kb;
+        }
+        TSV_STEP_MARK(2);
+        if (A.k_per_request) {
+            __syncthreads();
+            gp_write_k_per_request<kGpChooseThreads>(A, s_best, caps);
+        }
+    }
+#else
     choose_k_block<kGpChooseThreads>(A);
+#endif
 }
 
 // Request-sharded ArgMaxGoodput in ONE kernel (the exchange step fused with its

@@ -30,7 +30,7 @@ readers = [getattr(L, f"tsv_debug_step_trace_{n}") for n in ("lookup", "goodput"
 for r in readers:
     r.argtypes = [ctypes.c_void_p, ctypes.c_uint32]
     r.restype = ctypes.c_uint32
-buf = np.zeros((1 << 16, 4), np.uint64)
+buf = np.zeros((1 << 16, 6), np.uint64)
 
 
 def read_all():
@@ -64,12 +64,14 @@ for k in range(5):
     for j in range(len(steps)):
         s_ = sel[j * n:(j + 1) * n]
         w = t_wait[s_]
-        launches.append((j, k, t_in[s_].min(), w[w > 0].min() if (w > 0).any() else 0, t_out[s_].max()))
+        m1, m2 = ev[s_, 4].astype(np.int64), ev[s_, 5].astype(np.int64)
+        launches.append((j, k, t_in[s_].min(), w[w > 0].min() if (w > 0).any() else 0, t_out[s_].max(),
+                         m1.max(), m2.max()))
 launches.sort(key=lambda x: (x[0], x[1]))
 t0 = min(l[2] for l in launches)
-print(f"{'step':>4} {'kernel':>9} {'entry':>8} {'waited':>8} {'exit':>8}   (us from the graph's first entry)")
-prev_exit = None
-for j, k, a, w, b in launches:
-    print(f"{j:>4} {names[k]:>9} {(a - t0) / 1e3:8.2f} {(w - t0) / 1e3 if w else float('nan'):8.2f} {(b - t0) / 1e3:8.2f}")
-ends = [b for j, k, a, w, b in launches if k == 4]
+print(f"{'step':>4} {'kernel':>9} {'entry':>8} {'waited':>8} {'exit':>8} {'mark1':>8} {'mark2':>8}  (us from the first entry)")
+for j, k, a, w, b, m1, m2 in launches:
+    f = lambda x: (x - t0) / 1e3 if x else float("nan")  # noqa: E731
+    print(f"{j:>4} {names[k]:>9} {f(a):8.2f} {f(w):8.2f} {f(b):8.2f} {f(m1):8.2f} {f(m2):8.2f}")
+ends = [l[4] for l in launches if l[1] == 4]
 print("emit-to-emit (us per step):", np.round(np.diff(ends) / 1e3, 2))
