@@ -115,13 +115,14 @@ template <int NT>
 __device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int32_t* cap_cache) {
     constexpr int NW = NT / 32;
     __shared__ uint32_t sH[NW][kGpMaxK];
-    __shared__ long long sC[NW][2];
+    __shared__ long long sC[NW][3];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t B = A.B, k_max = A.k_max;
     uint32_t cnt[kGpMaxK];
 #pragma unroll
     for (int j = 0; j < kGpMaxK; ++j) cnt[j] = 0;
     long long n_ctx = 0, n_ctx_spec = 0;
+    uint32_t b_spec = 0;  // #{cap_i > 0} (not n_0's complement: with k_max = 0 every j_i is 0)
     const double a = warp == 0 ? __ldcg(A.alpha) : 0.0;  // issued with the caps: one round trip for both
     int slot = 0;
     for (int32_t i = threadIdx.x; i < B; i += NT, ++slot) {
@@ -129,7 +130,10 @@ __device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int3
         if (cap_cache && slot < kGpCapCache) cap_cache[slot] = ci;
         const int32_t cl = __ldcg(A.ctx_len + i);
         n_ctx += cl;
-        if (ci > 0) n_ctx_spec += cl;
+        if (ci > 0) {
+            n_ctx_spec += cl;
+            b_spec += 1;
+        }
         const int32_t j = ci < 0 ? 0 : (ci > k_max ? k_max : ci);
 #pragma unroll
         for (int b = 0; b < kGpMaxK; ++b) cnt[b] += (b == j) ? 1u : 0u;
@@ -143,9 +147,11 @@ __device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int3
     }
     n_ctx = warp_sum_i64(n_ctx);
     n_ctx_spec = warp_sum_i64(n_ctx_spec);
+    const uint32_t b_spec_w = __reduce_add_sync(0xFFFFFFFFu, b_spec);
     if (lane == 0) {
         sC[warp][0] = n_ctx;
         sC[warp][1] = n_ctx_spec;
+        sC[warp][2] = b_spec_w;
     }
     __syncthreads();
     GpTotals t = {0, 0, 0, 0, 0, static_cast<long long>(B)};
@@ -158,6 +164,7 @@ __device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int3
         for (int w = 0; w < NW; ++w) {
             t.c0 += sC[w][0];
             t.c1 += sC[w][1];
+            t.c2 += sC[w][2];
         }
         // lane j: fix_j = rint(2^32 l(alpha, j)), l by the Horner recurrence from 1.0, j steps
         double l = 1.0;
@@ -179,7 +186,6 @@ __device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int3
             t.L = Lk + tail * fix_j;
             t.N = Nk + tail * lane;
         }
-        t.c2 = B - __shfl_sync(0xFFFFFFFFu, nj, 0);  // #{cap_i > 0}
     }
     return t;
 }

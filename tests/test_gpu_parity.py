@@ -745,6 +745,35 @@ def test_goodput_sharded_sums_equal_oracle(tsv):
             assert (kp == np.maximum(np.minimum(ok, cap[idx]), 0)).all()
 
 
+def test_goodput_histogram_sums_equal_per_request_sums(tsv):
+    # a global alpha takes the histogram path (sums from the counts of clamp(cap_i, 0, K)); the same
+    # alpha given per request takes the per-request path: the exact int64 sums must be identical,
+    # including K = 0, negative caps and caps above K (every word of the partial: L, N, sum ctx_len,
+    # sum ctx_len over cap > 0, #{cap > 0}, B)
+    rng = np.random.Generator(np.random.PCG64(12))
+    for trial in range(40):
+        B = int(rng.integers(1, 700))
+        K = int(rng.integers(0, 9)) if trial % 4 else 0
+        ctx = rng.integers(0, 5000, B).astype(np.int32)
+        cap = rng.integers(-2, K + 4, B).astype(np.int32)
+        a = float(rng.uniform(0, 1))
+        c, cp = torch.tensor(ctx, device=DEV), torch.tensor(cap, device=DEV)
+        hist = tsv.tsv_goodput_partial(torch.tensor([a], dtype=torch.float64, device=DEV), c, cp, K,
+                                       alpha_per_request=False)
+        per = tsv.tsv_goodput_partial(torch.full((B,), a, dtype=torch.float64, device=DEV), c, cp, K,
+                                      alpha_per_request=True)
+        torch.cuda.synchronize()
+        assert torch.equal(hist, per), (trial, K, _np(hist), _np(per))
+        capc = np.maximum(cap, 0).astype(np.int32)  # the oracle's caps are counts (>= 0)
+        for pol in (0, 1):
+            target, draft = PROFILES[pol]
+            ok, og = oracle.choose_k(a, ctx, capc, K, pol, target, draft, pld_cost_ms=0.05)
+            k, g, _ = tsv.tsv_goodput_choose_k(torch.tensor([a], dtype=torch.float64, device=DEV), c,
+                                               torch.tensor(capc, device=DEV), K, pol, target, draft, 0.05)
+            torch.cuda.synchronize()
+            assert int(k.item()) == ok and (_np(g).view(np.uint64) == og.view(np.uint64)).all(), (trial, K, pol)
+
+
 def test_update_sharded_sums_equal_oracle(tsv):
     rng = np.random.Generator(np.random.PCG64(9))
     for trial in range(40):
