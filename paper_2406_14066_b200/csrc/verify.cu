@@ -95,8 +95,19 @@ __device__ __forceinline__ float race_lower_bound(float w, float omu) {
     return __fmul_rd(__fmul_rd(w, u), __fmul_rd(rcp_approx(omu), kLbC));
 }
 
+#ifndef TSV_RACE_FTZ
+#define TSV_RACE_FTZ 1
+#endif
 __device__ __forceinline__ float prune_scale(float T) {
+#if TSV_RACE_FTZ
+    // one flush-to-zero multiply: a subnormal T, or a product below the normal range, gives Tc = 0
+    // (nothing with w > 0 is skipped), as conservative as the explicit test it replaces
+    float r;
+    asm("mul.rm.ftz.f32 %0, %1, %2;" : "=f"(r) : "f"(T), "f"(kPruneC));
+    return r;
+#else
     return T >= kMinNormal ? __fmul_rd(T, kPruneC) : 0.0f;
+#endif
 }
 
 struct Race;
@@ -117,17 +128,17 @@ __device__ unsigned long long g_exact_count[4];
 struct Race {
     float T, Tc, Th, Tloc;
     uint64_t best;
-    bool has_pend;
+    // the parked candidate: pend_w > 0 iff one is parked (only w > 0 is ever parked); its 1 - u
+    // determines E(u) exactly (race_E_omu), so the Philox word itself is not kept
     float pend_w, pend_omu;
-    uint32_t pend_x, pend_v;
+    uint32_t pend_v;
 
     __device__ __forceinline__ void init() {
         T = Tc = Th = Tloc = 0.0f;
         best = 0;
-        has_pend = false;
         pend_w = 0.0f;
         pend_omu = 1.0f;
-        pend_x = pend_v = 0;
+        pend_v = 0;
     }
 
     __device__ __forceinline__ void set_T(float t) {
@@ -136,11 +147,11 @@ struct Race {
         Th = __fmul_ru(Tc, 0x1.000002p+0f);
     }
 
-    __device__ __forceinline__ void eval_exact(float w, uint32_t x, uint32_t vg) {
+    __device__ __forceinline__ void eval_exact(float w, float omu, uint32_t vg) {
 #if TSV_COUNT_EXACT
         atomicAdd(&g_exact_count[0], 1ull);
 #endif
-        const uint64_t key = exact_race_key(w, x, vg);
+        const uint64_t key = pack_key(__fdiv_rn(w, race_E_omu(omu)), vg);  // = exact_race_key(w, x, vg)
         best = key > best ? key : best;
         Tloc = fmaxf(Tloc, __uint_as_float(static_cast<uint32_t>(best >> 32)));
     }
@@ -163,7 +174,7 @@ struct Race {
         if constexpr (!PRUNE) {
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-                if (w[e] > 0.0f) eval_exact(w[e], rw[e], v0 + e);
+                if (w[e] > 0.0f) eval_exact(w[e], one_minus_u_race(rw[e]), v0 + e);
         } else {
             bool cand[4];
 #pragma unroll
@@ -173,16 +184,17 @@ struct Race {
             atomicAdd(&g_exact_count[1], static_cast<unsigned long long>(cand[0] + cand[1] + cand[2] + cand[3]));
 #endif
             if (cand[0] | cand[1] | cand[2] | cand[3]) {
+#if TSV_COUNT_EXACT
+                if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(&g_exact_count[3], 32ull);  // warp entries
+#endif
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     if (cand[e] && w[e] > 0.0f) {
                         const float omu = one_minus_u_race(rw[e]);
                         Tloc = fmaxf(Tloc, race_lower_bound(w[e], omu));
-                        if (has_pend && pend_w > __fmul_rd(Tc, pend_omu)) eval_exact(pend_w, pend_x, pend_v);
-                        has_pend = true;
+                        if (pend_w > __fmul_rd(Tc, pend_omu)) eval_exact(pend_w, pend_omu, pend_v);
                         pend_w = w[e];
                         pend_omu = omu;
-                        pend_x = rw[e];
                         pend_v = v0 + e;
                     }
                 }
@@ -199,8 +211,8 @@ struct Race {
     __device__ __forceinline__ void finish(float T_final) {
         if constexpr (PRUNE) {
             const float tc = prune_scale(T_final);
-            if (has_pend && pend_w > __fmul_rd(tc, pend_omu)) eval_exact(pend_w, pend_x, pend_v);
-            has_pend = false;
+            if (pend_w > __fmul_rd(tc, pend_omu)) eval_exact(pend_w, pend_omu, pend_v);
+            pend_w = 0.0f;
         }
     }
 };
@@ -230,6 +242,25 @@ __device__ __forceinline__ void quad_weights(float (&w)[4], const float4& a, con
 #pragma unroll
         for (int e = 0; e < 4; ++e)
             if (col + e >= col_end) w[e] = 0.0f;
+    }
+}
+
+// Weights of one float4 in the streaming loop: p (w, already loaded), minus q (dense, when use_q) or
+// minus the one-hot draft at local column xm (one-hot q on a rejection); col: the float4's local column.
+template <bool DENSE_Q>
+__device__ __forceinline__ void race_weights(float (&w)[4], const float4& b, bool use_q, bool residual, int32_t col,
+                                             int32_t xm) {
+    if (DENSE_Q) {
+        if (use_q) {
+            w[0] = __fsub_rn(w[0], b.x);
+            w[1] = __fsub_rn(w[1], b.y);
+            w[2] = __fsub_rn(w[2], b.z);
+            w[3] = __fsub_rn(w[3], b.w);
+        }
+    } else if (residual && (col >> 2) == (xm >> 2)) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (col + e == xm) w[e] = __fsub_rn(w[e], 1.0f);
     }
 }
 
@@ -498,6 +529,9 @@ constexpr int kRaceWarps = kRaceThreads / 32;
 #define TSV_RACE_UNROLL 2
 #endif
 constexpr int kUnroll = TSV_RACE_UNROLL;
+#ifndef TSV_RACE_LOOP2
+#define TSV_RACE_LOOP2 1
+#endif
 
 #ifndef TSV_TRACE
 #define TSV_TRACE 0
@@ -576,7 +610,65 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
         R.init();
         const int32_t nfull = (col_end - col_begin) >> 7;  // iterations with all 128 columns in range
         int32_t it = 0;
-        for (; it + kUnroll <= nfull; it += kUnroll) {
+#if TSV_RACE_LOOP2
+        if (!LOGITS) {
+            // Full steps with explicit pointer / counter increments: kUnroll float4 of p (and of q on a
+            // rejection) per lane per step, the Philox quad counter advancing by 32 per float4.  q is only
+            // loaded (and only subtracted) when use_q, and nothing else is kept live for the tail loop.
+            // rem (columns left in the chunk) is the loop counter and the tail's bound: nothing else about the
+            // chunk stays live across the streaming loop
+            int32_t rem = col_end - col_begin;
+            const float4* pp = prow + lane;
+            const float4* qp = qrow + lane;
+            uint32_t ctr = (vbase >> 2) + static_cast<uint32_t>(col_begin >> 2) + static_cast<uint32_t>(lane);
+            for (; rem >= 128 * kUnroll; rem -= 128 * kUnroll) {
+                float4 a[kUnroll], b[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) a[u] = ldg_stream(pp + 32 * u);
+                if (use_q) {
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) b[u] = ldg_stream(qp + 32 * u);
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const uint32_t cu = ctr + 32u * u;
+                    const uint4 r = philox_race(rc, cu, P);
+                    float w[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+                    race_weights<DENSE_Q>(w, b[u], use_q, residual, static_cast<int32_t>(4u * (cu - (vbase >> 2))),
+                                          xm_local);
+                    if (PRUNE && u == 0 && R.T == 0.0f) R.warm(w, r);
+                    R.quad<PRUNE>(w, r, vbase + 4u * (cu - (vbase >> 2)));
+                }
+                if (PRUNE) R.sync_T();
+                pp += 32 * kUnroll;
+                qp += 32 * kUnroll;
+                ctr += 32u * kUnroll;
+            }
+            // the rest of the chunk (< 128 kUnroll columns): one float4 per lane per step, masked at rem
+            for (int32_t f0 = 0; 4 * f0 < rem; f0 += 32, pp += 32, qp += 32, ctr += 32) {
+                float w[4] = {0.f, 0.f, 0.f, 0.f};
+                uint4 r = make_uint4(0, 0, 0, 0);
+                const int32_t cl = 4 * (f0 + lane);  // column offset inside the rest
+                if (cl < rem) {
+                    const float4 a = ldg_stream(pp);
+                    float4 b = a;
+                    if (use_q) b = ldg_stream(qp);
+                    w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w;
+                    race_weights<DENSE_Q>(w, b, use_q, residual, static_cast<int32_t>(4u * (ctr - (vbase >> 2))),
+                                          xm_local);
+#pragma unroll
+                    for (int e = 1; e < 4; ++e)
+                        if (cl + e >= rem) w[e] = 0.0f;
+                    r = philox_race(rc, ctr, P);
+                }
+                if (PRUNE && R.T == 0.0f) R.warm(w, r);
+                R.quad<PRUNE>(w, r, vbase + 4u * (ctr - (vbase >> 2)));
+                if (PRUNE) R.sync_T();
+            }
+            it = iters;
+        }
+#endif
+        for (; !(TSV_RACE_LOOP2 && !LOGITS) && it + kUnroll <= nfull; it += kUnroll) {
             float4 a[kUnroll], b[kUnroll];
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) a[u] = ldg_stream(prow + (it + u) * 32 + lane);
@@ -1482,7 +1574,7 @@ static int sm_count();
 // (148 SMs x 4 CTAs x 8 warps), in whole 128-column iterations.  Never changes results.
 static int32_t auto_chunk(const tsv_verify_args* a) {
     if (a->chunk > 0) return a->chunk;
-    const int64_t warps = static_cast<int64_t>(sm_count()) * 32;  // resident warps of the race kernel
+    const int64_t warps = static_cast<int64_t>(sm_count()) * kRaceWarps * TSV_RACE_MINB;  // resident race warps
     // chunks per row so that B * chunks <= warps (one wave), then the chunk covering V in that many
     const int64_t per_row = std::max<int64_t>(1, warps / std::max<int32_t>(a->B, 1));
     int64_t c = (a->vocab + per_row - 1) / per_row;

@@ -22,8 +22,9 @@ for lam in (0.7, 0.3, 0.9):
         tsv.tsv_verify_accept(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 240614066, step, 8)
     torch.cuda.synchronize()
     f(ctypes.cast(out, ctypes.c_void_p))
-    ex, cand, quads = out[0] / 4, out[1] / 4, out[2] / 4
+    ex, cand, quads, went = out[0] / 4, out[1] / 4, out[2] / 4, out[3] / 4 / 32
     el = quads * 4  # the quad counter counts per lane
     print(f"lambda {lam}: per call exact evals {ex:.0f}, prune candidates {cand:.0f}, elements {el:.0f}; "
           f"candidates/element {cand / max(1, el):.4f}, exact/element {ex / max(1, el):.5f}, "
-          f"exact per row (256 x ~1.6 rows) {ex / 418:.0f}")
+          f"exact per row (256 x ~1.6 rows) {ex / 418:.0f}; warp entries into the candidate path {went:.0f} "
+          f"(of {quads / 32:.0f} warp-quads)")
