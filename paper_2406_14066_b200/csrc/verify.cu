@@ -110,6 +110,34 @@ __device__ __forceinline__ float prune_scale(float T) {
 #endif
 }
 
+// Packed fp32 pairs (sm_100 FADD2 / FFMA2: two IEEE binary32 operations per instruction, each
+// rounded exactly as its scalar form).
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {  // RN(a - b) per lane
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ void f2_sub_if(uint64_t& a, uint64_t b, bool on) {  // a = RN(a - b) per lane if on
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q sub.rn.f32x2 %0, %0, %1;\n\t}"
+        : "+l"(a)
+        : "l"(b), "r"(static_cast<uint32_t>(on)));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {  // RN(a b + c) per lane
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 struct Race;
 #ifndef TSV_COUNT_EXACT
 #define TSV_COUNT_EXACT 0
@@ -200,6 +228,38 @@ struct Race {
                 }
             }
         }
+    }
+
+    // The same race step with the prune values precomputed two at a time (TSV_RACE_F32X2):
+    // s[e] = RN(w_e - Tc F_e) = -RN(Tc F_e - w_e) exactly (round-to-nearest is symmetric), so
+    // "t < Th" is "s > -Th".
+    // cu: the float4's Philox quad counter, vbase: the vocab offset; its global index is 4 cu + (vbase & 3),
+    // formed on the candidate path only.
+    __device__ __forceinline__ void quad_s(const float (&w)[4], const float (&sv)[4], const uint4& r, uint32_t cu,
+                                           int32_t vbase) {
+        const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+        const float nTh = -Th;
+        if (fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3])) > nTh) {
+#if TSV_COUNT_EXACT
+            if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(&g_exact_count[3], 32ull);  // warp entries
+#endif
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (sv[e] > nTh && w[e] > 0.0f) {
+                    const float omu = one_minus_u_race(rw[e]);
+                    Tloc = fmaxf(Tloc, race_lower_bound(w[e], omu));
+                    if (pend_w > __fmul_rd(Tc, pend_omu)) eval_exact(pend_w, pend_omu, pend_v);
+                    pend_w = w[e];
+                    pend_omu = omu;
+                    pend_v = 4u * cu + (static_cast<uint32_t>(vbase) & 3u) + e;
+                }
+            }
+        }
+#if TSV_COUNT_EXACT
+        atomicAdd(&g_exact_count[2], 1ull);
+        atomicAdd(&g_exact_count[1], static_cast<unsigned long long>((sv[0] > nTh) + (sv[1] > nTh) + (sv[2] > nTh) +
+                                                                     (sv[3] > nTh)));
+#endif
     }
 
     __device__ __forceinline__ void sync_T() {  // warp-wide max (REDUX on the float bits)
@@ -532,6 +592,9 @@ constexpr int kUnroll = TSV_RACE_UNROLL;
 #ifndef TSV_RACE_LOOP2
 #define TSV_RACE_LOOP2 1
 #endif
+#ifndef TSV_RACE_F32X2
+#define TSV_RACE_F32X2 1
+#endif
 
 #ifndef TSV_TRACE
 #define TSV_TRACE 0
@@ -621,8 +684,18 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
             const float4* pp = prow + lane;
             const float4* qp = qrow + lane;
             uint32_t ctr = (vbase >> 2) + static_cast<uint32_t>(col_begin >> 2) + static_cast<uint32_t>(lane);
+#if TSV_RACE_F32X2
+            // q registers: zero for a bonus row (never loaded), so w = p - q is one unconditional FADD2
+            float4 b[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) b[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
             for (; rem >= 128 * kUnroll; rem -= 128 * kUnroll) {
+#if TSV_RACE_F32X2
+                float4 a[kUnroll];
+#else
                 float4 a[kUnroll], b[kUnroll];
+#endif
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) a[u] = ldg_stream(pp + 32 * u);
                 if (use_q) {
@@ -633,11 +706,28 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
                 for (int u = 0; u < kUnroll; ++u) {
                     const uint32_t cu = ctr + 32u * u;
                     const uint4 r = philox_race(rc, cu, P);
+#if TSV_RACE_F32X2
+                    if (PRUNE && DENSE_Q) {
+                        // w = p - q (FADD2 on a rejection), s = w - Tc F (FFMA2 with -Tc on both lanes)
+                        uint64_t w01 = f2_pack(a[u].x, a[u].y), w23 = f2_pack(a[u].z, a[u].w);
+                        w01 = f2_sub(w01, f2_pack(b[u].x, b[u].y));  // p - 0 = p exactly for a bonus row
+                        w23 = f2_sub(w23, f2_pack(b[u].z, b[u].w));
+                        const float2 wa = f2_unpack(w01), wb = f2_unpack(w23);
+                        float w[4] = {wa.x, wa.y, wb.x, wb.y};
+                        if (u == 0 && R.T == 0.0f) R.warm(w, r);
+                        const uint64_t ntc = f2_pack(-R.Tc, -R.Tc);
+                        const float2 sa = f2_unpack(f2_fma(ntc, f2_pack(race_F(r.x), race_F(r.y)), w01));
+                        const float2 sb = f2_unpack(f2_fma(ntc, f2_pack(race_F(r.z), race_F(r.w)), w23));
+                        const float sv[4] = {sa.x, sa.y, sb.x, sb.y};
+                        R.quad_s(w, sv, r, cu, P.vocab_offset);
+                        continue;
+                    }
+#endif
                     float w[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
                     race_weights<DENSE_Q>(w, b[u], use_q, residual, static_cast<int32_t>(4u * (cu - (vbase >> 2))),
                                           xm_local);
                     if (PRUNE && u == 0 && R.T == 0.0f) R.warm(w, r);
-                    R.quad<PRUNE>(w, r, vbase + 4u * (cu - (vbase >> 2)));
+                    R.quad<PRUNE>(w, r, 4u * cu + (vbase & 3u));  // = vbase + col
                 }
                 if (PRUNE) R.sync_T();
                 pp += 32 * kUnroll;
@@ -662,7 +752,7 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
                     r = philox_race(rc, ctr, P);
                 }
                 if (PRUNE && R.T == 0.0f) R.warm(w, r);
-                R.quad<PRUNE>(w, r, vbase + 4u * (ctr - (vbase >> 2)));
+                R.quad<PRUNE>(w, r, 4u * ctr + (vbase & 3u));
                 if (PRUNE) R.sync_T();
             }
             it = iters;
