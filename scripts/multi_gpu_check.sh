@@ -17,6 +17,10 @@ for n in 2 4 8; do
   for m in lazy p2p p2p_fused; do
     run --workload config4 --shard-mode $m > gpurun_out/scale_c4_${m}_$n.json 2> gpurun_out/scale_c4_${m}_$n.err; echo "config4 $m N=$n rc=$?"
   done
+  # the lazy mode's key all-reduce is ncclAllReduce(max, uint64): NCCL's algorithm choice (NVLS = in-switch
+  # reduction) is in its INFO log
+  NCCL_DEBUG=INFO NCCL_DEBUG_SUBSYS=INIT,COLL,TUNING run --workload config4 --shard-mode lazy --steps 8 --warmup 3 \
+      > /dev/null 2> gpurun_out/nccl_c4_lazy_$n.log; echo "config4 lazy NCCL log N=$n rc=$? NVLS lines: $(grep -ci nvls gpurun_out/nccl_c4_lazy_$n.log)"
 done
 nvcc -gencode arch=compute_100a,code=sm_100a -o /tmp/probe_multicast scripts/probe_multicast.cu -lcuda && \
   timeout 60 /tmp/probe_multicast > gpurun_out/probe_multicast.log 2>&1; tail -3 gpurun_out/probe_multicast.log
