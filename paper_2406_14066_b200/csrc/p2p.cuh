@@ -126,6 +126,29 @@ __device__ __forceinline__ void p2p_allreduce_block(long long* v, int32_t count,
     if (threadIdx.x == 0) *p2p_sums_epoch(V) = e;
 }
 
+// The same exchange for a pair held by ONE warp (the race grid's update warp): lane j < 2 publishes and
+// sums word j; every lane returns with both sums.
+__device__ __forceinline__ void p2p_allreduce_warp(long long& a, long long& b, const P2PView& V, int32_t* devstatus) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t e = *reinterpret_cast<volatile uint32_t*>(p2p_sums_epoch(V)) + 1u;
+    if (lane < 2) {
+        const uint64_t x = static_cast<uint64_t>(lane == 0 ? a : b);
+        for (int32_t g = 0; g < V.G; ++g)
+            st_ll(p2p_sums(V, e, g, V.rank, lane), make_uint4(static_cast<uint32_t>(x), e, static_cast<uint32_t>(x >> 32), e));
+        uint64_t sum = 0;
+        for (int32_t g = 0; g < V.G; ++g) {
+            const uint4 w = ld_ll_wait(p2p_sums(V, e, V.rank, g, lane), e, devstatus);
+            sum += (static_cast<uint64_t>(w.z) << 32) | w.x;
+        }
+        if (lane == 0) a = static_cast<long long>(sum);
+        else b = static_cast<long long>(sum);
+    }
+    a = __shfl_sync(0xFFFFFFFFu, a, 0);
+    b = __shfl_sync(0xFFFFFFFFu, b, 1);
+    __syncwarp();  // both lanes have read the epoch and finished their slots
+    if (lane == 0) *p2p_sums_epoch(V) = e;
+}
+
 }  // namespace tsv
 
 // The opaque handle of include/tsv.h.
