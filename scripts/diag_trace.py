@@ -95,3 +95,13 @@ for us, buf in res:
     bins = np.arange(0, end.max() + 0.5, 0.5)
     inflight = [int(((start <= b) & (end > b)).sum()) for b in bins]
     print("  items in flight every 0.5 us:", inflight)
+    # per-SM load vs finish: residual items (2x bytes) per SM against the SM's last item end
+    sms = np.unique(sm)
+    nres = np.array([resid[sm == k].sum() for k in sms])
+    nit = np.array([(sm == k).sum() for k in sms])
+    units = nit + nres  # bonus 1 unit, residual 2 units of bytes
+    cc = np.corrcoef(units, sm_max)[0, 1]
+    print(f"  per-SM byte units (items + residual items): min {units.min()} p50 {np.median(units):.0f} max {units.max()} "
+          f"| corr(units, SM last end) {cc:.2f}; SM last end of the 10 lightest / heaviest SMs: "
+          f"{np.mean(sm_max[np.argsort(units)[:10]]):.2f} / {np.mean(sm_max[np.argsort(units)[-10:]]):.2f} us; "
+          f"per-SM mean end {np.mean([end[sm == k].mean() for k in sms]):.2f} us")
