@@ -633,9 +633,6 @@ constexpr int kRaceWarps = kRaceThreads / 32;
 #define TSV_RACE_UNROLL 2
 #endif
 constexpr int kUnroll = TSV_RACE_UNROLL;
-#ifndef TSV_RACE_LOOP2
-#define TSV_RACE_LOOP2 1
-#endif
 #ifndef TSV_RACE_F32X2
 #define TSV_RACE_F32X2 1
 #endif
@@ -715,16 +712,11 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
         const float4* prow = reinterpret_cast<const float4*>(P.p + static_cast<int64_t>(rm.r0 + sel) * P.ld + col_begin);
         const float4* qrow = use_q ? reinterpret_cast<const float4*>(P.q + static_cast<int64_t>(rm.qbase + sel) * P.ld + col_begin)
                                    : prow;
-        const int32_t nq = (col_end - col_begin + 3) >> 2;
-        const int32_t iters = (nq + 31) >> 5;
         const RaceCtr rc = race_ctr((kPurposeRace << 16) | static_cast<uint32_t>(sel), rm.rid, P.step, P.k0, P.k1);
         const float4 ls = LOGITS ? P.lstats[i] : make_float4(0.f, 0.f, 0.f, 0.f);  // row m's softmax stats
         Race R;
         R.init();
-        const int32_t nfull = (col_end - col_begin) >> 7;  // iterations with all 128 columns in range
-        int32_t it = 0;
-#if TSV_RACE_LOOP2
-        if (!LOGITS) {
+        {
             // Full steps with explicit pointer / counter increments: kUnroll float4 of p (and of q on a
             // rejection) per lane per step, the Philox quad counter advancing by 32 per float4.  q is only
             // loaded (and only subtracted) when use_q, and nothing else is kept live for the tail loop.
@@ -751,6 +743,13 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
                 if (use_q) {
 #pragma unroll
                     for (int u = 0; u < kUnroll; ++u) b[u] = ldg_stream(qp + 32 * u);
+                }
+                if (LOGITS) {  // probabilities from the logits on the fly (q only on a rejection: b stays zero)
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u) {
+                        a[u] = to_prob4(a[u], ls.x, ls.y, P.inv_tau);
+                        if (use_q) b[u] = to_prob4(b[u], ls.z, ls.w, P.inv_tau);
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
@@ -790,9 +789,13 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
                 uint4 r = make_uint4(0, 0, 0, 0);
                 const int32_t cl = 4 * (f0 + lane);  // column offset inside the rest
                 if (cl < rem) {
-                    const float4 a = ldg_stream(pp);
+                    float4 a = ldg_stream(pp);
                     float4 b = a;
                     if (use_q) b = ldg_stream(qp);
+                    if (LOGITS) {
+                        a = to_prob4(a, ls.x, ls.y, P.inv_tau);
+                        if (use_q) b = to_prob4(b, ls.z, ls.w, P.inv_tau);
+                    }
                     w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w;
                     race_weights<DENSE_Q>(w, b, use_q, residual, static_cast<int32_t>(4u * (ctr - (vbase >> 2))),
                                           xm_local);
@@ -805,51 +808,6 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
                 R.quad<PRUNE>(w, r, 4u * ctr + (vbase & 3u));
                 if (PRUNE) R.sync_T();
             }
-            it = iters;
-        }
-#endif
-        for (; !(TSV_RACE_LOOP2 && !LOGITS) && it + kUnroll <= nfull; it += kUnroll) {
-            float4 a[kUnroll], b[kUnroll];
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) a[u] = ldg_stream(prow + (it + u) * 32 + lane);
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) b[u] = use_q ? ldg_stream(qrow + (it + u) * 32 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (LOGITS) {
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    a[u] = to_prob4(a[u], ls.x, ls.y, P.inv_tau);
-                    if (use_q) b[u] = to_prob4(b[u], ls.z, ls.w, P.inv_tau);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                const int32_t col = col_begin + 4 * ((it + u) * 32 + lane);
-                const uint4 r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col >> 2), P);
-                float w[4];
-                quad_weights<DENSE_Q>(w, a[u], b[u], residual, col, 0x7FFFFFFF, xm_local);
-                if (PRUNE && u == 0 && R.T == 0.0f) R.warm(w, r);
-                R.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
-            }
-            if (PRUNE) R.sync_T();
-        }
-        for (; it < iters; ++it) {  // remaining iterations: bounds checks and column masking
-            const int32_t f = it * 32 + lane;
-            const int32_t col = col_begin + 4 * f;
-            float w[4] = {0.f, 0.f, 0.f, 0.f};
-            uint4 r = make_uint4(0, 0, 0, 0);
-            if (f < nq) {
-                float4 a = ldg_stream(prow + f);
-                float4 b = use_q ? ldg_stream(qrow + f) : a;
-                if (LOGITS) {
-                    a = to_prob4(a, ls.x, ls.y, P.inv_tau);
-                    if (use_q) b = to_prob4(b, ls.z, ls.w, P.inv_tau);
-                }
-                quad_weights<DENSE_Q>(w, a, b, residual, col, col_end, xm_local);
-                r = philox_race(rc, (vbase >> 2) + static_cast<uint32_t>(col >> 2), P);
-            }
-            if (PRUNE && R.T == 0.0f) R.warm(w, r);
-            R.quad<PRUNE>(w, r, vbase + static_cast<uint32_t>(col));
-            if (PRUNE) R.sync_T();
         }
 #if TSV_TRACE
         const unsigned long long tr1 = gtimer();
