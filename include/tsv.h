@@ -480,9 +480,10 @@ TSV_API tsv_status tsv_update_acceptance(double* alpha, int32_t per_request, con
 
 /* Fused Accept + UpdateGlobalAcceptance (Listing 1 lines 18-19): tsv_verify_accept
  * followed by tsv_update_acceptance(alpha, per_request, a->num_accepted,
- * a->row_offsets, a->B, decay, estimator), with the update run by one extra CTA
- * of verify's race kernel (beside the race) -- the accepted counts are final after
- * the acceptance scan, so it needs no handshake.  Outputs identical to the two
+ * a->row_offsets, a->B, decay, estimator), with the update run beside the race by the
+ * race grid's last warp when it has no work item (else by one extra CTA of the race
+ * kernel) -- the accepted counts are final after the acceptance scan, so it needs no
+ * handshake.  Outputs identical to the two
  * separate calls; same workspace as tsv_verify_accept. */
 TSV_API tsv_status tsv_verify_accept_update(const tsv_verify_args* a, double* alpha, int32_t per_request,
                                     double decay, int32_t estimator, void* stream);
@@ -507,8 +508,8 @@ TSV_API tsv_status tsv_verify_accept_update_ex(const tsv_verify_args* a, double*
  *  tsv_update_acceptance_p2p: UpdateGlobalAcceptance with (sum m, sum t) summed over the
  *    ranks before the EWMA (every rank applies the same update); per_request != 0 updates
  *    the local alphas with no exchange.
- *  tsv_verify_accept_update_p2p: tsv_verify_accept_update whose update CTA (beside the
- *    race) performs that exchange -- the global alpha costs no extra launch.
+ *  tsv_verify_accept_update_p2p: tsv_verify_accept_update whose update warp / CTA (beside
+ *    the race) performs that exchange -- the global alpha costs no extra launch.
  * All ranks must make the same sequence of exchange calls (tsv_goodput_choose_k_p2p,
  * tsv_update_acceptance_p2p, tsv_verify_accept_update_p2p, tsv_allreduce_i64_p2p share
  * one epoch).  device_status (nullable) gets TSV_DEVSTATUS_P2P_TIMEOUT.

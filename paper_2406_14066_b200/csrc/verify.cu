@@ -16,8 +16,8 @@
 //     double-log + IEEE-division score of elements that cannot reach the best score seen,
 //     deferred exact evaluation of survivors, and a packed (score, ~index) u64 key per
 //     row combined with red.max.  No shared memory, no barriers in the race itself; with
-//     tsv_verify_accept_update one extra CTA runs the alpha update beside the race (the
-//     accepted counts are final after the scan).
+//     tsv_verify_accept_update the grid's item-less last warp (else one extra CTA) runs the
+//     alpha update beside the race (the accepted counts are final after the scan).
 //  3. verify_emit_kernel: one warp per request (or p row in shard mode) reads the row key,
 //     falls back to the p_m race when the residual was identically zero (R5), and emits
 //     the correction / bonus token (or the shard tuple).
@@ -64,7 +64,7 @@ struct RaceParams {
     int32_t meta_ready;         // TSV_VERIFY_META_READY: the scan reads row_offsets/drafts/rids before its wait
     int32_t early_trigger;      // TSV_VERIFY_EARLY_TRIGGER: the emit kernel triggers its dependents before its wait
     uint32_t* alpha_ready;      // nullable (tsv_verify_accept_update_ex): reset to 0 by the scan, set by the update
-    int32_t race_update;        // lazy race: one extra CTA runs the alpha update (ua) beside the race
+    int32_t race_update;        // lazy race: the alpha update (ua) beside the race (1: extra CTA, 2: last warp)
     UpdateArgs ua;
     int32_t push;               // TSV_VERIFY_P2P_FUSED: each race item pushes its chunk key to every rank (pv)
     P2PView pv;

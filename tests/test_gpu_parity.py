@@ -961,14 +961,18 @@ def test_alpha_ready_wait_times_out_without_producer(tsv):
     assert (_np(pl) == opl).all() and int(k.item()) == ok
 
 
+@pytest.mark.parametrize("chunk", [0, 128])
 @pytest.mark.parametrize("est", [0, 1])  # TESTED (default), PROPOSED
-def test_fused_verify_update_equals_separate(tsv, est):
-    # the fused update runs as an extra CTA of the race kernel: same alpha bits as the separate call
+def test_fused_verify_update_equals_separate(tsv, est, chunk):
+    # the fused update runs beside the race: on the race grid's item-less last warp (chunk 0: 4608 work items
+    # for 4736 warps) or as an extra CTA (chunk 128: 64000 items, every warp busy).  Same alpha bits as the
+    # separate call either way.
     vb = synth.make_verify_batch(B=256, V=32000, k_max=8, lam=0.7, seed=22).to(DEV)
     for per in (False, True):
         na = torch.empty(256, dtype=torch.int32, device=DEV)
         out = torch.empty((256, 9), dtype=torch.int32, device=DEV)
-        a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 7, 3, 8, na, out)
+        a = tsv.make_verify_args(vb.p, vb.q, vb.row_offsets, vb.draft_tokens, vb.request_ids, 7, 3, 8, na, out,
+                                 chunk=chunk)
         ws = tsv.alloc_workspace(tsv.tsv_verify_workspace_size(a), DEV)
         a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
         a0 = torch.rand(256 if per else 1, dtype=torch.float64, device=DEV, generator=torch.Generator(DEV).manual_seed(1))
