@@ -233,7 +233,10 @@ typedef struct tsv_verify_args {
                                   /* the preceding kernel" is not enough if that      */
                                   /* kernel itself triggered early.  The scan then    */
                                   /* reads them before its grid-dependency wait and   */
-                                  /* waits only before reading p and q.  Honoured by  */
+                                  /* waits only before reading p and q (it prefetches */
+                                  /* the p / q words it will gather into L2 before    */
+                                  /* the wait: no data is read, L2 is coherent for    */
+                                  /* writes).  Honoured by                            */
                                   /* tsv_verify_accept and tsv_verify_accept_update;  */
                                   /* ignored by every other entry point (sharded,     */
                                   /* greedy, logits).  libtsv's own kernels trigger   */

@@ -95,6 +95,9 @@ __device__ __forceinline__ float race_lower_bound(float w, float omu) {
     return __fmul_rd(__fmul_rd(w, u), __fmul_rd(rcp_approx(omu), kLbC));
 }
 
+#ifndef TSV_SCAN_PREFETCH
+#define TSV_SCAN_PREFETCH 1
+#endif
 #ifndef TSV_UPDATE_WARP
 #define TSV_UPDATE_WARP 1
 #endif
@@ -420,6 +423,17 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     bool bad = false, acc = false, own = false;
     if (ok && lane < k) x = P.drafts[qbase + lane];
     if (P.meta_ready) {
+#if TSV_SCAN_PREFETCH
+        // the words gathered below, into L2 while the previous kernel drains: a prefetch returns no data, and
+        // every write reaches L2 (the coherence point), so what is read after the wait is what was written
+        if (ok && lane < k && x >= 0 && x < P.vocab_global) {
+            const int32_t xl = x - P.vocab_offset;
+            if (xl >= 0 && xl < P.vocab) {
+                prefetch_l2(P.p + static_cast<int64_t>(r0 + lane) * P.ld + xl);
+                if (P.q) prefetch_l2(P.q + static_cast<int64_t>(qbase + lane) * P.ld + xl);
+            }
+        }
+#endif
         pdl_wait();
         TSV_STEP_WAITED();
         pdl_launch_dependents();
