@@ -422,16 +422,22 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     int32_t x = -1;
     bool bad = false, acc = false, own = false;
     if (ok && lane < k) x = P.drafts[qbase + lane];
+    // everything that does not read p or q: with META_READY before the wait (the acceptance uniform too)
+    const int32_t xl = x - P.vocab_offset;
+    if (ok && lane < k) {
+        bad = x < 0 || x >= P.vocab_global;
+        own = !bad && xl >= 0 && xl < P.vocab;
+    }
+    float u = 0.0f;
+    if (own) u = u_acc_from_word(philox4x32_10(0u, (kPurposeAccept << 16) | static_cast<uint32_t>(lane), rid, P.step,
+                                               P.k0, P.k1).x);
     if (P.meta_ready) {
 #if TSV_SCAN_PREFETCH
         // the words gathered below, into L2 while the previous kernel drains: a prefetch returns no data, and
         // every write reaches L2 (the coherence point), so what is read after the wait is what was written
-        if (ok && lane < k && x >= 0 && x < P.vocab_global) {
-            const int32_t xl = x - P.vocab_offset;
-            if (xl >= 0 && xl < P.vocab) {
-                prefetch_l2(P.p + static_cast<int64_t>(r0 + lane) * P.ld + xl);
-                if (P.q) prefetch_l2(P.q + static_cast<int64_t>(qbase + lane) * P.ld + xl);
-            }
+        if (own) {
+            prefetch_l2(P.p + static_cast<int64_t>(r0 + lane) * P.ld + xl);
+            if (P.q) prefetch_l2(P.q + static_cast<int64_t>(qbase + lane) * P.ld + xl);
         }
 #endif
         pdl_wait();
@@ -440,18 +446,10 @@ __global__ void __launch_bounds__(256) verify_scan_kernel(const RaceParams P) {
     }
     zero_step_counts(P.step_counts);
     if (P.alpha_ready && blockIdx.x == 0 && threadIdx.x == 0) *P.alpha_ready = 0u;  // alpha of this call: pending
-    if (ok && lane < k) {
-        bad = x < 0 || x >= P.vocab_global;
-        const int32_t xl = x - P.vocab_offset;
-        own = !bad && xl >= 0 && xl < P.vocab;
-        if (own) {
-            const uint4 rr = philox4x32_10(0u, (kPurposeAccept << 16) | static_cast<uint32_t>(lane), rid, P.step,
-                                           P.k0, P.k1);
-            const float u = u_acc_from_word(rr.x);
-            const float qx = P.q ? P.q[static_cast<int64_t>(qbase + lane) * P.ld + xl] : 1.0f;
-            const float px = P.p[static_cast<int64_t>(r0 + lane) * P.ld + xl];
-            acc = __fmul_rn(u, qx) < px;  // strict; NaN rejects
-        }
+    if (own) {
+        const float qx = P.q ? P.q[static_cast<int64_t>(qbase + lane) * P.ld + xl] : 1.0f;
+        const float px = P.p[static_cast<int64_t>(r0 + lane) * P.ld + xl];
+        acc = __fmul_rn(u, qx) < px;  // strict; NaN rejects
     }
     const uint32_t badm = __ballot_sync(0xFFFFFFFFu, bad);
     const uint32_t accm = __ballot_sync(0xFFFFFFFFu, acc);
