@@ -23,8 +23,22 @@ namespace tsv {
 #define TSV_GP_CHOOSE_THREADS 256
 #endif
 constexpr int kGpChooseThreads = TSV_GP_CHOOSE_THREADS;  // B = 256 step: 256 threads 2.84 us; 128: 3.12; 64: 3.86; 32: 6.10
+// Before the grid-dependency wait: prefetch the context lengths (a step input that may have left L2 since
+// it was last read) and alpha into L2, so the loads after the wait are L2 hits.  A prefetch returns no
+// data and L2 is the coherence point for writes, so this is safe whatever is still in flight.
+#ifndef TSV_GP_PREFETCH
+#define TSV_GP_PREFETCH 1
+#endif
+__device__ __forceinline__ void gp_prefetch(const ChooseArgs& A) {
+    if (!TSV_GP_PREFETCH) return;
+    const int32_t line = static_cast<int32_t>(threadIdx.x) * 32;  // one 128-byte line of ctx_len per thread
+    if (line < A.B) prefetch_l2(A.ctx_len + line);
+    if (threadIdx.x == 0) prefetch_l2(A.alpha);
+}
+
 __global__ void __launch_bounds__(kGpChooseThreads) goodput_choose_k_kernel(const ChooseArgs A) {
     TSV_STEP_SPAN(1);
+    gp_prefetch(A);
     pdl_wait();
     TSV_STEP_WAITED();
     pdl_launch_dependents();
@@ -57,6 +71,7 @@ __global__ void __launch_bounds__(kGpChooseThreads) goodput_choose_k_p2p_kernel(
                                                                               int32_t* devstatus) {
     __shared__ long long s_sums[2 * kGpMaxK + 4];
     __shared__ int s_best;
+    gp_prefetch(A);
     pdl_wait();
     pdl_launch_dependents();
     int32_t caps[kGpCapCache];
