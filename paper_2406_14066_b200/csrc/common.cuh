@@ -224,13 +224,25 @@ __device__ __forceinline__ float race_F(uint32_t x) {
     return __uint_as_float(b);
 }
 
+// Warp-wide max of a u64 (all lanes): the max high word by one REDUX, then the max low word among the
+// lanes holding it by a second -- the same value as the lexicographic max, in two reductions instead of
+// five rounds of 64-bit shuffles.
+#ifndef TSV_WARP_MAX_REDUX
+#define TSV_WARP_MAX_REDUX 1
+#endif
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+    if (!TSV_WARP_MAX_REDUX) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t t = __shfl_xor_sync(0xFFFFFFFFu, v, o);
-        v = t > v ? t : v;
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t t = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+            v = t > v ? t : v;
+        }
+        return v;
     }
-    return v;
+    const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+    const uint32_t mhi = __reduce_max_sync(0xFFFFFFFFu, hi);
+    const uint32_t mlo = __reduce_max_sync(0xFFFFFFFFu, hi == mhi ? lo : 0u);
+    return (static_cast<uint64_t>(mhi) << 32) | mlo;
 }
 
 __device__ __forceinline__ float4 ldg_stream(const float4* p) {
