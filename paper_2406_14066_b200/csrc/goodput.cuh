@@ -111,6 +111,80 @@ constexpr int kGpCapCache = 4;  // caps kept in registers for k_i = min(k*, cap_
 #ifndef TSV_GP_HISTOGRAM
 #define TSV_GP_HISTOGRAM 1
 #endif
+// The histogram's batch sums (one warp, lane j holding n_j for j <= k_max): fix_j = rint(2^32 l(alpha, j))
+// by the Horner recurrence from 1.0 (j steps), then lane k: L[k] = sum_{j<k} n_j fix_j + (sum_{j>=k} n_j)
+// fix_k and N[k] = sum_j n_j min(k, j).
+__device__ __forceinline__ void gp_hist_tail(GpTotals& t, long long nj, double a, int32_t k_max, int lane) {
+    double l = 1.0;
+    for (int s = 0; s < lane && s < k_max; ++s) l = __fma_rn(a, l, 1.0);
+    const long long fix_j = __double2ll_rn(l * 0x1p32);
+    long long Lk = 0, Nk = 0, tail = 0;
+    for (int j = 0; j <= k_max; ++j) {
+        const long long n_ = __shfl_sync(0xFFFFFFFFu, nj, j);
+        const long long f_ = __shfl_sync(0xFFFFFFFFu, fix_j, j);
+        if (j < lane) {
+            Lk += n_ * f_;
+            Nk += n_ * j;
+        } else {
+            tail += n_;
+        }
+    }
+    if (lane <= k_max) {
+        t.L = Lk + tail * fix_j;
+        t.N = Nk + tail * lane;
+    }
+}
+
+// The same sums from ONE warp (global alpha): no shared memory, no barrier.  Lane l takes requests l,
+// l + 32, ...; its bin counts are 8-bit fields of two 64-bit words (<= 255 requests per lane: B <= 8160),
+// summed over the warp one bin per REDUX; the context sums are exact int64 warp sums.  Identical integers
+// to gp_sums_block_hist (integer addition is exact and order-free), so identical k* and goodput bits.
+constexpr int kGpWarpMaxB = 32 * 255;
+constexpr int kGpWarpCaps = 8;  // caps kept in registers for k_i = min(k*, cap_i)
+__device__ __forceinline__ GpTotals gp_sums_warp(const ChooseArgs& A, int32_t (&cap_cache)[kGpWarpCaps]) {
+    const int lane = threadIdx.x & 31;
+    const int32_t B = A.B, k_max = A.k_max;
+    const double a = __ldcg(A.alpha);  // every lane (broadcast): the Horner recurrence is per lane
+    long long n_ctx = 0, n_ctx_spec = 0;
+    uint32_t b_spec = 0;
+    unsigned long long f_lo = 0ull, f_hi = 0ull;  // bins 0-7 / 8-15, 8 bits each
+    auto take = [&](int32_t ci, int32_t cl) {
+        n_ctx += cl;
+        if (ci > 0) {
+            n_ctx_spec += cl;
+            b_spec += 1;
+        }
+        const int32_t j = ci < 0 ? 0 : (ci > k_max ? k_max : ci);
+        if (j < 8) f_lo += 1ull << (8 * j);
+        else f_hi += 1ull << (8 * (j - 8));
+    };
+    // the first 32 kGpWarpCaps requests: every load issued before any is used (one round trip)
+    int32_t cls[kGpWarpCaps];
+#pragma unroll
+    for (int r = 0; r < kGpWarpCaps; ++r) {
+        const int32_t i = r * 32 + lane;
+        cap_cache[r] = i < B ? __ldcg(A.cap + i) : 0;
+        cls[r] = i < B ? __ldcg(A.ctx_len + i) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kGpWarpCaps; ++r)
+        if (r * 32 + lane < B) take(cap_cache[r], cls[r]);
+    for (int32_t i = kGpWarpCaps * 32 + lane; i < B; i += 32) take(__ldcg(A.cap + i), __ldcg(A.ctx_len + i));
+    long long nj = 0;  // lane j: n_j
+#pragma unroll
+    for (int b = 0; b < kGpMaxK; ++b) {
+        if (b <= k_max) {
+            const uint32_t field = static_cast<uint32_t>(((b < 8 ? f_lo : f_hi) >> (8 * (b & 7))) & 0xFFull);
+            const uint32_t h = __reduce_add_sync(0xFFFFFFFFu, field);
+            if (lane == b) nj = h;
+        }
+    }
+    GpTotals t = {0, 0, warp_sum_i64(n_ctx), warp_sum_i64(n_ctx_spec),
+                  static_cast<long long>(__reduce_add_sync(0xFFFFFFFFu, b_spec)), static_cast<long long>(B)};
+    gp_hist_tail(t, nj, a, k_max, lane);
+    return t;
+}
+
 template <int NT>
 __device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int32_t* cap_cache) {
     constexpr int NW = NT / 32;
@@ -166,26 +240,7 @@ __device__ __forceinline__ GpTotals gp_sums_block_hist(const ChooseArgs& A, int3
             t.c1 += sC[w][1];
             t.c2 += sC[w][2];
         }
-        // lane j: fix_j = rint(2^32 l(alpha, j)), l by the Horner recurrence from 1.0, j steps
-        double l = 1.0;
-        for (int s = 0; s < lane && s < k_max; ++s) l = __fma_rn(a, l, 1.0);
-        const long long fix_j = __double2ll_rn(l * 0x1p32);
-        // lane k: L[k] = sum_{j<k} n_j fix_j + (sum_{j>=k} n_j) fix_k;  N[k] = sum_j n_j min(k, j)
-        long long Lk = 0, Nk = 0, tail = 0;
-        for (int j = 0; j <= k_max; ++j) {
-            const long long n_ = __shfl_sync(0xFFFFFFFFu, nj, j);
-            const long long f_ = __shfl_sync(0xFFFFFFFFu, fix_j, j);
-            if (j < lane) {
-                Lk += n_ * f_;
-                Nk += n_ * j;
-            } else {
-                tail += n_;
-            }
-        }
-        if (lane <= k_max) {
-            t.L = Lk + tail * fix_j;
-            t.N = Nk + tail * lane;
-        }
+        gp_hist_tail(t, nj, a, k_max, lane);
     }
     return t;
 }
@@ -323,8 +378,45 @@ __device__ __forceinline__ void gp_write_k_per_request(const ChooseArgs& A, int 
 
 // ArgMaxGoodput over one CTA of kGpThreads threads (all threads must call).  Inputs are read
 // with ld.global.cg so values written by other CTAs of a fused kernel are seen.
+// ArgMaxGoodput by warp 0 alone (global alpha, B <= kGpWarpMaxB; the other warps return): the batch sums,
+// Listing 2 and k_i = min(k*, cap_i), with no shared memory or barrier on the chain.  Used for one-warp CTAs
+// and small batches (choose_k_block).
+#ifndef TSV_GP_WARP
+#define TSV_GP_WARP 1
+#endif
+__device__ __forceinline__ bool choose_k_warp_ok(const ChooseArgs& A) {
+    return TSV_GP_WARP && TSV_GP_HISTOGRAM && !A.alpha_per_request && A.B <= kGpWarpMaxB;
+}
+__device__ __forceinline__ void choose_k_warp(const ChooseArgs& A) {
+    int32_t caps[kGpWarpCaps];
+    const GpTotals t = gp_sums_warp(A, caps);
+    const int kb = gp_argmax_warp(A, t);
+    if (A.k_per_request) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int r = 0; r < kGpWarpCaps; ++r) {
+            const int32_t i = r * 32 + lane;
+            if (i < A.B) {
+                const int32_t ki = kb < caps[r] ? kb : caps[r];
+                A.k_per_request[i] = ki < 0 ? 0 : ki;
+            }
+        }
+        for (int32_t i = kGpWarpCaps * 32 + lane; i < A.B; i += 32) {
+            const int32_t ci = __ldcg(A.cap + i);
+            const int32_t ki = kb < ci ? kb : ci;
+            A.k_per_request[i] = ki < 0 ? 0 : ki;
+        }
+    }
+}
+
 template <int NT = kGpThreads>
 __device__ __forceinline__ void choose_k_block(const ChooseArgs& A) {
+    // one warp when the CTA is one warp anyway (the batched kernel: config 5 7.9 vs 9.6 us) or the batch is
+    // small; for B = 256 on 256 threads the eight warps' parallel loads and sums win (21.1 vs 21.45 us step)
+    if (choose_k_warp_ok(A) && (NT == 32 || A.B <= 64)) {
+        if ((threadIdx.x >> 5) == 0) choose_k_warp(A);
+        return;
+    }
     __shared__ int s_best;
     int32_t caps[kGpCapCache];
     const GpTotals t = gp_sums_block<NT>(A, caps);
