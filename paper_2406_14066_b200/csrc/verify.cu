@@ -730,10 +730,9 @@ __global__ void __launch_bounds__(kRaceThreads, TSV_RACE_MINB) verify_race_kerne
         R.init();
         {
             // Full steps with explicit pointer / counter increments: kUnroll float4 of p (and of q on a
-            // rejection) per lane per step, the Philox quad counter advancing by 32 per float4.  q is only
-            // loaded (and only subtracted) when use_q, and nothing else is kept live for the tail loop.
-            // rem (columns left in the chunk) is the loop counter and the tail's bound: nothing else about the
-            // chunk stays live across the streaming loop
+            // rejection) per lane per step, the Philox quad counter advancing by 32 per float4.  rem (columns
+            // left in the chunk) is the loop counter and the masked tail's bound: nothing else about the chunk
+            // stays live across the streaming loop (the last table)
             int32_t rem = col_end - col_begin;
             const float4* pp = prow + lane;
             const float4* qp = qrow + lane;
