@@ -13,9 +13,8 @@ whose footprint is > 3x L2 so no step reads another's rows from L2.
 Metric: generated (verified) tokens/s = sum_i (m_i + 1) / time, whole job.
 Roofline: the dominant kernel (verify_race_kernel) timed alone -- at least 64 race-only launches per
 graph (TSV_VERIFY_RACE_ONLY) over per-step workspaces, at least 4 replays whatever K -- against its
-algorithmic bytes (the rows the
-steps actually select) and MEASURED_PEAKS.json's HBM copy bandwidth; the whole verify call is
-reported beside it.  e2e: the same ABI calls with the inputs in pinned host memory.
+algorithmic bytes (the rows the steps actually select) and MEASURED_PEAKS.json's HBM copy bandwidth;
+the whole verify call is reported beside it.  e2e: the same ABI calls with the inputs in pinned host memory.
 Timing: W untimed warm-up steps, then exactly K steps (CUDA-graph replays of up to 64 steps) between
 CUDA events on the launching stream, bracketed by a barrier + synchronize; a ~50 us spin kernel
 enqueued just before the start event keeps the device busy while the host submits the first replay,
